@@ -1,0 +1,263 @@
+"""ctypes wrapper of the fp64 CPU oracle (oracle/msa_oracle.c).
+
+TEST INFRASTRUCTURE ONLY. Only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` legs may import this package. The product
+package (paper_2510_16154_b200) never imports it and shares no code with it.
+
+Parity status: every function here is pinned by tests/test_oracle_pins.py
+ except the composite agent+TV trajectory, which is
+"parity unpinned" beyond the invariants P8 (mean) and P9 (constant fixed point)
+(DESIGN.md §3).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass, asdict
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "libmsa_oracle.so")
+_lib = None
+
+NSTAT_FIXED = 8
+STAT_NAMES = ["E_TV", "E_fid", "P", "D", "gap", "residual", "rho", "nonfinite"]
+
+
+def build(force: bool = False) -> str:
+    src = os.path.join(_HERE, "msa_oracle.c")
+    hdr = os.path.join(_HERE, "msa_oracle.h")
+    newest = max(os.path.getmtime(src), os.path.getmtime(hdr))
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < newest:
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-D_GNU_SOURCE", "-ffp-contract=off", "-fopenmp", "-fPIC",
+                               "-shared", "-o", _LIB_PATH, src, "-lm"])
+    return _LIB_PATH
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("height", ctypes.c_int32), ("width", ctypes.c_int32), ("channels", ctypes.c_int32),
+                ("radius", ctypes.c_int32), ("kernel", ctypes.c_int32), ("iters_per_round", ctypes.c_int32),
+                ("rounds", ctypes.c_int32), ("pad_", ctypes.c_int32)] + [
+        (n, ctypes.c_double) for n in ("hx", "hy", "alpha", "beta", "eps_x", "eps_c", "dt", "rho", "gamma",
+                                       "kappa", "tau", "sigma", "theta")]
+
+
+@dataclass
+class Params:
+    height: int
+    width: int
+    channels: int
+    radius: int = 2
+    kernel: int = 0
+    iters_per_round: int = 1
+    rounds: int = 1
+    hx: float = 0.0
+    hy: float = 0.0
+    alpha: float = 1.0
+    beta: float = 1.0
+    eps_x: float = 0.0
+    eps_c: float = 57.0
+    dt: float = 0.25
+    rho: float = 1.0
+    gamma: float = 1.0
+    kappa: float = 1.0
+    tau: float = 0.0
+    sigma: float = 0.0
+    theta: float = 1.0
+
+    def c(self) -> _Params:
+        d = asdict(self)
+        return _Params(**{k: d[k] for k in ("height", "width", "channels", "radius", "kernel", "iters_per_round",
+                                            "rounds")}, pad_=0,
+                       **{k: float(d[k]) for k in ("hx", "hy", "alpha", "beta", "eps_x", "eps_c", "dt", "rho",
+                                                   "gamma", "kappa", "tau", "sigma", "theta")})
+
+    @staticmethod
+    def from_solver(H: int, W: int, C: int, sp: dict) -> "Params":
+        return Params(height=H, width=W, channels=C, radius=sp["radius"], kernel=sp["kernel"],
+                      iters_per_round=sp["iters_per_round"], rounds=sp["rounds"], alpha=sp["alpha"],
+                      beta=sp["beta"], eps_x=sp["eps_x"], eps_c=sp["eps_c"], dt=sp["dt"], rho=sp["rho"],
+                      gamma=sp["gamma"], kappa=sp["kappa"], tau=sp["tau"], sigma=sp["sigma"], theta=sp["theta"])
+
+
+_D = ctypes.c_void_p
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB_PATH)
+        P = ctypes.POINTER(_Params)
+        sig = {
+            "mo_derive": ([P, P], ctypes.c_int),
+            "mo_phi": ([ctypes.c_double, ctypes.c_int], ctypes.c_double),
+            "mo_pair_r": ([ctypes.c_double] * 5, ctypes.c_double),
+            "mo_window_size": ([ctypes.c_int], ctypes.c_int),
+            "mo_grad": ([_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double], None),
+            "mo_div": ([_D, _D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_double, ctypes.c_double], None),
+            "mo_agent_rhs": ([P, _D, _D], None),
+            "mo_init_state": ([P, _D, _D, _D, _D, _D], None),
+            "mo_iteration": ([P, ctypes.c_double, _D, _D, _D, _D, _D], None),
+            "mo_round_stats": ([P, ctypes.c_double, _D, _D, _D, _D, _D], None),
+            "mo_round_update": ([P, ctypes.c_double, _D, _D], None),
+            "mo_run": ([P, _D, _D, _D, _D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _D,
+                        ctypes.c_int32], ctypes.c_int),
+            "mo_energy_K": ([P, _D, _D], ctypes.c_double),
+            "mo_energy_L": ([P, ctypes.c_double, _D, _D, _D, _D], ctypes.c_double),
+            "mo_energy_Ltilde": ([P, ctypes.c_double, _D, _D, _D, _D], ctypes.c_double),
+            "mo_shrink_field": ([P, ctypes.c_double, _D, _D, _D], None),
+            "mo_labels": ([_D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_float, _D,
+                           ctypes.POINTER(ctypes.c_int32), _D, ctypes.c_int32], ctypes.c_int),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _f64(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data
+
+
+def derive(p: Params) -> Params:
+    out = _Params()
+    if _load().mo_derive(ctypes.byref(p.c()), ctypes.byref(out)) != 0:
+        raise ValueError(f"invalid oracle params {p}")
+    d = {f[0]: getattr(out, f[0]) for f in _Params._fields_ if f[0] != "pad_"}
+    return Params(**d)
+
+
+def phi(r: float, kernel: int = 0) -> float:
+    return _load().mo_phi(r, kernel)
+
+
+def pair_r(dx: float, dy: float, dc2: float, eps_x: float, eps_c: float) -> float:
+    return _load().mo_pair_r(dx, dy, dc2, eps_x, eps_c)
+
+
+def window_size(R: int) -> int:
+    return _load().mo_window_size(R)
+
+
+def grad(u: np.ndarray, hx: float, hy: float) -> np.ndarray:
+    u = _f64(u)
+    H, W, C = u.shape
+    g = np.empty((H, W, 2 * C))
+    _load().mo_grad(_ptr(u), _ptr(g), H, W, C, hx, hy)
+    return g
+
+
+def div(p: np.ndarray, hx: float, hy: float) -> np.ndarray:
+    p = _f64(p)
+    H, W, C2 = p.shape
+    d = np.empty((H, W, C2 // 2))
+    _load().mo_div(_ptr(p), _ptr(d), H, W, C2 // 2, hx, hy)
+    return d
+
+
+def agent_rhs(p: Params, c: np.ndarray) -> np.ndarray:
+    c = _f64(c)
+    assert c.shape == (p.height, p.width, p.channels), "field shape must match the params"
+    F = np.empty_like(c)
+    _load().mo_agent_rhs(ctypes.byref(derive(p).c()), _ptr(c), _ptr(F))
+    return F
+
+
+class State:
+    """Oracle state of one image: c, cbar [H][W][C]; p, mu [H][W][2C]; rho; global iteration."""
+
+    def __init__(self, p: Params, I: np.ndarray):
+        self.params = p
+        self.I = _f64(I)
+        H, W, C = self.I.shape
+        assert (H, W, C) == (p.height, p.width, p.channels)
+        self.c = np.empty_like(self.I)
+        self.cbar = np.empty_like(self.I)
+        self.p = np.empty((H, W, 2 * C))
+        self.mu = np.empty((H, W, 2 * C))
+        _load().mo_init_state(ctypes.byref(p.c()), _ptr(self.I), _ptr(self.c), _ptr(self.cbar), _ptr(self.p),
+                              _ptr(self.mu))
+        self.rho = float(p.rho)
+        self.iter = 0
+        self.stats: list[np.ndarray] = []
+
+    def run(self, n_iters: int) -> list[np.ndarray]:
+        C = self.params.channels
+        cap = n_iters // max(self.params.iters_per_round, 1) + 2
+        st = np.zeros((cap, NSTAT_FIXED + C))
+        rho = ctypes.c_double(self.rho)
+        nr = _load().mo_run(ctypes.byref(self.params.c()), _ptr(self.I), _ptr(self.c), _ptr(self.cbar),
+                            _ptr(self.p), _ptr(self.mu), self.iter, n_iters, ctypes.byref(rho), _ptr(st), cap)
+        if nr < 0:
+            raise ValueError("oracle rejected params")
+        self.rho = rho.value
+        self.iter += n_iters
+        new = [st[r].copy() for r in range(nr)]
+        self.stats.extend(new)
+        return new
+
+    def iteration(self) -> None:
+        """One iteration (steps 1-3) without any round logic."""
+        _load().mo_iteration(ctypes.byref(derive(self.params).c()), self.rho, _ptr(self.I), _ptr(self.c),
+                             _ptr(self.cbar), _ptr(self.p), _ptr(self.mu))
+
+    def round_stats(self) -> np.ndarray:
+        C = self.params.channels
+        st = np.zeros(NSTAT_FIXED + C)
+        _load().mo_round_stats(ctypes.byref(derive(self.params).c()), self.rho, _ptr(self.I), _ptr(self.c),
+                               _ptr(self.p), _ptr(self.mu), _ptr(st))
+        return st
+
+    def round_update(self) -> None:
+        _load().mo_round_update(ctypes.byref(derive(self.params).c()), self.rho, _ptr(self.c), _ptr(self.mu))
+
+
+def solve(p: Params, I: np.ndarray) -> State:
+    """rounds x K iterations from the initial state (SURVEY.md §8(c) oracle block)."""
+    s = State(p, I)
+    s.run(p.rounds * p.iters_per_round)
+    return s
+
+
+def energy_K(p: Params, u, I) -> float:
+    u, I = _f64(u), _f64(I)
+    return _load().mo_energy_K(ctypes.byref(p.c()), _ptr(u), _ptr(I))
+
+
+def energy_L(p: Params, rho: float, u, v, mu, I) -> float:
+    u, v, mu, I = _f64(u), _f64(v), _f64(mu), _f64(I)
+    return _load().mo_energy_L(ctypes.byref(p.c()), rho, _ptr(u), _ptr(v), _ptr(mu), _ptr(I))
+
+
+def energy_Ltilde(p: Params, rho: float, u, v, mu, I) -> float:
+    u, v, mu, I = _f64(u), _f64(v), _f64(mu), _f64(I)
+    return _load().mo_energy_Ltilde(ctypes.byref(p.c()), rho, _ptr(u), _ptr(v), _ptr(mu), _ptr(I))
+
+
+def shrink_field(p: Params, rho: float, c, mu) -> np.ndarray:
+    c, mu = _f64(c), _f64(mu)
+    v = np.empty_like(mu)
+    _load().mo_shrink_field(ctypes.byref(derive(p).c()), rho, _ptr(c), _ptr(mu), _ptr(v))
+    return v
+
+
+def labels(c: np.ndarray, delta: float = 0.1, max_k: int = 0):
+    """Q(c; delta) of reading R16 on a float32 [H][W][C] field -> (labels int32 [H][W], count, palette)."""
+    c = np.ascontiguousarray(c, dtype=np.float32)
+    H, W, C = c.shape
+    lab = np.empty((H, W), dtype=np.int32)
+    n = ctypes.c_int32(0)
+    pal = np.zeros((max(max_k, 1), C), dtype=np.float32)
+    rc = _load().mo_labels(_ptr(c), H, W, C, ctypes.c_float(delta), _ptr(lab), ctypes.byref(n), _ptr(pal), max_k)
+    if rc != 0:
+        raise ValueError("labels: non-finite or out-of-range field")
+    return lab, n.value, pal[:min(max_k, n.value)] if max_k > 0 else None

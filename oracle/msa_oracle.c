@@ -1,0 +1,509 @@
+/*
+ * msa_oracle.c - plain, slow, fp64 CPU oracle of the msa hot path.
+ *
+ * TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs are the only callers. Nothing under
+ * paper_2510_16154_b200/ includes, links or executes this file, and it shares
+ * no code with the CUDA path.
+ *
+ * It follows the oracle block of SURVEY.md §8(c) step by step, in the paper's
+ * notation and order, one pixel loop per step, no fusion or reordering:
+ *   step 1  agent Euler step          eq:MAsystem PAPER.md:86-95, eq:ellipsoid :97-102,
+ *                                     eq:kernel :259-267, explicit Euler :270
+ *                                     (windowed sum with 1/N_R: reading R2)
+ *   step 2  dual ascent + projection  eq:complete_square :397-404, eq:soft_threshold :431-440
+ *                                     (Chambolle-Pock dual step with v eliminated: reading R7)
+ *   step 3  divergence, prox fidelity, extrapolation   eq:new_adjoint :405-413 (R7, R21)
+ *   step 4  multiplier round          Alg. 2 lines 6-7; ascent :442
+ *   step 5  round statistics          eq:cost_TV :346-350, eq:complete_square, stopping :444
+ *   step 7  labels                    reading R16 (clusters in colour space)
+ * Readings R1-R27 are listed in DESIGN.md §2.
+ *
+ * Pixel loops are parallel over rows with OpenMP; every pixel's arithmetic is
+ * in a fixed order, so results do not depend on the thread count.
+ */
+#include "msa_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define IDX(j, i) ((size_t)(j) * (size_t)W + (size_t)(i))
+
+/* ---------------------------------------------------------------- params */
+
+/* Fills the documented defaults (SURVEY.md §8(b) params struct, §8(c) "derive"). */
+int mo_derive(const mo_params* in, mo_params* out) {
+  *out = *in;
+  if (in->height < 1 || in->width < 1 || in->channels < 1 || in->radius < 0) return -1;
+  if (in->alpha < 0 || in->beta < 0 || in->rho <= 0 || in->gamma <= 0 || in->dt < 0 || in->kappa <= 0) return -1;
+  if (in->iters_per_round < 1 || in->rounds < 0) return -1;
+  if (out->hx <= 0) out->hx = in->width > 1 ? 1.0 / (double)(in->width - 1) : 1.0;   /* R5 */
+  if (out->hy <= 0) out->hy = in->height > 1 ? 1.0 / (double)(in->height - 1) : 1.0;
+  if (out->eps_x <= 0) {                                                              /* R2 */
+    double h = out->hx < out->hy ? out->hx : out->hy;
+    double Rh = (in->radius > 0 ? in->radius : 1) * h;
+    out->eps_x = 2.0 / (Rh * Rh);
+  }
+  double L = sqrt(4.0 / (out->hx * out->hx) + 4.0 / (out->hy * out->hy));            /* ||grad|| <= L */
+  if (out->tau <= 0) out->tau = 0.99 / L;                                             /* R7 */
+  if (out->sigma <= 0) out->sigma = 0.99 / L;
+  if (out->theta < 0) out->theta = 1.0;
+  if (out->eps_c < 0) return -1;
+  return 0;
+}
+
+/* ------------------------------------------------------ kernel, distance */
+
+/* eq:kernel. The printed form (4r-1)(1-r)^4 is negative near
+ * r = 0 (repulsion), contradicting the cited Wendland C^2 function; the default
+ * is the standard (4r+1)(1-r)^4 (reading R3). Zero outside [0,1]. */
+double mo_phi(double r, int kernel) {
+  if (r < 0.0 || r > 1.0) return 0.0;
+  double om = 1.0 - r;
+  double om4 = om * om * om * om;
+  return kernel == 1 ? (4.0 * r - 1.0) * om4 : (4.0 * r + 1.0) * om4;
+}
+
+/* eq:ellipsoid: r = eps_x/2 [(x_j-x_i)^2 + (y_j-y_i)^2] + eps_c/2 (c_j-c_i)^2,
+ * with (c_j-c_i)^2 read as the squared Euclidean colour distance (reading R4a). */
+double mo_pair_r(double dx_omega, double dy_omega, double dc2, double eps_x, double eps_c) {
+  return 0.5 * eps_x * (dx_omega * dx_omega + dy_omega * dy_omega) + 0.5 * eps_c * dc2;
+}
+
+/* N_R = |D_R| (reading R2) */
+int mo_window_size(int R) {
+  int n = 0;
+  for (int dy = -R; dy <= R; ++dy)
+    for (int dx = -R; dx <= R; ++dx)
+      if (dx * dx + dy * dy <= R * R) ++n;
+  return n;
+}
+
+/* ------------------------------------------------------ grad, div (R6) */
+
+/* Forward differences, zero on the last column / row (Neumann, reading R6). */
+void mo_grad(const double* u, double* g, int H, int W, int C, double hx, double hy) {
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < H; ++j)
+    for (int i = 0; i < W; ++i)
+      for (int k = 0; k < C; ++k) {
+        double gx = 0.0, gy = 0.0;
+        if (i < W - 1) gx = (u[IDX(j, i + 1) * C + k] - u[IDX(j, i) * C + k]) / hx;
+        if (j < H - 1) gy = (u[IDX(j + 1, i) * C + k] - u[IDX(j, i) * C + k]) / hy;
+        g[IDX(j, i) * 2 * C + k] = gx;
+        g[IDX(j, i) * 2 * C + C + k] = gy;
+      }
+}
+
+/* Divergence = exact negative adjoint of mo_grad (reading R6):
+ * (div p)(i,j) = (p_x(i,j)[i<W-1] - p_x(i-1,j)[i>0])/hx + (p_y(i,j)[j<H-1] - p_y(i,j-1)[j>0])/hy. */
+void mo_div(const double* p, double* d, int H, int W, int C, double hx, double hy) {
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < H; ++j)
+    for (int i = 0; i < W; ++i)
+      for (int k = 0; k < C; ++k) {
+        double ax = 0.0, ay = 0.0;
+        if (i < W - 1) ax += p[IDX(j, i) * 2 * C + k];
+        if (i > 0) ax -= p[IDX(j, i - 1) * 2 * C + k];
+        if (j < H - 1) ay += p[IDX(j, i) * 2 * C + C + k];
+        if (j > 0) ay -= p[IDX(j - 1, i) * 2 * C + C + k];
+        d[IDX(j, i) * C + k] = ax / hx + ay / hy;
+      }
+}
+
+/* ---------------------------------------------------------- step 1 (F) */
+
+/* F(n) = (1/N_R) sum_{delta in D_R, n+delta inside} phi(r(n,delta)) (c(n+delta) - c(n)).
+ * eq:MAsystem restricted to the disc D_R with constant normalisation
+ * N_R (reading R2); out-of-image neighbours are excluded, not padded (R20);
+ * the weight phi is shared by all channels (R4b). prm must be derived. */
+void mo_agent_rhs(const mo_params* prm, const double* c, double* F) {
+  const int H = prm->height, W = prm->width, C = prm->channels, R = prm->radius;
+  const double NR = (double)mo_window_size(R);
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < H; ++j)
+    for (int i = 0; i < W; ++i) {
+      double acc[64];
+      for (int k = 0; k < C; ++k) acc[k] = 0.0;
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx) {
+          if (dx * dx + dy * dy > R * R) continue;
+          int ii = i + dx, jj = j + dy;
+          if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;
+          double dc2 = 0.0;
+          for (int k = 0; k < C; ++k) {
+            double d = c[IDX(jj, ii) * C + k] - c[IDX(j, i) * C + k];
+            dc2 += d * d;
+          }
+          double r = mo_pair_r(dx * prm->hx, dy * prm->hy, dc2, prm->eps_x, prm->eps_c);
+          double w = mo_phi(r, prm->kernel);
+          for (int k = 0; k < C; ++k) acc[k] += w * (c[IDX(jj, ii) * C + k] - c[IDX(j, i) * C + k]);
+        }
+      for (int k = 0; k < C; ++k) F[IDX(j, i) * C + k] = acc[k] / NR;
+    }
+}
+
+/* ------------------------------------------------------------ state */
+
+/* Step 0: c = cbar = I, p = mu = 0 (Alg. 2 REQUIRE PAPER.md:450; c(0) = I PAPER.md:93; R10). */
+void mo_init_state(const mo_params* prm, const double* I, double* c, double* cbar, double* p, double* mu) {
+  size_t n = (size_t)prm->height * prm->width * prm->channels;
+  memcpy(c, I, n * sizeof(double));
+  memcpy(cbar, I, n * sizeof(double));
+  memset(p, 0, 2 * n * sizeof(double));
+  memset(mu, 0, 2 * n * sizeof(double));
+}
+
+/* Pi_beta(q) = q min(1, beta/|q|) over the whole 2C-vector (coupled TV, R4c). */
+static void project_ball(double* q, int n2, double beta) {
+  double s = 0.0;
+  for (int m = 0; m < n2; ++m) s += q[m] * q[m];
+  double nq = sqrt(s);
+  if (nq > beta) {
+    double f = beta / nq;
+    for (int m = 0; m < n2; ++m) q[m] *= f;
+  }
+}
+
+/* One solver iteration, steps 1-3 (SURVEY.md §8(c) oracle block). In place on
+ * c, cbar, p; mu is read only. prm must be derived. */
+void mo_iteration(const mo_params* prm, double rho, const double* I, double* c, double* cbar, double* p,
+                  const double* mu) {
+  const int H = prm->height, W = prm->width, C = prm->channels;
+  const size_t n1 = (size_t)H * W * C, n2 = 2 * n1;
+  const double dt = prm->dt, tau = prm->tau, sigma = prm->sigma, alpha = prm->alpha, theta = prm->theta;
+  double* F = (double*)malloc(n1 * sizeof(double));
+  double* chalf = (double*)malloc(n1 * sizeof(double));
+  double* g = (double*)malloc(n2 * sizeof(double));
+  double* d = (double*)malloc(n1 * sizeof(double));
+  /* step 1: c_half = c + dt F(c)  (explicit Euler) */
+  mo_agent_rhs(prm, c, F);
+  for (size_t q = 0; q < n1; ++q) chalf[q] = c[q] + dt * F[q];
+  /* step 2: p+ = Pi_beta( (rho (p + sigma grad cbar) - sigma mu) / (rho + sigma) )  (R7) */
+  mo_grad(cbar, g, H, W, C, prm->hx, prm->hy);
+#pragma omp parallel for schedule(static)
+  for (long long n = 0; n < (long long)H * W; ++n) {
+    double q[128];
+    for (int m = 0; m < 2 * C; ++m) {
+      size_t e = (size_t)n * 2 * C + m;
+      q[m] = (rho * (p[e] + sigma * g[e]) - sigma * mu[e]) / (rho + sigma);
+    }
+    project_ball(q, 2 * C, prm->beta);
+    for (int m = 0; m < 2 * C; ++m) p[(size_t)n * 2 * C + m] = q[m];
+  }
+  /* step 3: c+ = c_half + (tau div p+ + tau alpha (I - c_half)) / (1 + tau alpha)  (prox of the
+   * fidelity term, increment form R21); cbar+ = c+ + theta (c+ - c_half) */
+  mo_div(p, d, H, W, C, prm->hx, prm->hy);
+  for (size_t q = 0; q < n1; ++q) {
+    double cp = chalf[q] + (tau * d[q] + tau * alpha * (I[q] - chalf[q])) / (1.0 + tau * alpha);
+    cbar[q] = cp + theta * (cp - chalf[q]);
+    c[q] = cp;
+  }
+  free(F); free(chalf); free(g); free(d);
+}
+
+/* v = S_{beta/rho}(grad c - mu/rho), S_t(a) = max(0, 1 - t/|a|) a  (eq:soft_threshold,
+ * PAPER.md:431-440, with threshold beta/rho for TV weight beta, R27). */
+void mo_shrink_field(const mo_params* prm, double rho, const double* c, const double* mu, double* v) {
+  const int H = prm->height, W = prm->width, C = prm->channels;
+  double* g = (double*)malloc((size_t)H * W * 2 * C * sizeof(double));
+  mo_grad(c, g, H, W, C, prm->hx, prm->hy);
+  const double t = prm->beta / rho;
+  for (size_t n = 0; n < (size_t)H * W; ++n) {
+    double a[128], s = 0.0;
+    for (int m = 0; m < 2 * C; ++m) {
+      a[m] = g[n * 2 * C + m] - mu[n * 2 * C + m] / rho;
+      s += a[m] * a[m];
+    }
+    double na = sqrt(s);
+    double f = na > t ? 1.0 - t / na : 0.0;
+    for (int m = 0; m < 2 * C; ++m) v[n * 2 * C + m] = f * a[m];
+  }
+  free(g);
+}
+
+/* Step 5: round statistics with the round's pre-update mu.
+ * <.>_w is the rectangular quadrature hx*hy*sum.
+ *   E_TV = <beta |grad c|>, E_fid = alpha/2 ||c - I||^2             (eq:cost_TV)
+ *   P    = <H(grad c - mu/rho)> + E_fid, H the Huber function = min_v of L~   (eq:complete_square)
+ *   D    = -<I, div p> - ||div p||^2/(2 alpha) - <mu,p>/rho - ||p||^2/(2 rho)  (CP dual, R7)
+ *   gap  = P - D >= 0 (weak duality; Thm 4.2 PAPER.md:363-382 is its continuous analogue)
+ *   res  = ||v - grad c||_w, v = S_{beta/rho}(grad c - mu/rho)      (Alg. 2 line 7 direction)
+ * alpha = 0 makes D and gap NaN. */
+void mo_round_stats(const mo_params* prm, double rho, const double* I, const double* c, const double* p,
+                    const double* mu, double* stats) {
+  const int H = prm->height, W = prm->width, C = prm->channels;
+  const size_t npx = (size_t)H * W;
+  const double w = prm->hx * prm->hy, beta = prm->beta, alpha = prm->alpha;
+  double* g = (double*)malloc(npx * 2 * C * sizeof(double));
+  double* v = (double*)malloc(npx * 2 * C * sizeof(double));
+  double* dv = (double*)malloc(npx * C * sizeof(double));
+  mo_grad(c, g, H, W, C, prm->hx, prm->hy);
+  mo_shrink_field(prm, rho, c, mu, v);
+  mo_div(p, dv, H, W, C, prm->hx, prm->hy);
+  double etv = 0, efid = 0, hub = 0, idp = 0, dp2 = 0, mup = 0, pp = 0, res = 0, nonfinite = 0;
+  double mean[64];
+  for (int k = 0; k < C; ++k) mean[k] = 0.0;
+  for (size_t n = 0; n < npx; ++n) {
+    double g2 = 0, a2 = 0;
+    for (int m = 0; m < 2 * C; ++m) {
+      size_t e = n * 2 * C + m;
+      double a = g[e] - mu[e] / rho;
+      g2 += g[e] * g[e];
+      a2 += a * a;
+      mup += mu[e] * p[e];
+      pp += p[e] * p[e];
+      res += (v[e] - g[e]) * (v[e] - g[e]);
+    }
+    etv += beta * sqrt(g2);
+    double na = sqrt(a2);
+    hub += na <= beta / rho ? 0.5 * rho * a2 : beta * na - beta * beta / (2.0 * rho);
+    for (int k = 0; k < C; ++k) {
+      size_t e = n * C + k;
+      double r = c[e] - I[e];
+      efid += r * r;
+      idp += I[e] * dv[e];
+      dp2 += dv[e] * dv[e];
+      mean[k] += c[e];
+      if (!isfinite(c[e])) nonfinite += 1;
+    }
+  }
+  stats[MO_STAT_ETV] = w * etv;
+  stats[MO_STAT_EFID] = 0.5 * alpha * w * efid;
+  stats[MO_STAT_P] = w * hub + stats[MO_STAT_EFID];
+  stats[MO_STAT_D] = alpha > 0 ? -w * idp - w * dp2 / (2.0 * alpha) - w * mup / rho - w * pp / (2.0 * rho) : NAN;
+  stats[MO_STAT_GAP] = stats[MO_STAT_P] - stats[MO_STAT_D];
+  stats[MO_STAT_RES] = sqrt(w * res);
+  stats[MO_STAT_RHO] = rho;
+  stats[MO_STAT_NONFINITE] = nonfinite;
+  for (int k = 0; k < C; ++k) stats[MO_STAT_MEAN0 + k] = mean[k] / (double)npx;
+  free(g); free(v); free(dv);
+}
+
+/* Step 4: mu+ = mu + gamma (v - grad c), v = S_{beta/rho}(grad c - mu/rho)
+ * (Alg. 2 lines 6-7; dual ascent PAPER.md:442). */
+void mo_round_update(const mo_params* prm, double rho, const double* c, double* mu) {
+  const int H = prm->height, W = prm->width, C = prm->channels;
+  const size_t n2 = (size_t)H * W * 2 * C;
+  double* g = (double*)malloc(n2 * sizeof(double));
+  double* v = (double*)malloc(n2 * sizeof(double));
+  mo_grad(c, g, H, W, C, prm->hx, prm->hy);
+  mo_shrink_field(prm, rho, c, mu, v);
+  for (size_t e = 0; e < n2; ++e) mu[e] = mu[e] + prm->gamma * (v[e] - g[e]);
+  free(g); free(v);
+}
+
+/* Runs n_iters iterations starting at global iteration iter0. After every iteration that
+ * completes a round ((iter+1) % K == 0) it records the stats with the pre-update mu, applies
+ * the multiplier update and rho <- kappa rho (R8, R9). Returns the number of rounds recorded
+ * (stats[r * MO_NSTAT(C)]) or -1 on bad params. */
+int mo_run(const mo_params* prm_in, const double* I, double* c, double* cbar, double* p, double* mu,
+           int64_t iter0, int64_t n_iters, double* rho_inout, double* stats, int32_t stats_cap) {
+  mo_params prm;
+  if (mo_derive(prm_in, &prm) != 0) return -1;
+  const int C = prm.channels;
+  double rho = *rho_inout;
+  int nr = 0;
+  for (int64_t it = iter0; it < iter0 + n_iters; ++it) {
+    mo_iteration(&prm, rho, I, c, cbar, p, mu);
+    if ((it + 1) % prm.iters_per_round == 0) {
+      if (stats && nr < stats_cap) mo_round_stats(&prm, rho, I, c, p, mu, stats + (size_t)nr * MO_NSTAT(C));
+      ++nr;
+      mo_round_update(&prm, rho, c, mu);
+      rho = prm.kappa * rho;
+    }
+  }
+  *rho_inout = rho;
+  return nr;
+}
+
+/* -------------------------------------------------------- energies */
+
+/* K(u) = int beta |grad u| + alpha/2 (u - I)^2  (eq:cost_TV) */
+double mo_energy_K(const mo_params* prm_in, const double* u, const double* I) {
+  mo_params prm;
+  mo_derive(prm_in, &prm);
+  const int H = prm.height, W = prm.width, C = prm.channels;
+  double* g = (double*)malloc((size_t)H * W * 2 * C * sizeof(double));
+  mo_grad(u, g, H, W, C, prm.hx, prm.hy);
+  double s = 0;
+  for (size_t n = 0; n < (size_t)H * W; ++n) {
+    double g2 = 0;
+    for (int m = 0; m < 2 * C; ++m) g2 += g[n * 2 * C + m] * g[n * 2 * C + m];
+    s += prm.beta * sqrt(g2);
+    for (int k = 0; k < C; ++k) s += 0.5 * prm.alpha * (u[n * C + k] - I[n * C + k]) * (u[n * C + k] - I[n * C + k]);
+  }
+  free(g);
+  return prm.hx * prm.hy * s;
+}
+
+/* L(u,v,mu) = int beta|v| + mu.(v - grad u) + rho/2 |v - grad u|^2 + alpha/2 (u-I)^2
+ * (eq:cost_tv_regular; TV weight beta, R27) */
+double mo_energy_L(const mo_params* prm_in, double rho, const double* u, const double* v, const double* mu,
+                   const double* I) {
+  mo_params prm;
+  mo_derive(prm_in, &prm);
+  const int H = prm.height, W = prm.width, C = prm.channels;
+  double* g = (double*)malloc((size_t)H * W * 2 * C * sizeof(double));
+  mo_grad(u, g, H, W, C, prm.hx, prm.hy);
+  double s = 0;
+  for (size_t n = 0; n < (size_t)H * W; ++n) {
+    double v2 = 0;
+    for (int m = 0; m < 2 * C; ++m) {
+      size_t e = n * 2 * C + m;
+      v2 += v[e] * v[e];
+      s += mu[e] * (v[e] - g[e]) + 0.5 * rho * (v[e] - g[e]) * (v[e] - g[e]);
+    }
+    s += prm.beta * sqrt(v2);
+    for (int k = 0; k < C; ++k) s += 0.5 * prm.alpha * (u[n * C + k] - I[n * C + k]) * (u[n * C + k] - I[n * C + k]);
+  }
+  free(g);
+  return prm.hx * prm.hy * s;
+}
+
+/* L~(u,v) = int rho/2 |v - grad u + mu/rho|^2 + beta|v| + alpha/2 (u-I)^2
+ * (eq:complete_square) */
+double mo_energy_Ltilde(const mo_params* prm_in, double rho, const double* u, const double* v, const double* mu,
+                        const double* I) {
+  mo_params prm;
+  mo_derive(prm_in, &prm);
+  const int H = prm.height, W = prm.width, C = prm.channels;
+  double* g = (double*)malloc((size_t)H * W * 2 * C * sizeof(double));
+  mo_grad(u, g, H, W, C, prm.hx, prm.hy);
+  double s = 0;
+  for (size_t n = 0; n < (size_t)H * W; ++n) {
+    double v2 = 0, q2 = 0;
+    for (int m = 0; m < 2 * C; ++m) {
+      size_t e = n * 2 * C + m;
+      double q = v[e] - g[e] + mu[e] / rho;
+      q2 += q * q;
+      v2 += v[e] * v[e];
+    }
+    s += 0.5 * rho * q2 + prm.beta * sqrt(v2);
+    for (int k = 0; k < C; ++k) s += 0.5 * prm.alpha * (u[n * C + k] - I[n * C + k]) * (u[n * C + k] - I[n * C + k]);
+  }
+  free(g);
+  return prm.hx * prm.hy * s;
+}
+
+/* ---------------------------------------------------------- labels (R16) */
+
+static int32_t uf_find(int32_t* parent, int32_t x) {
+  while (parent[x] != x) {
+    parent[x] = parent[parent[x]];
+    x = parent[x];
+  }
+  return x;
+}
+/* union by smallest index: a set's root is its smallest member */
+static void uf_union(int32_t* parent, int32_t a, int32_t b) {
+  a = uf_find(parent, a);
+  b = uf_find(parent, b);
+  if (a == b) return;
+  if (a < b) parent[b] = a; else parent[a] = b;
+}
+
+typedef struct { double m0; int32_t seg; } seg_key;
+static int cmp_seg_key(const void* x, const void* y) {
+  const seg_key* a = (const seg_key*)x;
+  const seg_key* b = (const seg_key*)y;
+  if (a->m0 < b->m0) return -1;
+  if (a->m0 > b->m0) return 1;
+  return a->seg < b->seg ? -1 : (a->seg > b->seg);
+}
+
+/* The quantisation rule Q(c; delta) of reading R16 (the paper reads clusters off colour
+ * histograms; SPEC.md:568-576 is its grey-scale 1-D analogue):
+ *  (i)   union 4-neighbours a, b with max_k |c_a,k - c_b,k| <= delta  -> segments
+ *        (differences in fp32, the precision of the field being labelled);
+ *  (ii)  union segments A, B whose means satisfy max_k |m_A,k - m_B,k| <= delta -> clusters;
+ *        means are exact fixed-point sums: m = (double)sum_n llrint(c_n * 2^32) / count * 2^-32;
+ *  (iii) label = rank of the cluster's smallest member index n = j*W + i; palette = cluster mean.
+ * Returns 0, or -1 if a value is non-finite or too large for the fixed-point sums. */
+int mo_labels(const float* c, int H, int W, int C, float delta, int32_t* labels, int32_t* n_clusters,
+              float* palette, int32_t max_k) {
+  const int32_t N = H * W;
+  for (int64_t q = 0; q < (int64_t)N * C; ++q)
+    if (!isfinite(c[q]) || fabsf(c[q]) > 64.0f) return -1;
+  int32_t* parent = (int32_t*)malloc(sizeof(int32_t) * N);
+  for (int32_t n = 0; n < N; ++n) parent[n] = n;
+  /* (i) 4-neighbour segments */
+  for (int j = 0; j < H; ++j)
+    for (int i = 0; i < W; ++i) {
+      int32_t a = j * W + i;
+      if (i + 1 < W) {
+        int ok = 1;
+        for (int k = 0; k < C; ++k) {
+          float d = c[(size_t)a * C + k] - c[(size_t)(a + 1) * C + k];
+          if (!(fabsf(d) <= delta)) ok = 0;
+        }
+        if (ok) uf_union(parent, a, a + 1);
+      }
+      if (j + 1 < H) {
+        int ok = 1;
+        for (int k = 0; k < C; ++k) {
+          float d = c[(size_t)a * C + k] - c[(size_t)(a + W) * C + k];
+          if (!(fabsf(d) <= delta)) ok = 0;
+        }
+        if (ok) uf_union(parent, a, a + W);
+      }
+    }
+  /* segment roots and exact fixed-point sums */
+  int32_t* seg_of_root = (int32_t*)malloc(sizeof(int32_t) * N);
+  int32_t S = 0;
+  for (int32_t n = 0; n < N; ++n) {
+    if (uf_find(parent, n) == n) seg_of_root[n] = S++;
+  }
+  int64_t* sum = (int64_t*)calloc((size_t)S * C, sizeof(int64_t));
+  int64_t* cnt = (int64_t*)calloc((size_t)S, sizeof(int64_t));
+  int32_t* seg_root = (int32_t*)malloc(sizeof(int32_t) * (S > 0 ? S : 1));
+  for (int32_t n = 0; n < N; ++n) {
+    int32_t r = uf_find(parent, n);
+    int32_t s = seg_of_root[r];
+    seg_root[s] = r;
+    cnt[s] += 1;
+    for (int k = 0; k < C; ++k) sum[(size_t)s * C + k] += llrint((double)c[(size_t)n * C + k] * 0x1.0p32);
+  }
+  double* mean = (double*)malloc(sizeof(double) * (size_t)(S > 0 ? S : 1) * C);
+  for (int32_t s = 0; s < S; ++s)
+    for (int k = 0; k < C; ++k) mean[(size_t)s * C + k] = (double)sum[(size_t)s * C + k] / (double)cnt[s] * 0x1.0p-32;
+  /* (ii) merge segments with close means: sort on channel 0, sweep the delta window */
+  seg_key* keys = (seg_key*)malloc(sizeof(seg_key) * (S > 0 ? S : 1));
+  for (int32_t s = 0; s < S; ++s) { keys[s].m0 = mean[(size_t)s * C]; keys[s].seg = s; }
+  qsort(keys, (size_t)S, sizeof(seg_key), cmp_seg_key);
+  const double dd = (double)delta;
+  for (int32_t a = 0; a < S; ++a) {
+    for (int32_t b = a + 1; b < S && keys[b].m0 - keys[a].m0 <= dd; ++b) {
+      int32_t sa = keys[a].seg, sb = keys[b].seg;
+      int ok = 1;
+      for (int k = 0; k < C; ++k)
+        if (!(fabs(mean[(size_t)sa * C + k] - mean[(size_t)sb * C + k]) <= dd)) { ok = 0; break; }
+      if (ok) uf_union(parent, seg_root[sa], seg_root[sb]);
+    }
+  }
+  /* (iii) canonical ids: rank of the smallest member index (roots are smallest members) */
+  int32_t* id_of_root = seg_of_root; /* reuse */
+  for (int32_t n = 0; n < N; ++n) id_of_root[n] = -1;
+  int32_t K = 0;
+  for (int32_t n = 0; n < N; ++n) {
+    int32_t r = uf_find(parent, n);
+    if (id_of_root[r] < 0) id_of_root[r] = K++;
+    labels[n] = id_of_root[r];
+  }
+  *n_clusters = K;
+  if (palette && max_k > 0) {
+    int64_t* psum = (int64_t*)calloc((size_t)K * C, sizeof(int64_t));
+    int64_t* pcnt = (int64_t*)calloc((size_t)K, sizeof(int64_t));
+    for (int32_t n = 0; n < N; ++n) {
+      int32_t l = labels[n];
+      pcnt[l] += 1;
+      for (int k = 0; k < C; ++k) psum[(size_t)l * C + k] += llrint((double)c[(size_t)n * C + k] * 0x1.0p32);
+    }
+    for (int32_t l = 0; l < K && l < max_k; ++l)
+      for (int k = 0; k < C; ++k) palette[(size_t)l * C + k] = (float)((double)psum[(size_t)l * C + k] / (double)pcnt[l] * 0x1.0p-32);
+    free(psum); free(pcnt);
+  }
+  free(parent); free(seg_of_root); free(sum); free(cnt); free(seg_root); free(mean); free(keys);
+  return 0;
+}

@@ -1,0 +1,74 @@
+/*
+ * msa_oracle.h - plain fp64 CPU oracle for the msa hot path (arXiv 2510.16154).
+ *
+ * TEST INFRASTRUCTURE. Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library. The product
+ * path (paper_2510_16154_b200/) never includes, links or calls it, and this
+ * code shares nothing with the CUDA path.
+ *
+ * Layouts (one image; the Python wrapper loops over the batch):
+ *   scalar fields  u[H][W][C]            row 0 = bottom
+ *   vector fields  p[H][W][2C]           components (x,0..C-1) then (y,0..C-1)
+ *
+ * Parity status per function is stated in DESIGN.md §3 ("pins"); the composite
+ * trajectory with the agent term on is "parity unpinned" beyond the invariants
+ * P8/P9.
+ */
+#ifndef MSA_ORACLE_H
+#define MSA_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  int32_t height, width, channels;
+  int32_t radius;           /* window D_R = {delta : |delta|^2 <= R^2}  (reading R2) */
+  int32_t kernel;           /* 0 = standard Wendland (4r+1)(1-r)^4, 1 = as printed (4r-1)(1-r)^4 (R3) */
+  int32_t iters_per_round;  /* K (reading R8) */
+  int32_t rounds;
+  int32_t pad_;
+  double hx, hy;            /* grid spacing; <= 0 -> 1/(W-1), 1/(H-1) (1 if the size is 1)  (R5) */
+  double alpha, beta;       /* fidelity weight (eq:cost_TV), TV weight (R27) */
+  double eps_x, eps_c;      /* eq:ellipsoid controls; eps_x <= 0 -> 2/(R*min(hx,hy))^2 (R2) */
+  double dt;                /* explicit Euler step */
+  double rho, gamma, kappa; /* penalty, ascent step (Alg. 2 line 7), penalty growth (R9) */
+  double tau, sigma, theta; /* CP steps (R7); tau/sigma <= 0 -> 0.99/L; theta < 0 -> 1 */
+} mo_params;
+
+enum { MO_STAT_ETV = 0, MO_STAT_EFID, MO_STAT_P, MO_STAT_D, MO_STAT_GAP, MO_STAT_RES, MO_STAT_RHO, MO_STAT_NONFINITE,
+       MO_STAT_MEAN0, /* mean[C] follows */ };
+#define MO_NSTAT(C) (8 + (C))
+
+int mo_derive(const mo_params* in, mo_params* out);
+double mo_phi(double r, int kernel);
+double mo_pair_r(double dx_omega, double dy_omega, double dc2, double eps_x, double eps_c);
+int mo_window_size(int R);
+
+void mo_grad(const double* u, double* g, int H, int W, int C, double hx, double hy);
+void mo_div(const double* p, double* d, int H, int W, int C, double hx, double hy);
+void mo_agent_rhs(const mo_params* prm, const double* c, double* F);
+
+void mo_init_state(const mo_params* prm, const double* I, double* c, double* cbar, double* p, double* mu);
+void mo_iteration(const mo_params* prm, double rho, const double* I, double* c, double* cbar, double* p,
+                  const double* mu);
+void mo_round_stats(const mo_params* prm, double rho, const double* I, const double* c, const double* p,
+                    const double* mu, double* stats);
+void mo_round_update(const mo_params* prm, double rho, const double* c, double* mu);
+int mo_run(const mo_params* prm, const double* I, double* c, double* cbar, double* p, double* mu,
+           int64_t iter0, int64_t n_iters, double* rho_inout, double* stats, int32_t stats_cap);
+
+double mo_energy_K(const mo_params* prm, const double* u, const double* I);
+double mo_energy_L(const mo_params* prm, double rho, const double* u, const double* v, const double* mu,
+                   const double* I);
+double mo_energy_Ltilde(const mo_params* prm, double rho, const double* u, const double* v, const double* mu,
+                        const double* I);
+void mo_shrink_field(const mo_params* prm, double rho, const double* c, const double* mu, double* v);
+
+int mo_labels(const float* c, int H, int W, int C, float delta, int32_t* labels, int32_t* n_clusters,
+              float* palette, int32_t max_k);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,30 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200, sm_100a); parity tests through the C ABI")
+    config.addinivalue_line("markers", "slow: long-running (full-size oracle runs)")
+
+
+@pytest.fixture(scope="session", autouse=True)
+def _built_libs():
+    import oracle
+    import synth
+    oracle.build()
+    synth.build()
+    yield
+
+
+def gpu_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
