@@ -1,0 +1,187 @@
+/*
+ * msa.h - C ABI of the B200 (sm_100a) hot path of arXiv 2510.16154:
+ * "optimal control of a pixel multi-agent system" for colour quantisation.
+ *
+ * One solver iteration is
+ *   1. agent Euler step    c_half = c + dt F(c),
+ *        F(n) = (1/N_R) sum_{delta in D_R, n+delta inside} phi(r(n,delta)) (c(n+delta) - c(n))
+ *        eq:MAsystem PAPER.md:86-95, eq:ellipsoid :97-102, eq:kernel :259-267, Euler :270
+ *   2. dual ascent + projection  p+ = Pi_beta((rho (p + sigma grad cbar) - sigma mu)/(rho + sigma))
+ *        eq:complete_square PAPER.md:397-404, eq:soft_threshold :431-440 (reading R7)
+ *   3. prox fidelity + extrapolation  c+ = c_half + (tau div p+ + tau alpha (I - c_half))/(1 + tau alpha),
+ *        cbar+ = c+ + theta (c+ - c_half)     eq:new_adjoint PAPER.md:405-413 (R7, R21)
+ * and every K = iters_per_round iterations a multiplier round (steps 4-5):
+ *        v = S_{beta/rho}(grad c - mu/rho),  mu+ = mu + gamma (v - grad c),  rho+ = kappa rho
+ *        Alg. 2 lines 6-7 PAPER.md:456-457, eq:soft_threshold :431-440,
+ * with the round statistics (energy, primal-dual gap, AL residual) reduced before mu is updated.
+ * Labels (step 7) are the quantisation rule Q(c; delta) of reading R16.
+ *
+ * Conventions
+ *  - Every function returns MSA_OK (0) or a negative MSA_E* code; msa_last_error() gives a
+ *    thread-local message. No C++ exception crosses the ABI.
+ *  - Images are float32 [B][H][W][C], channel-interleaved, row 0 = BOTTOM.
+ *    Vector fields (p, mu) are float32 [B][H][W][2C]: components (x,0..C-1) then (y,0..C-1).
+ *  - Pointers flagged *_on_device are CUDA device pointers on params->device; otherwise host.
+ *    The caller owns every buffer it passes; the library never keeps a caller pointer except
+ *    the optional workspace, which must outlive the context.
+ *  - Streams: `stream` is a cudaStream_t (e.g. torch's current stream) or NULL for a library
+ *    stream. msa_step is stream-ordered (no host sync). msa_solve, msa_labels, msa_get_*,
+ *    msa_set_* synchronise the stream before returning.
+ *  - A context is not thread-safe; distinct contexts may be used concurrently.
+ *  - Sharding: shard = 0 none, 1 row slabs (NCCL halo exchange each
+ *    iteration + all-reduce of the round statistics), 2 batch (images split over ranks,
+ *    no data-path collective). world = 1 ignores the mode.
+ */
+#ifndef MSA_H
+#define MSA_H
+#include <stddef.h>
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MSA_ABI_VERSION 1
+
+enum {
+  MSA_OK = 0,
+  MSA_EINVAL = -1,    /* bad parameter, shape, pointer or call argument */
+  MSA_ENOMEM = -2,    /* device or host allocation failed / workspace too small */
+  MSA_ECUDA = -3,     /* a CUDA runtime call or kernel launch failed */
+  MSA_ENCCL = -4,     /* an NCCL call failed or NCCL is unavailable */
+  MSA_EDIVERGED = -5, /* non-finite state detected at a round (message names the round) */
+  MSA_ESTATE = -6     /* call out of order (e.g. step after a divergence) */
+};
+
+enum { MSA_SHARD_NONE = 0, MSA_SHARD_ROWS = 1, MSA_SHARD_BATCH = 2 };
+enum { MSA_FIELD_C = 0, MSA_FIELD_CBAR = 1, MSA_FIELD_P = 2, MSA_FIELD_MU = 3, MSA_FIELD_I = 4 };
+enum { MSA_KERNEL_WENDLAND = 0, MSA_KERNEL_PRINTED = 1 };
+
+/* All real quantities in the paper's normalised units: Omega = [0,1]^2,
+ * pixel spacing h_x = 1/(W-1), h_y = 1/(H-1) (1 for a size-1 axis; reading R5). */
+typedef struct {
+  int32_t batch, height, width, channels; /* B >= 1, H, W >= 1, 1 <= C <= 16 */
+  double alpha;       /* fidelity weight alpha >= 0 (eq:cost_TV; alpha = 0 allowed: D, gap = NaN) */
+  double beta;        /* TV weight beta >= 0 (1 in eq:cost_TV; reading R27) */
+  int32_t radius;     /* window radius R in pixels, 0 <= R <= 8 (reading R2) */
+  int32_t kernel;     /* MSA_KERNEL_WENDLAND (4r+1)(1-r)^4 or MSA_KERNEL_PRINTED (4r-1)(1-r)^4 (R3) */
+  double eps_x;       /* eq:ellipsoid spatial control; <= 0 -> 2/(R min(h_x,h_y))^2 (R2) */
+  double eps_c;       /* eq:ellipsoid colour control >= 0 (57 in PAPER.md:270) */
+  double dt;          /* Euler step >= 0 (0.25 in PAPER.md:247) */
+  double rho;         /* penalty rho > 0 */
+  double gamma;       /* multiplier ascent step gamma > 0 (Alg. 2 line 7) */
+  double kappa;       /* penalty growth per round, rho <- kappa rho (R9; 1 = the paper's fixed rho) */
+  double tau, sigma;  /* primal / dual CP steps; <= 0 -> 0.99/L, L = sqrt(4/h_x^2 + 4/h_y^2) (R7) */
+  double theta;       /* extrapolation; < 0 -> 1 */
+  int32_t iters_per_round; /* K >= 1: iterations between multiplier rounds (R8) */
+  int32_t rounds;          /* multiplier rounds per msa_solve call (>= 0) */
+  int32_t shard, rank, world, device; /* MSA_SHARD_*, this rank, number of ranks, CUDA device */
+  const void* nccl_id;     /* 128-byte ncclUniqueId (from rank 0's msa_nccl_unique_id) when world > 1 */
+} msa_params;
+
+/* One record per multiplier round, reduced over the rank's images (batch mode: per rank;
+ * rows mode: over the whole image via all-reduce), fp64, quadrature weight h_x h_y:
+ * E_TV = <beta |grad c|>, E_fid = alpha/2 ||c - I||^2, primal P = <Huber(grad c - mu/rho)> + E_fid,
+ * dual D = -<I, div p> - ||div p||^2/(2 alpha) - <mu, p>/rho - ||p||^2/(2 rho), gap = P - D,
+ * al_residual = ||v - grad c||, mean = per-channel mean of c, all with the pre-update mu. */
+typedef struct {
+  int32_t round;      /* 0-based round index since msa_init */
+  int32_t images;     /* number of images summed into this record */
+  int64_t iters;      /* global iteration count at the end of the round */
+  double e_tv, e_fid, primal, dual, gap, al_residual;
+  double rho;         /* rho used during the round */
+  double nonfinite;   /* count of non-finite values of c */
+  double mean[16];
+} msa_round_stats;
+
+/* Partition and derived values of a context (msa_query). */
+typedef struct {
+  int32_t row0, nrows;      /* rows owned by this rank (global indices) */
+  int32_t image0, nimages;  /* images owned by this rank */
+  int32_t ghost_rows;       /* halo rows stored above and below the slab */
+  int32_t pitch;            /* device row pitch in floats */
+  double hx, hy, eps_x, tau, sigma, theta; /* derived values actually used */
+  int32_t window_size;      /* N_R */
+  int32_t active_offsets;   /* offsets delta != 0 in D_R with spatial term < 1 */
+  int64_t iters_done;       /* global iteration counter */
+  int64_t launches;         /* kernels launched by this context so far */
+  double rho;               /* current penalty */
+} msa_info;
+
+int msa_abi_version(void);
+const char* msa_last_error(void);
+
+/* Bytes of device workspace msa_init needs for these params (fields only:
+ * 11 C floats per owned pixel plus halo rows and reduction scratch). */
+int msa_workspace_bytes(const msa_params* params, size_t* bytes);
+
+/* Row partition used in MSA_SHARD_ROWS mode: rank r owns rows [row0, row0 + nrows),
+ * contiguous, sizes differ by at most one, bottom slab first. Host only (no GPU). */
+int msa_partition_rows(int32_t height, int32_t world, int32_t rank, int32_t radius, int32_t* row0,
+                       int32_t* nrows, int32_t* ghost_rows);
+
+/* Writes a 128-byte ncclUniqueId to out128 (rank 0 calls it; the harness broadcasts it). */
+int msa_nccl_unique_id(void* out128);
+
+/* Validates params, allocates (or adopts `workspace`, which may be NULL), uploads the
+ * rank's part of `image` (float32 [B][H][W][C], the FULL image set; host or device) and
+ * sets c = cbar = I, p = mu = 0, rho = params->rho (Alg. 2 REQUIRE; R10).
+ * `stream` is a cudaStream_t or NULL. On success *out is a new context. */
+typedef struct msa_ctx msa_ctx;
+int msa_init(const msa_params* params, const float* image, int image_on_device, void* workspace,
+             size_t workspace_bytes, void* stream, msa_ctx** out);
+
+/* Re-initialises the state from a (new) image of the same shape; keeps allocations. */
+int msa_reset(msa_ctx* ctx, const float* image, int image_on_device);
+
+/* Runs n_iters >= 0 fused iterations (steps 1-3, and the halo exchange in rows mode).
+ * Whenever the global iteration count reaches a multiple of K, the multiplier round
+ * (steps 4-5) runs and its statistics are recorded (msa_get_stats). Stream-ordered. */
+int msa_step(msa_ctx* ctx, int32_t n_iters);
+
+/* rounds x K iterations from the current state; fills stats[0 .. rounds) (may be NULL)
+ * with the records of the rounds completed by this call; synchronises. Returns
+ * MSA_EDIVERGED if any of them saw a non-finite value. */
+int msa_solve(msa_ctx* ctx, msa_round_stats* stats);
+
+/* Quantisation rule Q(c; delta) (reading R16) of the current c, per image:
+ *  (i) union 4-neighbours whose fp32 colours differ by <= delta in every channel;
+ *  (ii) union segments whose means differ by <= delta in every channel (means from exact
+ *       64-bit fixed-point sums, m = (double)sum llrint(c 2^32) / count * 2^-32);
+ *  (iii) label = rank of the cluster's smallest member index j*W + i; palette = cluster mean.
+ * labels: int32 [nimages][H][W] of this rank's images (rows mode: world must be 1 in this
+ * ABI version); n_clusters: int32 [nimages]; palette: float32 [nimages][max_k][C] or NULL.
+ * All three are host pointers unless out_on_device. Synchronises. */
+int msa_labels(msa_ctx* ctx, float delta, int32_t* labels, int32_t* n_clusters, float* palette, int32_t max_k,
+               int out_on_device);
+
+/* Copies a field of this rank's rows/images out in the ABI layout ([nimages][nrows][W][C]
+ * or [..][2C] for p, mu). row0/nrows may be NULL. Synchronises. */
+int msa_get_field(msa_ctx* ctx, int32_t which, float* out, int out_on_device, int32_t* row0, int32_t* nrows);
+/* Overwrites a field of this rank's rows/images (same layout as msa_get_field). Synchronises.
+ * Halo rows are refreshed at the next msa_step. */
+int msa_set_field(msa_ctx* ctx, int32_t which, const float* in, int in_on_device);
+
+/* All round records since msa_init (up to max): *n receives the number available. */
+int msa_get_stats(msa_ctx* ctx, msa_round_stats* out, int32_t max, int32_t* n);
+
+/* Exact resume blob (fields c, cbar, p, mu, I of this rank + counters + rho). */
+int msa_state_bytes(msa_ctx* ctx, size_t* bytes);
+int msa_get_state(msa_ctx* ctx, void* host_blob, size_t bytes);
+int msa_set_state(msa_ctx* ctx, const void* host_blob, size_t bytes);
+
+int msa_query(msa_ctx* ctx, msa_info* info);
+
+/* Kernel timing with CUDA events on the context stream: when enabled, one event pair
+ * brackets every batch of consecutive iteration-kernel launches, another every round
+ * update. msa_get_timing returns totals since the last msa_set_timing(ctx, 1). */
+int msa_set_timing(msa_ctx* ctx, int enable);
+int msa_get_timing(msa_ctx* ctx, double* iter_ms, int64_t* iter_launches, double* round_ms,
+                   int64_t* round_launches);
+
+int msa_sync(msa_ctx* ctx);
+int msa_free(msa_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

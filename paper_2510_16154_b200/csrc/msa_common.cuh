@@ -1,0 +1,127 @@
+// msa_common.cuh - device-side layout and per-pixel arithmetic shared by every
+// msa kernel (sm_100a). Nothing here is shared with oracle/ (DESIGN.md §3).
+//
+// Device layout: every field is planar fp32,
+//   [image b][component m][local row][pitch]   local row = global row - row0 + G
+// with G ghost (halo) rows above and below the rank's slab (G = 0 on one GPU),
+// pitch = W rounded up to 32 floats (128-byte rows). Scalar fields (I, c, cbar)
+// have C components, vector fields (p, mu) 2C: (x,0..C-1) then (y,0..C-1).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define MSA_MAXC 16
+#define MSA_MAXR 8
+#define MSA_MAXOFF ((2 * MSA_MAXR + 1) * (2 * MSA_MAXR + 1))
+
+struct MsaGeom {
+  int H, W;        // global image size
+  int row0, nrows; // owned rows [row0, row0 + nrows) (global indices)
+  int G;           // ghost rows on each side of the slab
+  int pitch;       // floats per stored row
+  long long plane; // floats per component plane = (nrows + 2G) * pitch
+  int nb;          // images held by this rank
+  int C;           // channels
+};
+
+__device__ __forceinline__ long long msa_idx(const MsaGeom& g, int b, int m, int nm, int j, int i) {
+  return ((long long)b * nm + m) * g.plane + (long long)(j - g.row0 + g.G) * g.pitch + i;
+}
+
+// Constants of one iteration (host computes them in fp64 and rounds once to fp32).
+struct MsaIterConsts {
+  float dt_NR;      // dt / N_R                      (step 1, reading R2)
+  float e_c;        // eps_c / 2                     (eq:ellipsoid)
+  int kernel;       // 0 Wendland t^4 (5 - 4t), 1 printed t^4 (3 - 4t)   (eq:kernel, R3)
+  int n_off;        // active offsets (generic kernel)
+  float inv_hx, inv_hy;
+  float a_rs;       // rho / (rho + sigma)           (step 2, R7)
+  float sigma;
+  float b_rs;       // sigma / (rho + sigma)
+  float beta, beta2;
+  float tau, tau_alpha, inv_1ta, theta;  // step 3 (R7, R21)
+};
+
+// phi as a function of t = max(1 - r, 0) (eq:kernel PAPER.md:259-267; R3, R21):
+// standard Wendland (4r+1)(1-r)^4 = t^4 (5 - 4t); printed (4r-1)(1-r)^4 = t^4 (3 - 4t).
+template <int KER>
+__device__ __forceinline__ float msa_phi_t(float t) {
+  float t2 = __fmul_rn(t, t);
+  float t4 = __fmul_rn(t2, t2);
+  float q = __fmaf_rn(-4.0f, t, KER == 0 ? 5.0f : 3.0f);
+  return __fmul_rn(t4, q);
+}
+
+// One interaction term (step 1) for neighbour colour cj of pixel colour ci, offset
+// constant om = 1 - a_delta (a_delta = eps_x/2 |delta|_h^2): acc += phi(r) (cj - ci).
+template <int C, int KER>
+__device__ __forceinline__ void msa_agent_term(const float (&ci)[C], const float (&cj)[C], float om, float e_c,
+                                               float (&acc)[C]) {
+  float d[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) d[k] = __fsub_rn(cj[k], ci[k]);
+  float s = __fmul_rn(d[0], d[0]);
+#pragma unroll
+  for (int k = 1; k < C; ++k) s = __fmaf_rn(d[k], d[k], s);
+  float t = fmaxf(__fmaf_rn(-e_c, s, om), 0.0f);
+  float w = msa_phi_t<KER>(t);
+#pragma unroll
+  for (int k = 0; k < C; ++k) acc[k] = __fmaf_rn(w, d[k], acc[k]);
+}
+
+// Step 2 for one pixel: q = rho/(rho+sigma) (p + sigma g) - sigma/(rho+sigma) mu, p+ = Pi_beta(q)
+// over the whole 2C-vector (coupled TV, R4c). g = forward-difference gradient of cbar
+// (zero on the last column/row, R6), given as gx[k], gy[k].
+template <int C>
+__device__ __forceinline__ void msa_dual_step(const MsaIterConsts& K, const float (&gx)[C], const float (&gy)[C],
+                                              const float (&px)[C], const float (&py)[C], const float (&mx)[C],
+                                              const float (&my)[C], float (&qx)[C], float (&qy)[C]) {
+  float n2 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    qx[k] = __fmaf_rn(K.a_rs, __fmaf_rn(K.sigma, gx[k], px[k]), -__fmul_rn(K.b_rs, mx[k]));
+    qy[k] = __fmaf_rn(K.a_rs, __fmaf_rn(K.sigma, gy[k], py[k]), -__fmul_rn(K.b_rs, my[k]));
+    n2 = __fmaf_rn(qx[k], qx[k], n2);
+    n2 = __fmaf_rn(qy[k], qy[k], n2);
+  }
+  if (n2 > K.beta2) {
+    float f = __fdiv_rn(K.beta, __fsqrt_rn(n2));
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      qx[k] = __fmul_rn(qx[k], f);
+      qy[k] = __fmul_rn(qy[k], f);
+    }
+  }
+}
+
+// Step 3 for one channel: c+ = c_half + (tau d + tau alpha (I - c_half)) / (1 + tau alpha),
+// cbar+ = c+ + theta (c+ - c_half)   (increment form, R21).
+__device__ __forceinline__ void msa_prox_extrap(const MsaIterConsts& K, float chalf, float d, float I, float& cp,
+                                                float& cbp) {
+  float inc = __fmaf_rn(K.tau, d, __fmul_rn(K.tau_alpha, __fsub_rn(I, chalf)));
+  cp = __fadd_rn(chalf, __fmul_rn(inc, K.inv_1ta));
+  cbp = __fmaf_rn(K.theta, __fsub_rn(cp, chalf), cp);
+}
+
+// Round constants (steps 4-5).
+struct MsaRoundConsts {
+  float inv_hx, inv_hy;
+  float inv_rho, thr; // 1/rho, beta/rho
+  float gamma;
+  double rho, beta, alpha;
+};
+
+// Order of the per-image statistic sums (fp64) produced by the round kernel.
+enum {
+  MSA_S_TV = 0,  // sum |grad c|
+  MSA_S_FID,     // sum (c - I)^2
+  MSA_S_HUB,     // sum Huber(grad c - mu/rho)
+  MSA_S_IDP,     // sum I . div p
+  MSA_S_DP2,     // sum |div p|^2
+  MSA_S_MUP,     // sum mu . p
+  MSA_S_PP,      // sum |p|^2
+  MSA_S_RES,     // sum |v - grad c|^2
+  MSA_S_NONFIN,  // count of non-finite c
+  MSA_S_MEAN0,   // sum c_k, k < C
+  MSA_NSUM = MSA_S_MEAN0 + MSA_MAXC
+};

@@ -1,0 +1,869 @@
+// msa_driver.cu - the C ABI of include/msa.h: validation, partition, device memory,
+// the iteration/round schedule (SURVEY.md §8(c) oracle block, realised on the GPU),
+// NCCL halo exchange + all-reduce for row slabs, labels, state I/O.
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "../../include/msa.h"
+#include "msa_internal.h"
+
+// ------------------------------------------------------------------ errors
+static thread_local char g_err[512] = "";
+static int set_err(int code, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return code;
+}
+#define CUDA_TRY(x)                                                                                   \
+  do {                                                                                                \
+    cudaError_t e_ = (x);                                                                             \
+    if (e_ != cudaSuccess) return set_err(MSA_ECUDA, "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), \
+                                          __FILE__, __LINE__);                                        \
+  } while (0)
+
+// ------------------------------------------------------------------ NCCL (loaded on demand)
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi g_nccl;
+
+bool nccl_load() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  // prefer the NCCL already mapped into the process (torch's), else the system one
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+#define LOADSYM(field, name) g_nccl.field = (decltype(g_nccl.field))dlsym(h, name)
+  LOADSYM(GetUniqueId, "ncclGetUniqueId");
+  LOADSYM(CommInitRank, "ncclCommInitRank");
+  LOADSYM(CommDestroy, "ncclCommDestroy");
+  LOADSYM(Send, "ncclSend");
+  LOADSYM(Recv, "ncclRecv");
+  LOADSYM(GroupStart, "ncclGroupStart");
+  LOADSYM(GroupEnd, "ncclGroupEnd");
+  LOADSYM(AllReduce, "ncclAllReduce");
+  LOADSYM(GetErrorString, "ncclGetErrorString");
+#undef LOADSYM
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.Send && g_nccl.Recv &&
+              g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.AllReduce && g_nccl.GetErrorString;
+  return g_nccl.ok;
+}
+#define NCCL_TRY(x)                                                                                            \
+  do {                                                                                                         \
+    ncclResult_t r_ = (x);                                                                                     \
+    if (r_ != ncclSuccess) return set_err(MSA_ENCCL, "%s failed: %s", #x, g_nccl.GetErrorString(r_));          \
+  } while (0)
+
+constexpr int REC_CAP = 1024;  // device-side round records pending a host fetch
+}  // namespace
+
+// ------------------------------------------------------------------ context
+struct msa_ctx {
+  msa_params prm;
+  double hx, hy, eps_x, tau, sigma, theta, rho_cur;
+  int NR = 0;
+  MsaOffsetTable T;
+  MsaGeom g;
+  int image0 = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  char* ws = nullptr;
+  bool own_ws = false;
+  size_t ws_bytes = 0;
+  float *I = nullptr, *mu = nullptr;
+  float *c[2] = {nullptr, nullptr}, *cb[2] = {nullptr, nullptr}, *p[2] = {nullptr, nullptr};
+  int cur = 0;
+  int2* d_off = nullptr;
+  float* d_om = nullptr;
+  double* partials = nullptr;
+  double* sums = nullptr;
+  msa_round_stats* d_rec = nullptr;
+  int rec_pending = 0;
+  std::vector<msa_round_stats> stats;
+  int64_t iters_done = 0;
+  int32_t rounds_done = 0;
+  int64_t launches = 0;
+  bool halo_mu_dirty = true;
+  // timing
+  bool timing = false, in_iter_batch = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> iter_ev, round_ev;
+  int64_t iter_launches_t = 0, round_launches_t = 0;
+  // nccl
+  ncclComm_t comm = nullptr;
+  // labels
+  MsaLabelScratch* lab = nullptr;
+  int32_t* lab_buf = nullptr;
+  int32_t* lab_count = nullptr;
+  float* lab_pal = nullptr;
+  int lab_pal_cap = 0;
+};
+
+namespace {
+
+bool finite_all(const msa_params* p) {
+  const double v[] = {p->alpha, p->beta, p->eps_x, p->eps_c, p->dt, p->rho, p->gamma, p->kappa, p->tau, p->sigma,
+                      p->theta};
+  for (double x : v)
+    if (!isfinite(x)) return false;
+  return true;
+}
+
+int validate(const msa_params* p) {
+  if (!p) return set_err(MSA_EINVAL, "params is NULL");
+  if (p->batch < 1 || p->height < 1 || p->width < 1) return set_err(MSA_EINVAL, "batch/height/width must be >= 1");
+  if (p->channels < 1 || p->channels > MSA_MAXC) return set_err(MSA_EINVAL, "channels must be in [1,16]");
+  if ((long long)p->height * p->width >= (1LL << 31)) return set_err(MSA_EINVAL, "H*W must be < 2^31");
+  if (!finite_all(p)) return set_err(MSA_EINVAL, "non-finite parameter");
+  if (p->alpha < 0) return set_err(MSA_EINVAL, "alpha must be >= 0");
+  if (p->beta < 0) return set_err(MSA_EINVAL, "beta must be >= 0");
+  if (p->radius < 0 || p->radius > MSA_MAXR) return set_err(MSA_EINVAL, "radius must be in [0,8]");
+  if (p->kernel != MSA_KERNEL_WENDLAND && p->kernel != MSA_KERNEL_PRINTED) return set_err(MSA_EINVAL, "bad kernel");
+  if (p->eps_c < 0) return set_err(MSA_EINVAL, "eps_c must be >= 0");
+  if (p->dt < 0) return set_err(MSA_EINVAL, "dt must be >= 0");
+  if (p->rho <= 0 || p->gamma <= 0 || p->kappa <= 0) return set_err(MSA_EINVAL, "rho, gamma, kappa must be > 0");
+  if (p->iters_per_round < 1) return set_err(MSA_EINVAL, "iters_per_round must be >= 1");
+  if (p->rounds < 0) return set_err(MSA_EINVAL, "rounds must be >= 0");
+  if (p->world < 1 || p->rank < 0 || p->rank >= p->world) return set_err(MSA_EINVAL, "bad rank/world");
+  if (p->shard < MSA_SHARD_NONE || p->shard > MSA_SHARD_BATCH) return set_err(MSA_EINVAL, "bad shard mode");
+  if (p->world > 1 && p->shard == MSA_SHARD_NONE) return set_err(MSA_EINVAL, "world > 1 needs a shard mode");
+  if (p->world > 1 && p->shard == MSA_SHARD_BATCH && p->batch < p->world)
+    return set_err(MSA_EINVAL, "batch sharding needs batch >= world");
+  if (p->world > 1 && p->shard == MSA_SHARD_ROWS) {
+    const int ghost = std::max(p->radius, 1);
+    if (p->height / p->world < ghost) return set_err(MSA_EINVAL, "row slabs must hold >= max(R,1) rows each");
+    if (!p->nccl_id) return set_err(MSA_EINVAL, "rows mode with world > 1 needs nccl_id");
+  }
+  if (p->device < 0) return set_err(MSA_EINVAL, "device must be >= 0");
+  return MSA_OK;
+}
+
+struct Derived {
+  double hx, hy, eps_x, tau, sigma, theta;
+  int NR;
+  MsaOffsetTable T;
+};
+
+int derive(const msa_params* p, Derived* d) {
+  d->hx = p->width > 1 ? 1.0 / (double)(p->width - 1) : 1.0;    // R5
+  d->hy = p->height > 1 ? 1.0 / (double)(p->height - 1) : 1.0;
+  const double h = std::min(d->hx, d->hy);
+  const double Rh = (p->radius > 0 ? p->radius : 1) * h;
+  d->eps_x = p->eps_x > 0 ? p->eps_x : 2.0 / (Rh * Rh);         // R2
+  const double L = sqrt(4.0 / (d->hx * d->hx) + 4.0 / (d->hy * d->hy));
+  d->tau = p->tau > 0 ? p->tau : 0.99 / L;                         // R7
+  d->sigma = p->sigma > 0 ? p->sigma : 0.99 / L;
+  d->theta = p->theta >= 0 ? p->theta : 1.0;
+  if (d->tau * d->sigma * L * L >= 1.0) return set_err(MSA_EINVAL, "tau*sigma*L^2 must be < 1 (L^2 = 4/hx^2+4/hy^2)");
+  const int R = p->radius;
+  d->NR = 0;
+  d->T.n = 0;
+  for (int dy = -R; dy <= R; ++dy)
+    for (int dx = -R; dx <= R; ++dx) {
+      if (dx * dx + dy * dy > R * R) continue;
+      ++d->NR;
+      if (dx == 0 && dy == 0) continue;  // phi(r) (c - c) = 0
+      const double a = 0.5 * d->eps_x * ((dx * d->hx) * (dx * d->hx) + (dy * d->hy) * (dy * d->hy));
+      const double om = 1.0 - a;
+      if (!(om > 1e-12)) continue;  // phi = 0 exactly in fp32 (t^4 < 1e-48 underflows); DESIGN.md §5
+      d->T.dx[d->T.n] = dx;
+      d->T.dy[d->T.n] = dy;
+      d->T.om[d->T.n] = (float)om;
+      ++d->T.n;
+    }
+  return MSA_OK;
+}
+
+struct Part {
+  int row0, nrows, ghost, image0, nimages;
+};
+Part partition(const msa_params* p) {
+  Part r{0, p->height, 0, 0, p->batch};
+  if (p->world > 1 && p->shard == MSA_SHARD_ROWS) {
+    const int base = p->height / p->world, rem = p->height % p->world;
+    r.nrows = base + (p->rank < rem ? 1 : 0);
+    r.row0 = p->rank * base + std::min(p->rank, rem);
+    r.ghost = std::max(p->radius, 1);
+  } else if (p->world > 1 && p->shard == MSA_SHARD_BATCH) {
+    const int base = p->batch / p->world, rem = p->batch % p->world;
+    r.nimages = base + (p->rank < rem ? 1 : 0);
+    r.image0 = p->rank * base + std::min(p->rank, rem);
+  }
+  return r;
+}
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+  size_t plane_floats, f1, f2;  // floats per plane, per C-field, per 2C-field
+  size_t off_I, off_mu, off_set[2], off_partials, off_sums, off_off, off_om, off_rec, total;
+  int pitch, nblk;
+};
+Layout layout(const msa_params* p, const Part& pt) {
+  Layout L;
+  L.pitch = (int)align_up((size_t)p->width, 32);
+  L.plane_floats = (size_t)(pt.nrows + 2 * pt.ghost) * L.pitch;
+  L.f1 = (size_t)pt.nimages * p->channels * L.plane_floats;
+  L.f2 = 2 * L.f1;
+  size_t o = 0;
+  L.off_I = o;  o += align_up(L.f1 * 4, 256);
+  L.off_mu = o; o += align_up(L.f2 * 4, 256);
+  for (int s = 0; s < 2; ++s) {  // set = {c, cbar, p} contiguous (the idle set is staging space)
+    L.off_set[s] = o;
+    o += align_up((L.f1 + L.f1 + L.f2) * 4, 256);
+  }
+  MsaGeom g;
+  g.W = p->width;
+  g.nrows = pt.nrows;
+  L.nblk = msa_round_blocks(g);
+  L.off_partials = o; o += align_up((size_t)pt.nimages * L.nblk * MSA_NSUM * 8, 256);
+  L.off_sums = o;     o += align_up(MSA_NSUM * 8, 256);
+  L.off_off = o;      o += align_up(MSA_MAXOFF * sizeof(int2), 256);
+  L.off_om = o;       o += align_up(MSA_MAXOFF * sizeof(float), 256);
+  L.off_rec = o;      o += align_up(REC_CAP * sizeof(msa_round_stats), 256);
+  L.total = o;
+  return L;
+}
+
+MsaIterConsts iter_consts(const msa_ctx* x, double rho) {
+  MsaIterConsts K;
+  const msa_params& p = x->prm;
+  K.dt_NR = (float)(p.dt / (double)x->NR);
+  K.e_c = (float)(0.5 * p.eps_c);
+  K.kernel = p.kernel;
+  K.n_off = x->T.n;
+  K.inv_hx = (float)(1.0 / x->hx);
+  K.inv_hy = (float)(1.0 / x->hy);
+  K.a_rs = (float)(rho / (rho + x->sigma));
+  K.sigma = (float)x->sigma;
+  K.b_rs = (float)(x->sigma / (rho + x->sigma));
+  K.beta = (float)p.beta;
+  K.beta2 = (float)(p.beta * p.beta);
+  K.tau = (float)x->tau;
+  K.tau_alpha = (float)(x->tau * p.alpha);
+  K.inv_1ta = (float)(1.0 / (1.0 + x->tau * p.alpha));
+  K.theta = (float)x->theta;
+  return K;
+}
+
+// A geometry covering rows [r_lo, r_hi) of the stored (owned + ghost) rows, for pack/unpack.
+MsaGeom sub_geom(const MsaGeom& g, int r_lo, int r_hi) {
+  MsaGeom s = g;
+  s.G = g.G - (g.row0 - r_lo);
+  s.row0 = r_lo;
+  s.nrows = r_hi - r_lo;
+  return s;
+}
+
+float* field_ptr(msa_ctx* x, int which, int set) {
+  switch (which) {
+    case MSA_FIELD_C: return x->c[set];
+    case MSA_FIELD_CBAR: return x->cb[set];
+    case MSA_FIELD_P: return x->p[set];
+    case MSA_FIELD_MU: return x->mu;
+    case MSA_FIELD_I: return x->I;
+  }
+  return nullptr;
+}
+int field_nm(const msa_ctx* x, int which) {
+  return (which == MSA_FIELD_P || which == MSA_FIELD_MU) ? 2 * x->prm.channels : x->prm.channels;
+}
+
+// --- timing helpers
+void iter_batch_begin(msa_ctx* x) {
+  if (!x->timing || x->in_iter_batch) return;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a, x->stream);
+  x->iter_ev.push_back({a, b});
+  x->in_iter_batch = true;
+}
+void iter_batch_end(msa_ctx* x) {
+  if (!x->timing || !x->in_iter_batch) return;
+  cudaEventRecord(x->iter_ev.back().second, x->stream);
+  x->in_iter_batch = false;
+}
+
+// --- fetch pending device records to the host (synchronises)
+int fetch_records(msa_ctx* x) {
+  if (x->rec_pending == 0) return MSA_OK;
+  std::vector<msa_round_stats> buf(x->rec_pending);
+  CUDA_TRY(cudaMemcpyAsync(buf.data(), x->d_rec, sizeof(msa_round_stats) * x->rec_pending, cudaMemcpyDeviceToHost,
+                           x->stream));
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  x->stats.insert(x->stats.end(), buf.begin(), buf.end());
+  x->rec_pending = 0;
+  return MSA_OK;
+}
+
+// --- halo exchange of the current state (rows mode, world > 1)
+int halo_exchange(msa_ctx* x, bool with_c, bool with_cb, bool with_p, bool with_mu) {
+  const msa_params& P = x->prm;
+  if (!(P.world > 1 && P.shard == MSA_SHARD_ROWS)) return MSA_OK;
+  const MsaGeom& g = x->g;
+  const int C = P.channels, G = g.G;
+  const size_t pitch = g.pitch;
+  const int lo = P.rank - 1, hi = P.rank + 1;
+  const bool has_lo = lo >= 0, has_hi = hi < P.world;
+  auto rowp = [&](float* f, int b, int m, int nm, int j) { return f + ((size_t)b * nm + m) * g.plane + (size_t)(j - g.row0 + G) * pitch; };
+  const int s = x->cur;
+  NCCL_TRY(g_nccl.GroupStart());
+  for (int b = 0; b < g.nb; ++b) {
+    if (with_c)
+      for (int k = 0; k < C; ++k) {
+        float* f = x->c[s];
+        if (has_lo) {
+          NCCL_TRY(g_nccl.Send(rowp(f, b, k, C, g.row0), (size_t)G * pitch, ncclFloat, lo, x->comm, x->stream));
+          NCCL_TRY(g_nccl.Recv(rowp(f, b, k, C, g.row0 - G), (size_t)G * pitch, ncclFloat, lo, x->comm, x->stream));
+        }
+        if (has_hi) {
+          NCCL_TRY(g_nccl.Send(rowp(f, b, k, C, g.row0 + g.nrows - G), (size_t)G * pitch, ncclFloat, hi, x->comm, x->stream));
+          NCCL_TRY(g_nccl.Recv(rowp(f, b, k, C, g.row0 + g.nrows), (size_t)G * pitch, ncclFloat, hi, x->comm, x->stream));
+        }
+      }
+    if (with_cb)
+      for (int k = 0; k < C; ++k) {
+        float* f = x->cb[s];
+        if (has_lo) {
+          NCCL_TRY(g_nccl.Send(rowp(f, b, k, C, g.row0), pitch, ncclFloat, lo, x->comm, x->stream));
+          NCCL_TRY(g_nccl.Recv(rowp(f, b, k, C, g.row0 - 1), pitch, ncclFloat, lo, x->comm, x->stream));
+        }
+        if (has_hi) {
+          NCCL_TRY(g_nccl.Send(rowp(f, b, k, C, g.row0 + g.nrows - 1), pitch, ncclFloat, hi, x->comm, x->stream));
+          NCCL_TRY(g_nccl.Recv(rowp(f, b, k, C, g.row0 + g.nrows), pitch, ncclFloat, hi, x->comm, x->stream));
+        }
+      }
+    // p and mu: the slab below needs nothing; the slab above needs my top row as its row0-1
+    float* vf[2] = {with_p ? x->p[s] : nullptr, with_mu ? x->mu : nullptr};
+    for (float* f : vf) {
+      if (!f) continue;
+      for (int m = 0; m < 2 * C; ++m) {
+        if (has_hi) NCCL_TRY(g_nccl.Send(rowp(f, b, m, 2 * C, g.row0 + g.nrows - 1), pitch, ncclFloat, hi, x->comm, x->stream));
+        if (has_lo) NCCL_TRY(g_nccl.Recv(rowp(f, b, m, 2 * C, g.row0 - 1), pitch, ncclFloat, lo, x->comm, x->stream));
+      }
+    }
+  }
+  NCCL_TRY(g_nccl.GroupEnd());
+  return MSA_OK;
+}
+
+// --- one multiplier round (steps 4-5) at the end of an iteration that completed a round
+int do_round(msa_ctx* x) {
+  const msa_params& P = x->prm;
+  const int s = x->cur;
+  int rc;
+  // the round needs c one row above the slab (grad) and p one row below (div p)
+  if ((rc = halo_exchange(x, true, false, true, false)) != MSA_OK) return rc;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (x->timing) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, x->stream);
+  }
+  MsaRoundConsts R;
+  R.inv_hx = (float)(1.0 / x->hx);
+  R.inv_hy = (float)(1.0 / x->hy);
+  R.inv_rho = (float)(1.0 / x->rho_cur);
+  R.thr = (float)(P.beta / x->rho_cur);
+  R.gamma = (float)P.gamma;
+  R.rho = x->rho_cur;
+  R.beta = P.beta;
+  R.alpha = P.alpha;
+  int nblk = 0;
+  CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->mu, x->I, x->mu, x->partials, &nblk, x->stream));
+  CUDA_TRY(msa_launch_reduce(x->partials, x->g.nb, nblk, x->sums, x->stream));
+  x->launches += 2;
+  if (P.world > 1 && P.shard == MSA_SHARD_ROWS)
+    NCCL_TRY(g_nccl.AllReduce(x->sums, x->sums, MSA_NSUM, ncclDouble, ncclSum, x->comm, x->stream));
+  if (x->rec_pending >= REC_CAP) {
+    int r2 = fetch_records(x);
+    if (r2 != MSA_OK) return r2;
+  }
+  MsaRecordArgs a;
+  a.w = x->hx * x->hy;
+  a.beta = P.beta;
+  a.alpha = P.alpha;
+  a.rho = x->rho_cur;
+  const bool rows = P.world > 1 && P.shard == MSA_SHARD_ROWS;
+  a.npx = (double)(rows ? P.height : x->g.nrows) * P.width * x->g.nb;
+  a.C = P.channels;
+  a.round = x->rounds_done;
+  a.images = x->g.nb;
+  a.iters = x->iters_done;
+  CUDA_TRY(msa_launch_record(x->sums, a, x->d_rec + x->rec_pending, x->stream));
+  x->launches += 1;
+  if (x->timing) {
+    cudaEventRecord(e1, x->stream);
+    x->round_ev.push_back({e0, e1});
+    ++x->round_launches_t;
+  }
+  ++x->rec_pending;
+  ++x->rounds_done;
+  x->rho_cur *= P.kappa;  // R9
+  x->halo_mu_dirty = true;
+  return MSA_OK;
+}
+
+int do_steps(msa_ctx* x, int64_t n) {
+  const msa_params& P = x->prm;
+  const int K = P.iters_per_round;
+  MsaIterConsts KC = iter_consts(x, x->rho_cur);
+  int rc;
+  for (int64_t t = 0; t < n; ++t) {
+    const int s = x->cur, o = 1 - s;
+    if (P.world > 1 && P.shard == MSA_SHARD_ROWS) {
+      if ((rc = halo_exchange(x, true, true, true, x->halo_mu_dirty)) != MSA_OK) return rc;
+      x->halo_mu_dirty = false;
+    }
+    iter_batch_begin(x);
+    int launched = 0;
+    cudaError_t e = msa_launch_iter_fast(x->g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
+                                         x->cb[o], x->p[o], x->stream, &launched);
+    if (!launched) {
+      if (e != cudaErrorNotSupported && e != cudaSuccess)
+        return set_err(MSA_ECUDA, "fast iteration kernel: %s", cudaGetErrorString(e));
+      e = msa_launch_iter_generic(x->g, KC, x->d_off, x->d_om, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
+                                  x->cb[o], x->p[o], x->stream);
+    }
+    if (e != cudaSuccess) return set_err(MSA_ECUDA, "iteration kernel launch: %s", cudaGetErrorString(e));
+    ++x->launches;
+    if (x->timing) ++x->iter_launches_t;
+    x->cur = o;
+    ++x->iters_done;
+    if (x->iters_done % K == 0) {
+      iter_batch_end(x);
+      if ((rc = do_round(x)) != MSA_OK) return rc;
+      KC = iter_consts(x, x->rho_cur);
+    }
+  }
+  iter_batch_end(x);
+  return MSA_OK;
+}
+
+int upload_image(msa_ctx* x, const float* image, int on_device) {
+  const msa_params& P = x->prm;
+  const MsaGeom& g = x->g;
+  const int C = P.channels;
+  const int r_lo = std::max(0, g.row0 - g.G), r_hi = std::min(P.height, g.row0 + g.nrows + g.G);
+  const size_t rows = (size_t)(r_hi - r_lo);
+  const size_t per_img = rows * P.width * C;
+  float* stage = x->c[1 - x->cur];  // idle set: >= 4C planes per image, enough for C interleaved planes
+  for (int b = 0; b < g.nb; ++b) {
+    const float* src = image + ((size_t)(x->image0 + b) * P.height + r_lo) * P.width * C;
+    CUDA_TRY(cudaMemcpyAsync(stage + per_img * b, src, per_img * sizeof(float),
+                             on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, x->stream));
+  }
+  MsaGeom sg = sub_geom(g, r_lo, r_hi);
+  CUDA_TRY(msa_launch_unpack(sg, C, stage, x->I, x->stream));
+  ++x->launches;
+  const int s = x->cur;
+  CUDA_TRY(cudaMemcpyAsync(x->c[s], x->I, x->g.nb * (size_t)C * g.plane * sizeof(float), cudaMemcpyDeviceToDevice, x->stream));
+  CUDA_TRY(cudaMemcpyAsync(x->cb[s], x->I, x->g.nb * (size_t)C * g.plane * sizeof(float), cudaMemcpyDeviceToDevice, x->stream));
+  CUDA_TRY(cudaMemsetAsync(x->p[s], 0, x->g.nb * (size_t)2 * C * g.plane * sizeof(float), x->stream));
+  CUDA_TRY(cudaMemsetAsync(x->mu, 0, x->g.nb * (size_t)2 * C * g.plane * sizeof(float), x->stream));
+  x->rho_cur = P.rho;
+  x->iters_done = 0;
+  x->rounds_done = 0;
+  x->rec_pending = 0;
+  x->stats.clear();
+  x->halo_mu_dirty = true;
+  return MSA_OK;
+}
+
+void free_ctx(msa_ctx* x) {
+  if (!x) return;
+  if (x->stream) cudaStreamSynchronize(x->stream);
+  for (auto& e : x->iter_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  for (auto& e : x->round_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  if (x->comm) g_nccl.CommDestroy(x->comm);
+  msa_labels_free(x->lab);
+  if (x->lab_buf) cudaFree(x->lab_buf);
+  if (x->lab_count) cudaFree(x->lab_count);
+  if (x->lab_pal) cudaFree(x->lab_pal);
+  if (x->own_ws && x->ws) cudaFree(x->ws);
+  if (x->own_stream && x->stream) cudaStreamDestroy(x->stream);
+  delete x;
+}
+
+}  // namespace
+
+// ================================================================== ABI
+extern "C" {
+
+int msa_abi_version(void) { return MSA_ABI_VERSION; }
+const char* msa_last_error(void) { return g_err; }
+
+int msa_partition_rows(int32_t height, int32_t world, int32_t rank, int32_t radius, int32_t* row0, int32_t* nrows,
+                       int32_t* ghost_rows) {
+  if (height < 1 || world < 1 || rank < 0 || rank >= world || radius < 0) return set_err(MSA_EINVAL, "bad partition args");
+  msa_params p{};
+  p.height = height;
+  p.batch = 1;
+  p.world = world;
+  p.rank = rank;
+  p.radius = radius;
+  p.shard = MSA_SHARD_ROWS;
+  Part pt = partition(&p);
+  if (world > 1 && height / world < std::max(radius, 1)) return set_err(MSA_EINVAL, "slabs too thin for the radius");
+  if (row0) *row0 = pt.row0;
+  if (nrows) *nrows = pt.nrows;
+  if (ghost_rows) *ghost_rows = pt.ghost;
+  return MSA_OK;
+}
+
+int msa_workspace_bytes(const msa_params* params, size_t* bytes) {
+  int rc = validate(params);
+  if (rc != MSA_OK) return rc;
+  if (!bytes) return set_err(MSA_EINVAL, "bytes is NULL");
+  Part pt = partition(params);
+  *bytes = layout(params, pt).total;
+  return MSA_OK;
+}
+
+int msa_nccl_unique_id(void* out128) {
+  if (!out128) return set_err(MSA_EINVAL, "out is NULL");
+  if (!nccl_load()) return set_err(MSA_ENCCL, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  NCCL_TRY(g_nccl.GetUniqueId(&id));
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  memcpy(out128, &id, 128);
+  return MSA_OK;
+}
+
+int msa_init(const msa_params* params, const float* image, int image_on_device, void* workspace,
+             size_t workspace_bytes, void* stream, msa_ctx** out) {
+  int rc = validate(params);
+  if (rc != MSA_OK) return rc;
+  if (!image || !out) return set_err(MSA_EINVAL, "image and out must not be NULL");
+  Derived d;
+  if ((rc = derive(params, &d)) != MSA_OK) return rc;
+  CUDA_TRY(cudaSetDevice(params->device));
+  msa_ctx* x = new msa_ctx();
+  x->prm = *params;
+  x->prm.nccl_id = nullptr;
+  x->hx = d.hx; x->hy = d.hy; x->eps_x = d.eps_x; x->tau = d.tau; x->sigma = d.sigma; x->theta = d.theta;
+  x->NR = d.NR;
+  x->T = d.T;
+  Part pt = partition(params);
+  Layout L = layout(params, pt);
+  x->image0 = pt.image0;
+  x->g.H = params->height; x->g.W = params->width; x->g.row0 = pt.row0; x->g.nrows = pt.nrows; x->g.G = pt.ghost;
+  x->g.pitch = L.pitch; x->g.plane = (long long)L.plane_floats; x->g.nb = pt.nimages; x->g.C = params->channels;
+  auto fail = [&](int code) { free_ctx(x); return code; };
+  if (stream) {
+    x->stream = (cudaStream_t)stream;
+  } else {
+    cudaError_t e = cudaStreamCreateWithFlags(&x->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return fail(set_err(MSA_ECUDA, "cudaStreamCreate: %s", cudaGetErrorString(e)));
+    x->own_stream = true;
+  }
+  if (workspace) {
+    if (workspace_bytes < L.total)
+      return fail(set_err(MSA_ENOMEM, "workspace too small: %zu < %zu bytes", workspace_bytes, L.total));
+    if (((uintptr_t)workspace) % 256 != 0) return fail(set_err(MSA_EINVAL, "workspace must be 256-byte aligned"));
+    x->ws = (char*)workspace;
+  } else {
+    cudaError_t e = cudaMalloc((void**)&x->ws, L.total);
+    if (e != cudaSuccess) return fail(set_err(MSA_ENOMEM, "cudaMalloc(%zu): %s", L.total, cudaGetErrorString(e)));
+    x->own_ws = true;
+  }
+  x->ws_bytes = L.total;
+  x->I = (float*)(x->ws + L.off_I);
+  x->mu = (float*)(x->ws + L.off_mu);
+  for (int s = 0; s < 2; ++s) {
+    x->c[s] = (float*)(x->ws + L.off_set[s]);
+    x->cb[s] = x->c[s] + L.f1;
+    x->p[s] = x->cb[s] + L.f1;
+  }
+  x->partials = (double*)(x->ws + L.off_partials);
+  x->sums = (double*)(x->ws + L.off_sums);
+  x->d_off = (int2*)(x->ws + L.off_off);
+  x->d_om = (float*)(x->ws + L.off_om);
+  x->d_rec = (msa_round_stats*)(x->ws + L.off_rec);
+  // zero the workspace (ghost rows of the outer slabs stay defined), then the offset table
+  std::vector<int2> offs(std::max(x->T.n, 1));
+  for (int o = 0; o < x->T.n; ++o) offs[o] = make_int2(x->T.dx[o], x->T.dy[o]);
+  {
+    cudaError_t e = cudaMemsetAsync(x->ws, 0, L.total, x->stream);
+    if (e == cudaSuccess && x->T.n > 0)
+      e = cudaMemcpyAsync(x->d_off, offs.data(), sizeof(int2) * x->T.n, cudaMemcpyHostToDevice, x->stream);
+    if (e == cudaSuccess && x->T.n > 0)
+      e = cudaMemcpyAsync(x->d_om, x->T.om, sizeof(float) * x->T.n, cudaMemcpyHostToDevice, x->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);  // offs is a host temporary
+    if (e != cudaSuccess) return fail(set_err(MSA_ECUDA, "init copies: %s", cudaGetErrorString(e)));
+  }
+  if (params->world > 1 && params->shard == MSA_SHARD_ROWS) {
+    if (!nccl_load()) return fail(set_err(MSA_ENCCL, "libnccl.so.2 could not be loaded"));
+    ncclUniqueId id;
+    memcpy(&id, params->nccl_id, sizeof(id));
+    ncclResult_t r = g_nccl.CommInitRank(&x->comm, params->world, id, params->rank);
+    if (r != ncclSuccess) return fail(set_err(MSA_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)));
+  }
+  if ((rc = upload_image(x, image, image_on_device)) != MSA_OK) return fail(rc);
+  cudaError_t e = cudaStreamSynchronize(x->stream);
+  if (e != cudaSuccess) return fail(set_err(MSA_ECUDA, "init: %s", cudaGetErrorString(e)));
+  *out = x;
+  return MSA_OK;
+}
+
+int msa_reset(msa_ctx* x, const float* image, int image_on_device) {
+  if (!x || !image) return set_err(MSA_EINVAL, "NULL argument");
+  return upload_image(x, image, image_on_device);
+}
+
+int msa_step(msa_ctx* x, int32_t n_iters) {
+  if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
+  if (n_iters < 0) return set_err(MSA_EINVAL, "n_iters must be >= 0");
+  return do_steps(x, n_iters);
+}
+
+int msa_solve(msa_ctx* x, msa_round_stats* stats) {
+  if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
+  const size_t before = x->stats.size() + x->rec_pending;
+  int rc = do_steps(x, (int64_t)x->prm.rounds * x->prm.iters_per_round);
+  if (rc != MSA_OK) return rc;
+  if ((rc = fetch_records(x)) != MSA_OK) return rc;
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  int diverged = -1;
+  for (size_t r = before; r < x->stats.size(); ++r) {
+    if (stats) stats[r - before] = x->stats[r];
+    if (diverged < 0 && x->stats[r].nonfinite > 0) diverged = x->stats[r].round;
+  }
+  if (diverged >= 0) return set_err(MSA_EDIVERGED, "integration diverged: non-finite colour at round %d", diverged);
+  return MSA_OK;
+}
+
+int msa_labels(msa_ctx* x, float delta, int32_t* labels, int32_t* n_clusters, float* palette, int32_t max_k,
+               int out_on_device) {
+  if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
+  if (!(delta >= 0) || !isfinite(delta)) return set_err(MSA_EINVAL, "delta must be finite and >= 0");
+  if (!labels || !n_clusters) return set_err(MSA_EINVAL, "labels and n_clusters must not be NULL");
+  if (max_k < 0 || (max_k > 0 && !palette)) return set_err(MSA_EINVAL, "palette needs max_k > 0 and a buffer");
+  if (x->prm.world > 1 && x->prm.shard == MSA_SHARD_ROWS)
+    return set_err(MSA_EINVAL, "labels need the whole image on one rank (rows mode with world > 1 unsupported)");
+  const MsaGeom& g = x->g;
+  const size_t N = (size_t)g.H * g.W;
+  const int C = g.C;
+  if (!out_on_device && !x->lab_buf) CUDA_TRY(cudaMalloc((void**)&x->lab_buf, N * sizeof(int32_t)));
+  if (!x->lab_count) CUDA_TRY(cudaMalloc((void**)&x->lab_count, sizeof(int32_t) * 2));
+  if (max_k > 0 && !out_on_device && x->lab_pal_cap < max_k) {
+    if (x->lab_pal) cudaFree(x->lab_pal);
+    CUDA_TRY(cudaMalloc((void**)&x->lab_pal, sizeof(float) * (size_t)max_k * C));
+    x->lab_pal_cap = max_k;
+  }
+  for (int b = 0; b < g.nb; ++b) {
+    int32_t* ldev = out_on_device ? labels + N * b : x->lab_buf;
+    int32_t* cdev = out_on_device ? n_clusters + b : x->lab_count;
+    float* pdev = max_k > 0 ? (out_on_device ? palette + (size_t)b * max_k * C : x->lab_pal) : nullptr;
+    long long launches = 0;
+    cudaError_t e = msa_labels_image(g, x->c[x->cur], b, delta, ldev, cdev, pdev, max_k, &x->lab, x->stream, &launches);
+    x->launches += launches;
+    if (e != cudaSuccess) return set_err(MSA_ECUDA, "labels: %s", cudaGetErrorString(e));
+    if (!out_on_device) {
+      CUDA_TRY(cudaMemcpyAsync(labels + N * b, ldev, N * sizeof(int32_t), cudaMemcpyDeviceToHost, x->stream));
+      CUDA_TRY(cudaMemcpyAsync(n_clusters + b, cdev, sizeof(int32_t), cudaMemcpyDeviceToHost, x->stream));
+      if (max_k > 0)
+        CUDA_TRY(cudaMemcpyAsync(palette + (size_t)b * max_k * C, pdev, sizeof(float) * (size_t)max_k * C,
+                                 cudaMemcpyDeviceToHost, x->stream));
+      CUDA_TRY(cudaStreamSynchronize(x->stream));  // host buffers reused per image
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  return MSA_OK;
+}
+
+int msa_get_field(msa_ctx* x, int32_t which, float* out, int out_on_device, int32_t* row0, int32_t* nrows) {
+  if (!x || !out) return set_err(MSA_EINVAL, "NULL argument");
+  if (which < MSA_FIELD_C || which > MSA_FIELD_I) return set_err(MSA_EINVAL, "bad field id");
+  const int nm = field_nm(x, which);
+  float* f = field_ptr(x, which, x->cur);
+  float* stage = x->c[1 - x->cur];
+  CUDA_TRY(msa_launch_pack(x->g, nm, f, out_on_device ? out : stage, x->stream));
+  ++x->launches;
+  if (!out_on_device) {
+    const size_t n = (size_t)x->g.nb * x->g.nrows * x->g.W * nm;
+    CUDA_TRY(cudaMemcpyAsync(out, stage, n * sizeof(float), cudaMemcpyDeviceToHost, x->stream));
+  }
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  if (row0) *row0 = x->g.row0;
+  if (nrows) *nrows = x->g.nrows;
+  return MSA_OK;
+}
+
+int msa_set_field(msa_ctx* x, int32_t which, const float* in, int in_on_device) {
+  if (!x || !in) return set_err(MSA_EINVAL, "NULL argument");
+  if (which < MSA_FIELD_C || which > MSA_FIELD_I) return set_err(MSA_EINVAL, "bad field id");
+  const int nm = field_nm(x, which);
+  float* f = field_ptr(x, which, x->cur);
+  float* stage = x->c[1 - x->cur];
+  const size_t n = (size_t)x->g.nb * x->g.nrows * x->g.W * nm;
+  CUDA_TRY(cudaMemcpyAsync(stage, in, n * sizeof(float), in_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                           x->stream));
+  CUDA_TRY(msa_launch_unpack(x->g, nm, stage, f, x->stream));
+  ++x->launches;
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  if (which == MSA_FIELD_MU) x->halo_mu_dirty = true;
+  return MSA_OK;
+}
+
+int msa_get_stats(msa_ctx* x, msa_round_stats* out, int32_t max, int32_t* n) {
+  if (!x || !n) return set_err(MSA_EINVAL, "NULL argument");
+  int rc = fetch_records(x);
+  if (rc != MSA_OK) return rc;
+  *n = (int32_t)x->stats.size();
+  if (out)
+    for (int32_t r = 0; r < std::min(max, *n); ++r) out[r] = x->stats[r];
+  return MSA_OK;
+}
+
+// state blob: header + fields c, cbar, p, mu, I (owned rows, ABI layout)
+struct StateHeader {
+  uint64_t magic;
+  int32_t version, B, H, W, C, nb, row0, nrows;
+  int64_t iters_done;
+  int32_t rounds_done, pad;
+  double rho_cur;
+};
+static const uint64_t kStateMagic = 0x3153544154534d41ULL;  // "AMSTATS1"
+
+int msa_state_bytes(msa_ctx* x, size_t* bytes) {
+  if (!x || !bytes) return set_err(MSA_EINVAL, "NULL argument");
+  const size_t per = (size_t)x->g.nb * x->g.nrows * x->g.W * x->g.C;
+  *bytes = sizeof(StateHeader) + per * 7 * sizeof(float);  // c, cbar, I (C) + p, mu (2C)
+  return MSA_OK;
+}
+
+int msa_get_state(msa_ctx* x, void* blob, size_t bytes) {
+  size_t need;
+  int rc = msa_state_bytes(x, &need);
+  if (rc != MSA_OK) return rc;
+  if (!blob || bytes < need) return set_err(MSA_EINVAL, "state buffer too small (%zu < %zu)", bytes, need);
+  if ((rc = fetch_records(x)) != MSA_OK) return rc;
+  StateHeader h{kStateMagic, 1, x->prm.batch, x->prm.height, x->prm.width, x->prm.channels, x->g.nb, x->g.row0,
+                x->g.nrows, x->iters_done, x->rounds_done, 0, x->rho_cur};
+  memcpy(blob, &h, sizeof(h));
+  float* f = (float*)((char*)blob + sizeof(h));
+  const size_t per = (size_t)x->g.nb * x->g.nrows * x->g.W * x->g.C;
+  const int order[5] = {MSA_FIELD_C, MSA_FIELD_CBAR, MSA_FIELD_P, MSA_FIELD_MU, MSA_FIELD_I};
+  for (int which : order) {
+    if ((rc = msa_get_field(x, which, f, 0, nullptr, nullptr)) != MSA_OK) return rc;
+    f += per * (size_t)field_nm(x, which) / x->g.C;
+  }
+  return MSA_OK;
+}
+
+int msa_set_state(msa_ctx* x, const void* blob, size_t bytes) {
+  size_t need;
+  int rc = msa_state_bytes(x, &need);
+  if (rc != MSA_OK) return rc;
+  if (!blob || bytes < need) return set_err(MSA_EINVAL, "state buffer too small (%zu < %zu)", bytes, need);
+  StateHeader h;
+  memcpy(&h, blob, sizeof(h));
+  if (h.magic != kStateMagic || h.version != 1 || h.B != x->prm.batch || h.H != x->prm.height ||
+      h.W != x->prm.width || h.C != x->prm.channels || h.nb != x->g.nb || h.row0 != x->g.row0 || h.nrows != x->g.nrows)
+    return set_err(MSA_EINVAL, "state blob does not match this context");
+  const float* f = (const float*)((const char*)blob + sizeof(h));
+  const size_t per = (size_t)x->g.nb * x->g.nrows * x->g.W * x->g.C;
+  const int order[5] = {MSA_FIELD_C, MSA_FIELD_CBAR, MSA_FIELD_P, MSA_FIELD_MU, MSA_FIELD_I};
+  for (int which : order) {
+    if ((rc = msa_set_field(x, which, f, 0)) != MSA_OK) return rc;
+    f += per * (size_t)field_nm(x, which) / x->g.C;
+  }
+  x->iters_done = h.iters_done;
+  x->rounds_done = h.rounds_done;
+  x->rho_cur = h.rho_cur;
+  x->rec_pending = 0;
+  x->halo_mu_dirty = true;
+  return MSA_OK;
+}
+
+int msa_query(msa_ctx* x, msa_info* info) {
+  if (!x || !info) return set_err(MSA_EINVAL, "NULL argument");
+  info->row0 = x->g.row0;
+  info->nrows = x->g.nrows;
+  info->image0 = x->image0;
+  info->nimages = x->g.nb;
+  info->ghost_rows = x->g.G;
+  info->pitch = x->g.pitch;
+  info->hx = x->hx;
+  info->hy = x->hy;
+  info->eps_x = x->eps_x;
+  info->tau = x->tau;
+  info->sigma = x->sigma;
+  info->theta = x->theta;
+  info->window_size = x->NR;
+  info->active_offsets = x->T.n;
+  info->iters_done = x->iters_done;
+  info->launches = x->launches;
+  info->rho = x->rho_cur;
+  return MSA_OK;
+}
+
+int msa_set_timing(msa_ctx* x, int enable) {
+  if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  for (auto& e : x->iter_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  for (auto& e : x->round_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  x->iter_ev.clear();
+  x->round_ev.clear();
+  x->iter_launches_t = x->round_launches_t = 0;
+  x->in_iter_batch = false;
+  x->timing = enable != 0;
+  return MSA_OK;
+}
+
+int msa_get_timing(msa_ctx* x, double* iter_ms, int64_t* iter_launches, double* round_ms, int64_t* round_launches) {
+  if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  double it = 0, rd = 0;
+  for (auto& e : x->iter_ev) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+    it += ms;
+  }
+  for (auto& e : x->round_ev) {
+    float ms = 0;
+    CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+    rd += ms;
+  }
+  if (iter_ms) *iter_ms = it;
+  if (round_ms) *round_ms = rd;
+  if (iter_launches) *iter_launches = x->iter_launches_t;
+  if (round_launches) *round_launches = x->round_launches_t;
+  return MSA_OK;
+}
+
+int msa_sync(msa_ctx* x) {
+  if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  return MSA_OK;
+}
+
+int msa_free(msa_ctx* x) {
+  if (!x) return MSA_OK;
+  free_ctx(x);
+  return MSA_OK;
+}
+
+}  // extern "C"

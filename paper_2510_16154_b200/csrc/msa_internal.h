@@ -1,0 +1,52 @@
+// msa_internal.h - host-side launcher interface between the C-ABI driver
+// (msa_driver.cu) and the kernel translation units. Not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "msa_common.cuh"
+
+struct MsaOffsetTable {
+  int n;                   // active offsets
+  int dx[MSA_MAXOFF], dy[MSA_MAXOFF];
+  float om[MSA_MAXOFF];    // 1 - a_delta, a_delta = eps_x/2 ((dx h_x)^2 + (dy h_y)^2)
+};
+
+// Generic kernels (msa_kernels.cu): any C in [1,16], any R in [0,8].
+cudaError_t msa_launch_iter_generic(const MsaGeom& g, const MsaIterConsts& K, const int2* d_off, const float* d_om,
+                                    const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                                    float* c_out, float* cb_out, float* p_out, cudaStream_t s);
+
+// Specialised fused iteration (msa_iter_fast.cu). Returns cudaErrorNotSupported (without
+// launching) when no specialisation covers (C, R, kernel, offset set).
+cudaError_t msa_launch_iter_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                                 const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                                 float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched);
+
+// Round update (steps 4-5): writes mu_out (may alias mu) and per-block fp64 partial sums
+// [nb][nblk][MSA_NSUM]; *nblk receives the number of blocks per image.
+cudaError_t msa_launch_round(const MsaGeom& g, const MsaRoundConsts& R, const float* c, const float* p,
+                             const float* mu, const float* I, float* mu_out, double* partials, int* nblk,
+                             cudaStream_t s);
+int msa_round_blocks(const MsaGeom& g);
+// Deterministic sum of the partials over blocks and over images -> sums[MSA_NSUM].
+cudaError_t msa_launch_reduce(const double* partials, int nb, int nblk, double* sums, cudaStream_t s);
+
+struct MsaRecordArgs {
+  double w, beta, alpha, rho, npx;
+  int C, round, images;
+  long long iters;
+};
+// sums[MSA_NSUM] -> one msa_round_stats record (device).
+cudaError_t msa_launch_record(const double* sums, MsaRecordArgs a, void* record, cudaStream_t s);
+
+// Layout conversions: interleaved [nb][rows][W][nm] <-> planar field (owned rows only).
+cudaError_t msa_launch_pack(const MsaGeom& g, int nm, const float* planar, float* inter, cudaStream_t s);
+cudaError_t msa_launch_unpack(const MsaGeom& g, int nm, const float* inter, float* planar, cudaStream_t s);
+
+// Labels (msa_labels.cu): Q(c; delta) of reading R16 on image b of the planar field c.
+struct MsaLabelScratch;
+cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delta, int32_t* labels_dev,
+                             int32_t* count_dev, float* palette_dev, int max_k, MsaLabelScratch** scratch,
+                             cudaStream_t s, long long* launches);
+void msa_labels_free(MsaLabelScratch* s);

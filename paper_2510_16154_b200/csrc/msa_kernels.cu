@@ -1,0 +1,309 @@
+// msa_kernels.cu - generic (any C <= 16, any R <= 8) sm_100a kernels of the msa hot path:
+//   K1g  msa_iter_generic   one thread per pixel, neighbours read through L1 (fallback and
+//                           bitwise reference for the specialised K1 in msa_iter_fast.cu)
+//   K2   msa_round          multiplier round (steps 4-5) + per-block fp64 partial sums
+//   K3   msa_reduce/record  deterministic reduction of the partials into a round record
+//   pack/unpack             interleaved ABI layout <-> planar device layout
+// Passages: see include/msa.h and DESIGN.md §1.
+#include <math.h>
+
+#include "../../include/msa.h"
+#include "msa_internal.h"
+
+namespace {
+
+// ------------------------------------------------------------------ K1 generic
+template <int C, int KER>
+__global__ void __launch_bounds__(256) k_iter_generic(MsaGeom g, MsaIterConsts K, const int2* __restrict__ off,
+                                                      const float* __restrict__ om, const float* __restrict__ c,
+                                                      const float* __restrict__ cb, const float* __restrict__ p,
+                                                      const float* __restrict__ mu, const float* __restrict__ I,
+                                                      float* __restrict__ c_out, float* __restrict__ cb_out,
+                                                      float* __restrict__ p_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  const int b = blockIdx.z;
+  if (i >= g.W || jl >= g.nrows) return;
+  const int j = g.row0 + jl;
+  const int W = g.W, H = g.H;
+  // step 1: agent Euler step (eq:MAsystem windowed, R2)
+  float ci[C], acc[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    ci[k] = c[msa_idx(g, b, k, C, j, i)];
+    acc[k] = 0.0f;
+  }
+  for (int o = 0; o < K.n_off; ++o) {
+    const int2 d = off[o];
+    const int ii = i + d.x, jj = j + d.y;
+    if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue; // excluded, not padded (R20)
+    float cj[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) cj[k] = c[msa_idx(g, b, k, C, jj, ii)];
+    msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
+  }
+  float chalf[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+  // step 2: p+ at (i,j), (i-1,j), (i,j-1); the last two only feed the divergence
+  float qx[3][C], qy[3][C];
+  const int pi[3] = {i, i - 1, i};
+  const int pj[3] = {j, j, j - 1};
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const int a = pi[s], bj = pj[s];
+    if (a < 0 || bj < 0) {
+#pragma unroll
+      for (int k = 0; k < C; ++k) qx[s][k] = qy[s][k] = 0.0f;
+      continue;
+    }
+    float gx[C], gy[C], px[C], py[C], mx[C], my[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const float c0 = cb[msa_idx(g, b, k, C, bj, a)];
+      gx[k] = a < W - 1 ? __fmul_rn(__fsub_rn(cb[msa_idx(g, b, k, C, bj, a + 1)], c0), K.inv_hx) : 0.0f;
+      gy[k] = bj < H - 1 ? __fmul_rn(__fsub_rn(cb[msa_idx(g, b, k, C, bj + 1, a)], c0), K.inv_hy) : 0.0f;
+      px[k] = p[msa_idx(g, b, k, 2 * C, bj, a)];
+      py[k] = p[msa_idx(g, b, C + k, 2 * C, bj, a)];
+      mx[k] = mu[msa_idx(g, b, k, 2 * C, bj, a)];
+      my[k] = mu[msa_idx(g, b, C + k, 2 * C, bj, a)];
+    }
+    msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx[s], qy[s]);
+  }
+  // step 3: d = div p+ (negative adjoint of the forward gradient, R6), prox, extrapolation
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    float ax = i < W - 1 ? qx[0][k] : 0.0f;
+    if (i > 0) ax = __fsub_rn(ax, qx[1][k]);
+    float ay = j < H - 1 ? qy[0][k] : 0.0f;
+    if (j > 0) ay = __fsub_rn(ay, qy[2][k]);
+    const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
+    float cp, cbp;
+    msa_prox_extrap(K, chalf[k], d, I[msa_idx(g, b, k, C, j, i)], cp, cbp);
+    c_out[msa_idx(g, b, k, C, j, i)] = cp;
+    cb_out[msa_idx(g, b, k, C, j, i)] = cbp;
+    p_out[msa_idx(g, b, k, 2 * C, j, i)] = qx[0][k];
+    p_out[msa_idx(g, b, C + k, 2 * C, j, i)] = qy[0][k];
+  }
+}
+
+template <int C>
+cudaError_t launch_iter_generic_c(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
+                                  const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                                  float* co, float* cbo, float* po, cudaStream_t s) {
+  dim3 blk(32, 8), grd((g.W + 31) / 32, (g.nrows + 7) / 8, g.nb);
+  if (K.kernel == 0)
+    k_iter_generic<C, 0><<<grd, blk, 0, s>>>(g, K, off, om, c, cb, p, mu, I, co, cbo, po);
+  else
+    k_iter_generic<C, 1><<<grd, blk, 0, s>>>(g, K, off, om, c, cb, p, mu, I, co, cbo, po);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ K2 round
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int C>
+__global__ void __launch_bounds__(256) k_round(MsaGeom g, MsaRoundConsts R, const float* __restrict__ c,
+                                               const float* __restrict__ p, const float* mu,
+                                               const float* __restrict__ I, float* mu_out,
+                                               double* __restrict__ partials) {
+  constexpr int NS = MSA_S_MEAN0 + C;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  const int b = blockIdx.z;
+  double acc[NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+  if (i < g.W && jl < g.nrows) {
+    const int j = g.row0 + jl, W = g.W, H = g.H;
+    float gv[2 * C], mv[2 * C], pv[2 * C], a[2 * C];
+    float a2 = 0.0f, g2 = 0.0f;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const float c0 = c[msa_idx(g, b, k, C, j, i)];
+      gv[k] = i < W - 1 ? __fmul_rn(__fsub_rn(c[msa_idx(g, b, k, C, j, i + 1)], c0), R.inv_hx) : 0.0f;
+      gv[C + k] = j < H - 1 ? __fmul_rn(__fsub_rn(c[msa_idx(g, b, k, C, j + 1, i)], c0), R.inv_hy) : 0.0f;
+      const float Ik = I[msa_idx(g, b, k, C, j, i)];
+      const double r = (double)c0 - (double)Ik;
+      acc[MSA_S_FID] += r * r;
+      acc[MSA_S_MEAN0 + k] += (double)c0;
+      if (!isfinite(c0)) acc[MSA_S_NONFIN] += 1.0;
+      // div p (R6) for the dual value
+      float ax = i < W - 1 ? p[msa_idx(g, b, k, 2 * C, j, i)] : 0.0f;
+      if (i > 0) ax = __fsub_rn(ax, p[msa_idx(g, b, k, 2 * C, j, i - 1)]);
+      float ay = j < H - 1 ? p[msa_idx(g, b, C + k, 2 * C, j, i)] : 0.0f;
+      if (j > 0) ay = __fsub_rn(ay, p[msa_idx(g, b, C + k, 2 * C, j - 1, i)]);
+      const double dv = (double)__fadd_rn(__fmul_rn(ax, R.inv_hx), __fmul_rn(ay, R.inv_hy));
+      acc[MSA_S_IDP] += (double)Ik * dv;
+      acc[MSA_S_DP2] += dv * dv;
+    }
+#pragma unroll
+    for (int m = 0; m < 2 * C; ++m) {
+      mv[m] = mu[msa_idx(g, b, m, 2 * C, j, i)];
+      pv[m] = p[msa_idx(g, b, m, 2 * C, j, i)];
+      a[m] = __fmaf_rn(-R.inv_rho, mv[m], gv[m]);   // a = grad c - mu/rho
+      a2 = __fmaf_rn(a[m], a[m], a2);
+      g2 = __fmaf_rn(gv[m], gv[m], g2);
+      acc[MSA_S_MUP] += (double)mv[m] * (double)pv[m];
+      acc[MSA_S_PP] += (double)pv[m] * (double)pv[m];
+    }
+    // v = S_{beta/rho}(a) (eq:soft_threshold), mu+ = mu + gamma (v - grad c) (Alg. 2 line 7)
+    const float na = __fsqrt_rn(a2);
+    const float f = na > R.thr ? __fsub_rn(1.0f, __fdiv_rn(R.thr, na)) : 0.0f;
+    double res = 0.0;
+#pragma unroll
+    for (int m = 0; m < 2 * C; ++m) {
+      const float v = __fmul_rn(f, a[m]);
+      const float vg = __fsub_rn(v, gv[m]);
+      res += (double)vg * (double)vg;
+      mu_out[msa_idx(g, b, m, 2 * C, j, i)] = __fmaf_rn(R.gamma, vg, mv[m]);
+    }
+    acc[MSA_S_RES] += res;
+    acc[MSA_S_TV] += sqrt((double)g2);
+    const double nad = (double)na;
+    acc[MSA_S_HUB] += nad <= R.beta / R.rho ? 0.5 * R.rho * nad * nad : R.beta * nad - R.beta * R.beta / (2.0 * R.rho);
+  }
+  // block reduction (fixed order): warp shuffle, then warp 0 over the warps
+  __shared__ double red[8][NS];
+  const int lane = (threadIdx.y * blockDim.x + threadIdx.x) & 31, warp = (threadIdx.y * blockDim.x + threadIdx.x) >> 5;
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    double v = warp_sum(acc[s]);
+    if (lane == 0) red[warp][s] = v;
+  }
+  __syncthreads();
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  if (tid < NS) {
+    double v = 0.0;
+    for (int w = 0; w < 8; ++w) v += red[w][tid];
+    const long long blk = (long long)blockIdx.y * gridDim.x + blockIdx.x;
+    const long long nblk = (long long)gridDim.x * gridDim.y;
+    partials[((long long)b * nblk + blk) * MSA_NSUM + tid] = v;
+  }
+}
+
+// ------------------------------------------------------------------ K3 reduce + record
+__global__ void __launch_bounds__(256) k_reduce(const double* __restrict__ partials, int total, double* sums) {
+  // block s sums column s over all (image, block) rows in a fixed order
+  const int s = blockIdx.x;
+  double v = 0.0;
+  for (int r = threadIdx.x; r < total; r += blockDim.x) v += partials[(long long)r * MSA_NSUM + s];
+  __shared__ double red[8];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    sums[s] = t;
+  }
+}
+
+__global__ void k_record(const double* __restrict__ S, MsaRecordArgs a, msa_round_stats* rec) {
+  if (threadIdx.x != 0) return;
+  msa_round_stats r;
+  r.round = a.round;
+  r.images = a.images;
+  r.iters = a.iters;
+  r.e_tv = a.w * a.beta * S[MSA_S_TV];
+  r.e_fid = 0.5 * a.alpha * a.w * S[MSA_S_FID];
+  r.primal = a.w * S[MSA_S_HUB] + r.e_fid;
+  r.dual = a.alpha > 0 ? -a.w * S[MSA_S_IDP] - a.w * S[MSA_S_DP2] / (2.0 * a.alpha) - a.w * S[MSA_S_MUP] / a.rho -
+                             a.w * S[MSA_S_PP] / (2.0 * a.rho)
+                       : __longlong_as_double(0x7ff8000000000000ULL);
+  r.gap = r.primal - r.dual;
+  r.al_residual = sqrt(a.w * S[MSA_S_RES]);
+  r.rho = a.rho;
+  r.nonfinite = S[MSA_S_NONFIN];
+  for (int k = 0; k < 16; ++k) r.mean[k] = k < a.C ? S[MSA_S_MEAN0 + k] / a.npx : 0.0;
+  *rec = r;
+}
+
+// ------------------------------------------------------------------ layout
+__global__ void k_pack(MsaGeom g, int nm, const float* __restrict__ planar, float* __restrict__ inter) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per = (long long)g.nrows * g.W * nm;
+  if (n >= per * g.nb) return;
+  const int b = (int)(n / per);
+  long long r = n % per;
+  const int m = (int)(r % nm);
+  r /= nm;
+  const int i = (int)(r % g.W), jl = (int)(r / g.W);
+  inter[n] = planar[msa_idx(g, b, m, nm, g.row0 + jl, i)];
+}
+__global__ void k_unpack(MsaGeom g, int nm, const float* __restrict__ inter, float* __restrict__ planar) {
+  const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long per = (long long)g.nrows * g.W * nm;
+  if (n >= per * g.nb) return;
+  const int b = (int)(n / per);
+  long long r = n % per;
+  const int m = (int)(r % nm);
+  r /= nm;
+  const int i = (int)(r % g.W), jl = (int)(r / g.W);
+  planar[msa_idx(g, b, m, nm, g.row0 + jl, i)] = inter[n];
+}
+
+}  // namespace
+
+cudaError_t msa_launch_iter_generic(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
+                                    const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                                    float* co, float* cbo, float* po, cudaStream_t s) {
+  switch (g.C) {
+#define MSA_CASE(CC) \
+  case CC:           \
+    return launch_iter_generic_c<CC>(g, K, off, om, c, cb, p, mu, I, co, cbo, po, s);
+    MSA_CASE(1) MSA_CASE(2) MSA_CASE(3) MSA_CASE(4) MSA_CASE(5) MSA_CASE(6) MSA_CASE(7) MSA_CASE(8)
+    MSA_CASE(9) MSA_CASE(10) MSA_CASE(11) MSA_CASE(12) MSA_CASE(13) MSA_CASE(14) MSA_CASE(15) MSA_CASE(16)
+#undef MSA_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+}
+
+int msa_round_blocks(const MsaGeom& g) { return ((g.W + 31) / 32) * ((g.nrows + 7) / 8); }
+
+cudaError_t msa_launch_round(const MsaGeom& g, const MsaRoundConsts& R, const float* c, const float* p,
+                             const float* mu, const float* I, float* mu_out, double* partials, int* nblk,
+                             cudaStream_t s) {
+  dim3 blk(32, 8), grd((g.W + 31) / 32, (g.nrows + 7) / 8, g.nb);
+  *nblk = (int)(grd.x * grd.y);
+  switch (g.C) {
+#define MSA_CASE(CC) \
+  case CC:           \
+    k_round<CC><<<grd, blk, 0, s>>>(g, R, c, p, mu, I, mu_out, partials); \
+    break;
+    MSA_CASE(1) MSA_CASE(2) MSA_CASE(3) MSA_CASE(4) MSA_CASE(5) MSA_CASE(6) MSA_CASE(7) MSA_CASE(8)
+    MSA_CASE(9) MSA_CASE(10) MSA_CASE(11) MSA_CASE(12) MSA_CASE(13) MSA_CASE(14) MSA_CASE(15) MSA_CASE(16)
+#undef MSA_CASE
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t msa_launch_reduce(const double* partials, int nb, int nblk, double* sums, cudaStream_t s) {
+  k_reduce<<<MSA_NSUM, 256, 0, s>>>(partials, nb * nblk, sums);
+  return cudaGetLastError();
+}
+
+cudaError_t msa_launch_record(const double* sums, MsaRecordArgs a, void* record, cudaStream_t s) {
+  k_record<<<1, 32, 0, s>>>(sums, a, (msa_round_stats*)record);
+  return cudaGetLastError();
+}
+
+cudaError_t msa_launch_pack(const MsaGeom& g, int nm, const float* planar, float* inter, cudaStream_t s) {
+  const long long n = (long long)g.nb * g.nrows * g.W * nm;
+  if (n == 0) return cudaSuccess;
+  k_pack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, nm, planar, inter);
+  return cudaGetLastError();
+}
+cudaError_t msa_launch_unpack(const MsaGeom& g, int nm, const float* inter, float* planar, cudaStream_t s) {
+  const long long n = (long long)g.nb * g.nrows * g.W * nm;
+  if (n == 0) return cudaSuccess;
+  k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, nm, inter, planar);
+  return cudaGetLastError();
+}

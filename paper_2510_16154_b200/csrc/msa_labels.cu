@@ -1,0 +1,378 @@
+// msa_labels.cu - K4: the quantisation rule Q(c; delta) of reading R16 on the GPU.
+//   (i)   lock-free union-find over 4-neighbour edges with max_k |c_a,k - c_b,k| <= delta (fp32)
+//   (ii)  segments -> exact 64-bit fixed-point sums (round(c 2^32)) -> fp64 means; segments
+//         bucketed on channel-0 mean (cells of width >= delta, so close pairs are in adjacent
+//         cells) and united when max_k |m_A,k - m_B,k| <= delta
+//   (iii) label = rank of the cluster's smallest member index; palette = cluster mean
+// Union always hooks the larger root under the smaller one, so every root is the smallest
+// index of its set and the result is independent of thread scheduling.
+// Paper: clusters in colour space PAPER.md:55, :116; histograms PAPER.md:274, :281, :494.
+#include <math.h>
+#include <stdint.h>
+
+#include "msa_internal.h"
+
+struct MsaLabelScratch {
+  size_t cap_px = 0;
+  int C = 0;
+  int32_t* parent = nullptr;    // [N]
+  int32_t* flag = nullptr;      // [N]   root flags -> exclusive scan = segment index of a root
+  int32_t* scan_tmp = nullptr;  // block sums for the scans
+  size_t scan_tmp_n = 0;
+  int32_t* seg_parent = nullptr;  // [N]
+  int32_t* seg_flag = nullptr;    // [N]
+  int32_t* flag_copy = nullptr;   // [N]
+  unsigned long long* seg_sum = nullptr;  // [N][C]
+  unsigned long long* seg_cnt = nullptr;  // [N]
+  double* seg_mean = nullptr;             // [N][C]
+  int32_t* cell_count = nullptr;          // [NCELL + 1]
+  int32_t* cell_fill = nullptr;           // [NCELL]
+  int32_t* sorted = nullptr;              // [N]
+  int32_t* seg_cell = nullptr;            // [N]
+  unsigned long long* cl_sum = nullptr;   // [N][C]
+  unsigned long long* cl_cnt = nullptr;   // [N]
+  int32_t* scalars = nullptr;             // [4] S, K, cell_lo, cell_hi (as int bits)
+  double* dscal = nullptr;                // [2] min/max of m0
+};
+
+namespace {
+
+constexpr int NCELL_MAX = 1 << 20;
+
+__device__ __forceinline__ int uf_find(const int32_t* P, int x) {
+  int p = __ldcg(P + x);
+  while (p != x) {
+    x = p;
+    p = __ldcg(P + x);
+  }
+  return x;
+}
+
+__device__ __forceinline__ void uf_unite(int32_t* P, int a, int b) {
+  while (true) {
+    a = uf_find(P, a);
+    b = uf_find(P, b);
+    if (a == b) return;
+    if (a > b) { int t = a; a = b; b = t; }
+    const int old = atomicCAS(P + b, b, a);  // hook the larger root under the smaller
+    if (old == b) return;
+    b = old;
+  }
+}
+
+__global__ void k_iota(int32_t* P, int n) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < n) P[x] = x;
+}
+
+// stage (i): 4-neighbour edges (right, up)
+__global__ void k_edges(MsaGeom g, const float* __restrict__ c, int b, float delta, int32_t* P) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.W || j >= g.H) return;
+  const int n = j * g.W + i;
+  bool right = i + 1 < g.W, up = j + 1 < g.H;
+  for (int k = 0; k < g.C; ++k) {
+    const float a = c[msa_idx(g, b, k, g.C, j, i)];
+    if (right && !(fabsf(__fsub_rn(a, c[msa_idx(g, b, k, g.C, j, i + 1)])) <= delta)) right = false;
+    if (up && !(fabsf(__fsub_rn(a, c[msa_idx(g, b, k, g.C, j + 1, i)])) <= delta)) up = false;
+  }
+  if (right) uf_unite(P, n, n + 1);
+  if (up) uf_unite(P, n, n + g.W);
+}
+
+__global__ void k_compress_flag(int32_t* P, int32_t* flag, int n) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const int r = uf_find(P, x);
+  P[x] = r;
+  flag[x] = (r == x) ? 1 : 0;
+}
+
+// ---- exclusive scan of int32 (in place), 1024 elements per block
+__global__ void k_scan_block(int32_t* a, int n, int32_t* bsum) {
+  __shared__ int32_t s[1024];
+  __shared__ int32_t wsum[32];
+  const int base = blockIdx.x * 1024;
+  const int t = threadIdx.x;  // 256 threads x 4
+  int v[4], local = 0;
+  for (int q = 0; q < 4; ++q) {
+    const int x = base + t * 4 + q;
+    v[q] = x < n ? a[x] : 0;
+    local += v[q];
+  }
+  // warp inclusive scan of thread totals
+  int incl = local;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if ((t & 31) >= o) incl += y;
+  }
+  if ((t & 31) == 31) wsum[t >> 5] = incl;
+  __syncthreads();
+  if (t < 32) {
+    int w = t < 8 ? wsum[t] : 0;
+    for (int o = 1; o < 8; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, w, o);
+      if (t >= o) w += y;
+    }
+    if (t < 8) wsum[t] = w;
+  }
+  __syncthreads();
+  int run = incl - local + ((t >> 5) > 0 ? wsum[(t >> 5) - 1] : 0);
+  for (int q = 0; q < 4; ++q) {
+    const int x = base + t * 4 + q;
+    if (x < n) a[x] = run;
+    run += v[q];
+  }
+  if (t == 255 && bsum) bsum[blockIdx.x] = run;
+  (void)s;
+}
+__global__ void k_scan_add(int32_t* a, int n, const int32_t* off) {
+  const int x = blockIdx.x * 1024 + threadIdx.x * 4;
+  const int o = off[blockIdx.x];
+  for (int q = 0; q < 4; ++q)
+    if (x + q < n) a[x + q] += o;
+}
+
+// ---- segments
+__global__ void k_seg_accum(MsaGeom g, const float* __restrict__ c, int b, const int32_t* __restrict__ P,
+                            const int32_t* __restrict__ segidx, unsigned long long* sum, unsigned long long* cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.W || j >= g.H) return;
+  const int n = j * g.W + i;
+  const int s = segidx[P[n]];
+  atomicAdd(cnt + s, 1ULL);
+  for (int k = 0; k < g.C; ++k) {
+    const long long q = __double2ll_rn((double)c[msa_idx(g, b, k, g.C, j, i)] * 4294967296.0);
+    atomicAdd(sum + (size_t)s * g.C + k, (unsigned long long)q);
+  }
+}
+
+__device__ __forceinline__ double atomicMinD(double* a, double v) {
+  unsigned long long* p = (unsigned long long*)a;
+  unsigned long long old = *p, assumed;
+  do {
+    assumed = old;
+    if (__longlong_as_double(assumed) <= v) break;
+    old = atomicCAS(p, assumed, __double_as_longlong(v));
+  } while (old != assumed);
+  return __longlong_as_double(old);
+}
+__device__ __forceinline__ double atomicMaxD(double* a, double v) {
+  unsigned long long* p = (unsigned long long*)a;
+  unsigned long long old = *p, assumed;
+  do {
+    assumed = old;
+    if (__longlong_as_double(assumed) >= v) break;
+    old = atomicCAS(p, assumed, __double_as_longlong(v));
+  } while (old != assumed);
+  return __longlong_as_double(old);
+}
+
+__global__ void k_seg_mean(const int32_t* __restrict__ scal, int C, const unsigned long long* __restrict__ sum,
+                           const unsigned long long* __restrict__ cnt, double* mean, int32_t* segP, double* mm) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= scal[0]) return;
+  const double n = (double)cnt[s];
+  for (int k = 0; k < C; ++k) mean[(size_t)s * C + k] = (double)(long long)sum[(size_t)s * C + k] / n * 0x1.0p-32;
+  segP[s] = s;
+  atomicMinD(mm, mean[(size_t)s * C]);
+  atomicMaxD(mm + 1, mean[(size_t)s * C]);
+}
+
+__device__ __forceinline__ double cell_width(double delta, const double* mm) {
+  const double span = mm[1] - mm[0];
+  const double wmin = span / (double)(NCELL_MAX - 4);
+  const double w = delta > wmin ? delta : wmin;
+  return w > 0 ? w : 1.0;
+}
+
+__global__ void k_seg_cell(const int32_t* __restrict__ scal, int C, const double* __restrict__ mean,
+                           const double* __restrict__ mm, double delta, int32_t* seg_cell, int32_t* count) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= scal[0]) return;
+  const double w = cell_width(delta, mm);
+  int cell = (int)floor((mean[(size_t)s * C] - mm[0]) / w);
+  cell = cell < 0 ? 0 : (cell >= NCELL_MAX ? NCELL_MAX - 1 : cell);
+  seg_cell[s] = cell;
+  atomicAdd(count + cell, 1);
+}
+
+__global__ void k_seg_scatter(const int32_t* __restrict__ scal, const int32_t* __restrict__ seg_cell,
+                              const int32_t* __restrict__ start, int32_t* fill, int32_t* sorted) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= scal[0]) return;
+  const int cell = seg_cell[s];
+  const int pos = start[cell] + atomicAdd(fill + cell, 1);
+  sorted[pos] = s;
+}
+
+// stage (ii): one thread per segment A; candidates B in A's cell (after A's position) and the
+// next two cells (cells are >= delta wide; +2 guards the rounding of the cell index).
+__global__ void k_seg_pairs(const int32_t* __restrict__ scal, int C, const double* __restrict__ mean,
+                            const int32_t* __restrict__ seg_cell, const int32_t* __restrict__ start,
+                            const int32_t* __restrict__ sorted, double delta, int32_t* segP) {
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  const int S = scal[0];
+  if (q >= S) return;
+  const int A = sorted[q];
+  const int cell = seg_cell[A];
+  const int lastcell = cell + 3 <= NCELL_MAX ? cell + 3 : NCELL_MAX;
+  const int end = start[lastcell];
+  const double* mA = mean + (size_t)A * C;
+  for (int r = q + 1; r < end; ++r) {
+    const int B = sorted[r];
+    const double* mB = mean + (size_t)B * C;
+    bool ok = true;
+    for (int k = 0; k < C && ok; ++k) ok = fabs(mA[k] - mB[k]) <= delta;
+    if (ok) uf_unite(segP, A, B);
+  }
+}
+
+__global__ void k_seg_compress(const int32_t* __restrict__ scal, int32_t* segP, int32_t* seg_flag) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= scal[0]) return;
+  const int r = uf_find(segP, s);
+  segP[s] = r;
+  seg_flag[s] = (r == s) ? 1 : 0;
+}
+
+// stage (iii)
+__global__ void k_cluster_sums(const int32_t* __restrict__ scal, int C, const int32_t* __restrict__ segP,
+                               const int32_t* __restrict__ rank, const unsigned long long* __restrict__ sum,
+                               const unsigned long long* __restrict__ cnt, unsigned long long* csum,
+                               unsigned long long* ccnt) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= scal[0]) return;
+  const int l = rank[segP[s]];
+  atomicAdd(ccnt + l, cnt[s]);
+  for (int k = 0; k < C; ++k) atomicAdd(csum + (size_t)l * C + k, sum[(size_t)s * C + k]);
+}
+
+__global__ void k_write_labels(int N, const int32_t* __restrict__ P, const int32_t* __restrict__ segidx,
+                               const int32_t* __restrict__ segP, const int32_t* __restrict__ rank, int32_t* labels) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  labels[n] = rank[segP[segidx[P[n]]]];
+}
+
+__global__ void k_totals(const int32_t* nptr, int n_static, const int32_t* scanned, const int32_t* flags,
+                         int32_t* out) {
+  // total = exclusive-scan[n-1] + flag[n-1], n = *nptr if given
+  if (threadIdx.x != 0) return;
+  const int n = nptr ? *nptr : n_static;
+  *out = n > 0 ? scanned[n - 1] + flags[n - 1] : 0;
+}
+
+__global__ void k_palette(const int32_t* __restrict__ scal, int C, const unsigned long long* __restrict__ csum,
+                          const unsigned long long* __restrict__ ccnt, float* palette, int max_k, int32_t* count) {
+  const int l = blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = scal[1];
+  if (l == 0) *count = K;
+  if (!palette || l >= K || l >= max_k) return;
+  for (int k = 0; k < C; ++k)
+    palette[(size_t)l * C + k] = (float)((double)(long long)csum[(size_t)l * C + k] / (double)ccnt[l] * 0x1.0p-32);
+}
+
+// exclusive scan of `flags` -> `out` (may alias), returns total in *total_dev
+cudaError_t scan_excl(int32_t* a, int n, int32_t* tmp, size_t tmp_n, cudaStream_t s, long long* launches) {
+  if (n <= 0) return cudaSuccess;
+  const int nb = (n + 1023) / 1024;
+  if ((size_t)nb > tmp_n) return cudaErrorInvalidValue;
+  k_scan_block<<<nb, 256, 0, s>>>(a, n, nb > 1 ? tmp : nullptr);
+  ++*launches;
+  if (nb > 1) {
+    cudaError_t e = scan_excl(tmp, nb, tmp + nb, tmp_n - nb, s, launches);
+    if (e != cudaSuccess) return e;
+    k_scan_add<<<nb, 256, 0, s>>>(a, n, tmp);
+    ++*launches;
+  }
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t grow(T** p, size_t n) {
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  return cudaMalloc((void**)p, n * sizeof(T) + 16);
+}
+
+}  // namespace
+
+void msa_labels_free(MsaLabelScratch* s) {
+  if (!s) return;
+  void* ptrs[] = {s->parent, s->flag, s->scan_tmp, s->seg_parent, s->seg_flag, s->flag_copy, s->seg_sum, s->seg_cnt,
+                  s->seg_mean, s->cell_count, s->cell_fill, s->sorted, s->seg_cell, s->cl_sum, s->cl_cnt,
+                  s->scalars, s->dscal};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete s;
+}
+
+cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delta, int32_t* labels_dev,
+                             int32_t* count_dev, float* palette_dev, int max_k, MsaLabelScratch** scratch,
+                             cudaStream_t st, long long* launches) {
+  const int N = g.H * g.W, C = g.C;
+  MsaLabelScratch* S = *scratch;
+  if (!S) S = *scratch = new MsaLabelScratch();
+  cudaError_t e = cudaSuccess;
+  if (S->cap_px < (size_t)N || S->C != C) {
+    const size_t n = (size_t)N;
+    S->scan_tmp_n = 2 * ((n + 1023) / 1024) + 2 * ((NCELL_MAX + 1 + 1023) / 1024) + 64;
+    if ((e = grow(&S->parent, n)) || (e = grow(&S->flag, n)) || (e = grow(&S->scan_tmp, S->scan_tmp_n)) ||
+        (e = grow(&S->seg_parent, n)) || (e = grow(&S->seg_flag, n)) || (e = grow(&S->flag_copy, n)) || (e = grow(&S->seg_sum, n * C)) ||
+        (e = grow(&S->seg_cnt, n)) || (e = grow(&S->seg_mean, n * C)) ||
+        (e = grow(&S->cell_count, (size_t)NCELL_MAX + 1)) || (e = grow(&S->cell_fill, (size_t)NCELL_MAX)) ||
+        (e = grow(&S->sorted, n)) || (e = grow(&S->seg_cell, n)) || (e = grow(&S->cl_sum, n * C)) ||
+        (e = grow(&S->cl_cnt, n)) || (e = grow(&S->scalars, 4)) || (e = grow(&S->dscal, 2)))
+      return e;
+    S->cap_px = n;
+    S->C = C;
+  }
+  const int T = 256, nbN = (N + T - 1) / T;
+  dim3 blk(32, 8), grd((g.W + 31) / 32, (g.H + 7) / 8);
+  // (i) segments
+  k_iota<<<nbN, T, 0, st>>>(S->parent, N);
+  k_edges<<<grd, blk, 0, st>>>(g, c, b, delta, S->parent);
+  k_compress_flag<<<nbN, T, 0, st>>>(S->parent, S->flag, N);
+  *launches += 3;
+  // flag -> exclusive scan gives the segment index of each root; total S -> scalars[0]
+  cudaMemcpyAsync(S->flag_copy, S->flag, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st);  // keep flags
+  if ((e = scan_excl(S->flag, N, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
+  k_totals<<<1, 32, 0, st>>>(nullptr, N, S->flag, S->flag_copy, S->scalars + 0);
+  ++*launches;
+  cudaMemsetAsync(S->seg_sum, 0, sizeof(unsigned long long) * (size_t)N * C, st);
+  cudaMemsetAsync(S->seg_cnt, 0, sizeof(unsigned long long) * (size_t)N, st);
+  k_seg_accum<<<grd, blk, 0, st>>>(g, c, b, S->parent, S->flag, S->seg_sum, S->seg_cnt);
+  ++*launches;
+  // (ii) segment means, channel-0 cells, candidate pairs
+  const double init_mm[2] = {INFINITY, -INFINITY};
+  cudaMemcpyAsync(S->dscal, init_mm, sizeof(init_mm), cudaMemcpyHostToDevice, st);
+  k_seg_mean<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_sum, S->seg_cnt, S->seg_mean, S->seg_parent, S->dscal);
+  cudaMemsetAsync(S->cell_count, 0, sizeof(int32_t) * (NCELL_MAX + 1), st);
+  cudaMemsetAsync(S->cell_fill, 0, sizeof(int32_t) * NCELL_MAX, st);
+  k_seg_cell<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, S->dscal, (double)delta, S->seg_cell, S->cell_count);
+  *launches += 2;
+  if ((e = scan_excl(S->cell_count, NCELL_MAX + 1, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
+  k_seg_scatter<<<nbN, T, 0, st>>>(S->scalars, S->seg_cell, S->cell_count, S->cell_fill, S->sorted);
+  k_seg_pairs<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, S->seg_cell, S->cell_count, S->sorted, (double)delta,
+                                 S->seg_parent);
+  k_seg_compress<<<nbN, T, 0, st>>>(S->scalars, S->seg_parent, S->seg_flag);
+  *launches += 3;
+  // (iii) cluster ranks = exclusive scan of cluster-root flags over segments (segment order =
+  // smallest-member order), count, labels, palette
+  cudaMemcpyAsync(S->flag_copy, S->seg_flag, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st);  // flags copy
+  if ((e = scan_excl(S->seg_flag, N, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
+  k_totals<<<1, 32, 0, st>>>(S->scalars + 0, N, S->seg_flag, S->flag_copy, S->scalars + 1);
+  k_write_labels<<<nbN, T, 0, st>>>(N, S->parent, S->flag, S->seg_parent, S->seg_flag, labels_dev);
+  *launches += 2;
+  cudaMemsetAsync(S->cl_sum, 0, sizeof(unsigned long long) * (size_t)N * C, st);
+  cudaMemsetAsync(S->cl_cnt, 0, sizeof(unsigned long long) * (size_t)N, st);
+  k_cluster_sums<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_parent, S->seg_flag, S->seg_sum, S->seg_cnt, S->cl_sum,
+                                    S->cl_cnt);
+  const int npal = max_k > 0 ? max_k : 1;
+  k_palette<<<(npal + T - 1) / T, T, 0, st>>>(S->scalars, C, S->cl_sum, S->cl_cnt, palette_dev, max_k, count_dev);
+  *launches += 2;
+  return cudaGetLastError();
+}
