@@ -119,6 +119,25 @@ int msa_workspace_bytes(const msa_params* params, size_t* bytes);
 int msa_partition_rows(int32_t height, int32_t world, int32_t rank, int32_t radius, int32_t* row0,
                        int32_t* nrows, int32_t* ghost_rows);
 
+/* Halo-exchange plan of MSA_SHARD_ROWS, host only. Each op
+ * moves rows [row0, row0 + nrows) (global indices) of one field between this rank and `peer`:
+ * send = 1 sends my copy of those rows, send = 0 receives them into my ghost rows.
+ *   MSA_HALO_ITER  before every iteration: c (G = max(R,1) rows each side), cbar (1 row each
+ *                  side), p (my top row goes up; the slab above needs it for div p);
+ *   MSA_HALO_ROUND before a multiplier round: c (row above, for grad c), p (row below);
+ *   MSA_HALO_MU    after a round: mu (my top row goes up).
+ * The driver issues exactly these ops as grouped ncclSend/ncclRecv. */
+typedef struct {
+  int32_t field; /* MSA_FIELD_C, MSA_FIELD_CBAR, MSA_FIELD_P or MSA_FIELD_MU */
+  int32_t peer;
+  int32_t send;
+  int32_t row0;
+  int32_t nrows;
+} msa_halo_op;
+enum { MSA_HALO_ITER = 0, MSA_HALO_ROUND = 1, MSA_HALO_MU = 2 };
+int msa_halo_plan(int32_t height, int32_t world, int32_t rank, int32_t radius, int32_t phase, msa_halo_op* ops,
+                  int32_t max_ops, int32_t* n_ops);
+
 /* Writes a 128-byte ncclUniqueId to out128 (rank 0 calls it; the harness broadcasts it). */
 int msa_nccl_unique_id(void* out128);
 

@@ -24,7 +24,7 @@ KERNEL_WENDLAND, KERNEL_PRINTED = 0, 1
 
 # every symbol include/msa.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["msa_abi_version", "msa_last_error", "msa_workspace_bytes", "msa_partition_rows",
-               "msa_nccl_unique_id", "msa_init", "msa_reset", "msa_step", "msa_solve", "msa_labels",
+               "msa_nccl_unique_id", "msa_halo_plan", "msa_init", "msa_reset", "msa_step", "msa_solve", "msa_labels",
                "msa_get_field", "msa_set_field", "msa_get_stats", "msa_state_bytes", "msa_get_state",
                "msa_set_state", "msa_query", "msa_set_timing", "msa_get_timing", "msa_sync", "msa_free"]
 
@@ -137,6 +137,7 @@ def lib():
             "msa_workspace_bytes": ([PP, PSZ], ctypes.c_int),
             "msa_partition_rows": ([I32, I32, I32, I32, PI32, PI32, PI32], ctypes.c_int),
             "msa_nccl_unique_id": ([V], ctypes.c_int),
+            "msa_halo_plan": ([I32, I32, I32, I32, I32, V, I32, PI32], ctypes.c_int),
             "msa_init": ([PP, V, ctypes.c_int, V, SZ, V, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),
             "msa_reset": ([P, V, ctypes.c_int], ctypes.c_int),
             "msa_step": ([P, I32], ctypes.c_int),
@@ -178,6 +179,23 @@ def partition_rows(height: int, world: int, rank: int, radius: int) -> tuple[int
     r0, nr, g = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
     _check(lib().msa_partition_rows(height, world, rank, radius, ctypes.byref(r0), ctypes.byref(nr), ctypes.byref(g)))
     return r0.value, nr.value, g.value
+
+
+HALO_ITER, HALO_ROUND, HALO_MU = 0, 1, 2
+
+
+class HaloOp(ctypes.Structure):
+    _fields_ = [("field", ctypes.c_int32), ("peer", ctypes.c_int32), ("send", ctypes.c_int32),
+                ("row0", ctypes.c_int32), ("nrows", ctypes.c_int32)]
+
+
+def halo_plan(height: int, world: int, rank: int, radius: int, phase: int) -> list[tuple]:
+    """msa_halo_plan: [(field, peer, send, row0, nrows)] - host only, no GPU needed."""
+    n = ctypes.c_int32(0)
+    _check(lib().msa_halo_plan(height, world, rank, radius, phase, None, 0, ctypes.byref(n)))
+    buf = (HaloOp * max(n.value, 1))()
+    _check(lib().msa_halo_plan(height, world, rank, radius, phase, buf, n.value, ctypes.byref(n)))
+    return [(o.field, o.peer, o.send, o.row0, o.nrows) for o in buf[:n.value]]
 
 
 def nccl_unique_id() -> bytes:

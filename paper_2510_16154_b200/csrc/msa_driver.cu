@@ -178,8 +178,10 @@ int derive(const msa_params* p, Derived* d) {
   const int R = p->radius;
   d->NR = 0;
   d->T.n = 0;
-  for (int dy = -R; dy <= R; ++dy)
-    for (int dx = -R; dx <= R; ++dx) {
+  // offset order: dx outer, dy inner (the order of K1's column caches; both kernels sum the
+  // terms of a pixel in this order, so they agree bitwise)
+  for (int dx = -R; dx <= R; ++dx)
+    for (int dy = -R; dy <= R; ++dy) {
       if (dx * dx + dy * dy > R * R) continue;
       ++d->NR;
       if (dx == 0 && dy == 0) continue;  // phi(r) (c - c) = 0
@@ -317,54 +319,76 @@ int fetch_records(msa_ctx* x) {
   return MSA_OK;
 }
 
-// --- halo exchange of the current state (rows mode, world > 1)
-int halo_exchange(msa_ctx* x, bool with_c, bool with_cb, bool with_p, bool with_mu) {
+// --- halo-exchange plan (include/msa.h msa_halo_plan), shared by the driver and the host tests
+int halo_plan(int H, int world, int rank, int R, int phase, std::vector<msa_halo_op>* ops) {
+  ops->clear();
+  if (world <= 1) return MSA_OK;
+  msa_params p{};
+  p.height = H; p.batch = 1; p.world = world; p.rank = rank; p.radius = R; p.shard = MSA_SHARD_ROWS;
+  const Part pt = partition(&p);
+  const int r0 = pt.row0, r1 = pt.row0 + pt.nrows, G = pt.ghost;
+  const int lo = rank - 1, hi = rank + 1;
+  const bool has_lo = lo >= 0, has_hi = hi < world;
+  auto add = [&](int f, int peer, int send, int row0, int n) { ops->push_back({f, peer, send, row0, n}); };
+  if (phase == MSA_HALO_ITER) {
+    if (has_lo) {
+      add(MSA_FIELD_C, lo, 1, r0, G);        // my bottom G rows -> the slab below (its top ghosts)
+      add(MSA_FIELD_C, lo, 0, r0 - G, G);    // its top G rows -> my bottom ghosts
+      add(MSA_FIELD_CBAR, lo, 1, r0, 1);
+      add(MSA_FIELD_CBAR, lo, 0, r0 - 1, 1);
+      add(MSA_FIELD_P, lo, 0, r0 - 1, 1);    // p below my slab (div p at row r0)
+    }
+    if (has_hi) {
+      add(MSA_FIELD_C, hi, 1, r1 - G, G);
+      add(MSA_FIELD_C, hi, 0, r1, G);
+      add(MSA_FIELD_CBAR, hi, 1, r1 - 1, 1);
+      add(MSA_FIELD_CBAR, hi, 0, r1, 1);     // cbar above my slab (forward difference at r1-1)
+      add(MSA_FIELD_P, hi, 1, r1 - 1, 1);
+    }
+  } else if (phase == MSA_HALO_ROUND) {
+    if (has_lo) {
+      add(MSA_FIELD_C, lo, 1, r0, 1);
+      add(MSA_FIELD_P, lo, 0, r0 - 1, 1);
+    }
+    if (has_hi) {
+      add(MSA_FIELD_C, hi, 0, r1, 1);        // grad c at row r1-1
+      add(MSA_FIELD_P, hi, 1, r1 - 1, 1);
+    }
+  } else if (phase == MSA_HALO_MU) {
+    if (has_lo) add(MSA_FIELD_MU, lo, 0, r0 - 1, 1);
+    if (has_hi) add(MSA_FIELD_MU, hi, 1, r1 - 1, 1);
+  } else {
+    return set_err(MSA_EINVAL, "bad halo phase %d", phase);
+  }
+  return MSA_OK;
+}
+
+// --- halo exchange of the current state (rows mode, world > 1): the plan's ops as one NCCL group
+int halo_exchange(msa_ctx* x, int phase) {
   const msa_params& P = x->prm;
   if (!(P.world > 1 && P.shard == MSA_SHARD_ROWS)) return MSA_OK;
+  std::vector<msa_halo_op> ops;
+  int rc = halo_plan(P.height, P.world, P.rank, P.radius, phase, &ops);
+  if (rc != MSA_OK) return rc;
   const MsaGeom& g = x->g;
-  const int C = P.channels, G = g.G;
-  const size_t pitch = g.pitch;
-  const int lo = P.rank - 1, hi = P.rank + 1;
-  const bool has_lo = lo >= 0, has_hi = hi < P.world;
-  auto rowp = [&](float* f, int b, int m, int nm, int j) { return f + ((size_t)b * nm + m) * g.plane + (size_t)(j - g.row0 + G) * pitch; };
+  const int C = P.channels;
   const int s = x->cur;
   NCCL_TRY(g_nccl.GroupStart());
-  for (int b = 0; b < g.nb; ++b) {
-    if (with_c)
-      for (int k = 0; k < C; ++k) {
-        float* f = x->c[s];
-        if (has_lo) {
-          NCCL_TRY(g_nccl.Send(rowp(f, b, k, C, g.row0), (size_t)G * pitch, ncclFloat, lo, x->comm, x->stream));
-          NCCL_TRY(g_nccl.Recv(rowp(f, b, k, C, g.row0 - G), (size_t)G * pitch, ncclFloat, lo, x->comm, x->stream));
-        }
-        if (has_hi) {
-          NCCL_TRY(g_nccl.Send(rowp(f, b, k, C, g.row0 + g.nrows - G), (size_t)G * pitch, ncclFloat, hi, x->comm, x->stream));
-          NCCL_TRY(g_nccl.Recv(rowp(f, b, k, C, g.row0 + g.nrows), (size_t)G * pitch, ncclFloat, hi, x->comm, x->stream));
-        }
+  for (const msa_halo_op& op : ops) {
+    float* f = field_ptr(x, op.field, s);
+    const int nm = field_nm(x, op.field);
+    for (int b = 0; b < g.nb; ++b)
+      for (int m = 0; m < nm; ++m) {
+        float* rows = f + ((size_t)b * nm + m) * g.plane + (size_t)(op.row0 - g.row0 + g.G) * g.pitch;
+        const size_t n = (size_t)op.nrows * g.pitch;
+        if (op.send)
+          NCCL_TRY(g_nccl.Send(rows, n, ncclFloat, op.peer, x->comm, x->stream));
+        else
+          NCCL_TRY(g_nccl.Recv(rows, n, ncclFloat, op.peer, x->comm, x->stream));
       }
-    if (with_cb)
-      for (int k = 0; k < C; ++k) {
-        float* f = x->cb[s];
-        if (has_lo) {
-          NCCL_TRY(g_nccl.Send(rowp(f, b, k, C, g.row0), pitch, ncclFloat, lo, x->comm, x->stream));
-          NCCL_TRY(g_nccl.Recv(rowp(f, b, k, C, g.row0 - 1), pitch, ncclFloat, lo, x->comm, x->stream));
-        }
-        if (has_hi) {
-          NCCL_TRY(g_nccl.Send(rowp(f, b, k, C, g.row0 + g.nrows - 1), pitch, ncclFloat, hi, x->comm, x->stream));
-          NCCL_TRY(g_nccl.Recv(rowp(f, b, k, C, g.row0 + g.nrows), pitch, ncclFloat, hi, x->comm, x->stream));
-        }
-      }
-    // p and mu: the slab below needs nothing; the slab above needs my top row as its row0-1
-    float* vf[2] = {with_p ? x->p[s] : nullptr, with_mu ? x->mu : nullptr};
-    for (float* f : vf) {
-      if (!f) continue;
-      for (int m = 0; m < 2 * C; ++m) {
-        if (has_hi) NCCL_TRY(g_nccl.Send(rowp(f, b, m, 2 * C, g.row0 + g.nrows - 1), pitch, ncclFloat, hi, x->comm, x->stream));
-        if (has_lo) NCCL_TRY(g_nccl.Recv(rowp(f, b, m, 2 * C, g.row0 - 1), pitch, ncclFloat, lo, x->comm, x->stream));
-      }
-    }
   }
   NCCL_TRY(g_nccl.GroupEnd());
+  (void)C;
   return MSA_OK;
 }
 
@@ -374,7 +398,7 @@ int do_round(msa_ctx* x) {
   const int s = x->cur;
   int rc;
   // the round needs c one row above the slab (grad) and p one row below (div p)
-  if ((rc = halo_exchange(x, true, false, true, false)) != MSA_OK) return rc;
+  if ((rc = halo_exchange(x, MSA_HALO_ROUND)) != MSA_OK) return rc;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (x->timing) {
     cudaEventCreate(&e0);
@@ -433,8 +457,9 @@ int do_steps(msa_ctx* x, int64_t n) {
   for (int64_t t = 0; t < n; ++t) {
     const int s = x->cur, o = 1 - s;
     if (P.world > 1 && P.shard == MSA_SHARD_ROWS) {
-      if ((rc = halo_exchange(x, true, true, true, x->halo_mu_dirty)) != MSA_OK) return rc;
+      if (x->halo_mu_dirty && (rc = halo_exchange(x, MSA_HALO_MU)) != MSA_OK) return rc;
       x->halo_mu_dirty = false;
+      if ((rc = halo_exchange(x, MSA_HALO_ITER)) != MSA_OK) return rc;
     }
     iter_batch_begin(x);
     int launched = 0;
@@ -529,6 +554,20 @@ int msa_partition_rows(int32_t height, int32_t world, int32_t rank, int32_t radi
   if (row0) *row0 = pt.row0;
   if (nrows) *nrows = pt.nrows;
   if (ghost_rows) *ghost_rows = pt.ghost;
+  return MSA_OK;
+}
+
+int msa_halo_plan(int32_t height, int32_t world, int32_t rank, int32_t radius, int32_t phase, msa_halo_op* ops,
+                  int32_t max_ops, int32_t* n_ops) {
+  if (height < 1 || world < 1 || rank < 0 || rank >= world || radius < 0 || !n_ops)
+    return set_err(MSA_EINVAL, "bad halo plan args");
+  if (world > 1 && height / world < std::max(radius, 1)) return set_err(MSA_EINVAL, "slabs too thin for the radius");
+  std::vector<msa_halo_op> v;
+  int rc = halo_plan(height, world, rank, radius, phase, &v);
+  if (rc != MSA_OK) return rc;
+  *n_ops = (int32_t)v.size();
+  if (ops)
+    for (int32_t i = 0; i < std::min(max_ops, *n_ops); ++i) ops[i] = v[i];
   return MSA_OK;
 }
 

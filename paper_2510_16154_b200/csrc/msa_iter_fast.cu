@@ -1,10 +1,336 @@
-// msa_iter_fast.cu - specialised fused iteration kernel K1 (placeholder: no
-// specialisation yet; the driver falls back to the generic kernel).
+// msa_iter_fast.cu - K1, the specialised fused iteration kernel (sm_100a) for C = 3.
+//
+// One CTA = one 32 x 64 tile of output pixels, 256 threads: lane = column, 8 strips of
+// 8 rows. Per iteration and pixel it does the whole of SURVEY §8(a)
+// steps 1-3:
+//   step 1  the agent interaction over the interior disc D°_R (ring offsets carry phi = 0
+//           for eps_x >= the default, so they are skipped exactly), reading the c tile +
+//           R halo from shared memory (cp.async, zero-filled outside the stored rows);
+//           each thread caches one neighbour column (8 + 2m rows x 3 channels) in
+//           registers and evaluates two vertically adjacent pixels per instruction with
+//           packed f32x2 arithmetic (FFMA2/FMUL2/FADD2 - the B200 FP32 pipe does 2 lanes
+//           per issue, so loads, FMNMX and addressing issue in the freed slots);
+//   step 2  p+ for the tile and its low-side halo (row y0-1, column x0-1) into smem;
+//   step 3  div p+, prox fidelity, extrapolation; coalesced stores of c+, cbar+, p+.
+// The per-pixel arithmetic and the order of the interaction terms (dx outer, dy inner) are
+// those of the generic kernel, so both produce bitwise-identical results and no result
+// depends on tile position (P19).
+#include <cstdlib>
+
 #include "msa_internal.h"
 
-cudaError_t msa_launch_iter_fast(const MsaGeom&, const MsaIterConsts&, const MsaOffsetTable&, int, const float*,
-                                 const float*, const float*, const float*, const float*, float*, float*, float*,
-                                 cudaStream_t, int* launched) {
+namespace {
+
+typedef unsigned long long f2;  // two fp32 lanes in one 64-bit register pair
+
+__device__ __forceinline__ f2 pk(float a, float b) {
+  f2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk(f2 v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+  f2 d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+  f2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+  f2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f2 relu2(f2 v) {
+  float a, b;
+  upk(v, a, b);
+  return pk(fmaxf(a, 0.0f), fmaxf(b, 0.0f));
+}
+
+constexpr int TW = 32;          // tile width (= lanes)
+constexpr int TH = 64;          // tile height
+constexpr int P = 8;            // rows per thread (4 packed pixel pairs)
+constexpr int NSTRIP = TH / P;  // 8 strips -> 256 threads
+constexpr int SX = 8;           // smem column of tile column 0 (16-byte aligned halo, >= R)
+constexpr int SW = TW + 2 * SX; // 48 smem columns
+
+// interior disc D°_R = {dx^2 + dy^2 < R^2}: half-height of column dx
+__host__ __device__ constexpr int col_m(int R, int dx) {
+  int m = -1;
+  for (int dy = 0; dy <= R; ++dy)
+    if (dx * dx + dy * dy < R * R) m = dy;
+  return m;
+}
+// index of offset (dx, dy) in the dx-outer, dy-inner enumeration of D°_R without the centre
+__host__ __device__ constexpr int off_index(int R, int dx, int dy) {
+  int n = 0;
+  for (int a = -R; a <= R; ++a) {
+    const int m = col_m(R, a);
+    for (int b = -m; b <= m; ++b) {
+      if (a == 0 && b == 0) continue;
+      if (a == dx && b == dy) return n;
+      ++n;
+    }
+  }
+  return -1;
+}
+__host__ __device__ constexpr int n_interior(int R) {
+  int n = 0;
+  for (int a = -R; a <= R; ++a) n += 2 * col_m(R, a) + 1;
+  return n - 1;
+}
+
+struct FastOm {
+  float v[200];
+};
+
+template <int R, bool MASK>
+__device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const FastOm& om, float e_c, float qc,
+                                            int lx, int strip, const float (&mrow)[P + 2 * R], const float (&mcol)[2 * R + 1],
+                                            const f2 (&ci)[P / 2][3], f2 (&acc)[P / 2][3]) {
+  const f2 NE = pk(-e_c, -e_c), M4 = pk(-4.0f, -4.0f), QC = pk(qc, qc);
+  int o = 0;  // offset index in the kernel's (dx outer, dy inner) order; constant after unrolling
+#pragma unroll
+  for (int dx = -R; dx <= R; ++dx) {
+    const int m = col_m(R, dx);
+    if (m < 0) continue;
+    // column cache: rows k = 0 .. P-1+2m of column lx+dx, relative row (strip*P - m + k)
+    f2 E[(P + 2 * R) / 2][3], O[(P + 2 * R) / 2][3];
+    f2 ME[(P + 2 * R) / 2], MO[(P + 2 * R) / 2];
+    const int base = (strip * P - m + R) * SW + SX + lx + dx;
+#pragma unroll
+    for (int q = 0; q < (P + 2 * m) / 2; ++q) {
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        const float* s = sc + k * (TH + 2 * R) * SW + base;
+        E[q][k] = pk(s[(2 * q) * SW], s[(2 * q + 1) * SW]);
+        if (2 * q + 2 < P + 2 * m) O[q][k] = pk(s[(2 * q + 1) * SW], s[(2 * q + 2) * SW]);
+      }
+      if (MASK) {
+        const float cm = mcol[dx + R];
+        ME[q] = pk(mrow[R - m + 2 * q] * cm, mrow[R - m + 2 * q + 1] * cm);
+        if (2 * q + 2 < P + 2 * m) MO[q] = pk(mrow[R - m + 2 * q + 1] * cm, mrow[R - m + 2 * q + 2] * cm);
+      }
+    }
+#pragma unroll
+    for (int dy = -m; dy <= m; ++dy) {
+      if (dx == 0 && dy == 0) continue;
+      const float omv = om.v[o++];
+      const f2 OM = pk(omv, omv);
+#pragma unroll
+      for (int j = 0; j < P / 2; ++j) {
+        const int kk = 2 * j + dy + m;  // first row of the neighbour pair in the cache
+        const bool even = (kk & 1) == 0;
+        f2 nb[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) nb[k] = even ? E[kk / 2][k] : O[kk / 2][k];
+        f2 d[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) d[k] = sub2(nb[k], ci[j][k]);
+        f2 s = mul2(d[0], d[0]);
+        s = fma2(d[1], d[1], s);
+        s = fma2(d[2], d[2], s);
+        const f2 t = relu2(fma2(NE, s, OM));
+        const f2 t2 = mul2(t, t);
+        const f2 t4 = mul2(t2, t2);
+        const f2 qv = fma2(M4, t, QC);
+        f2 w = mul2(t4, qv);
+        if (MASK) w = mul2(w, even ? ME[kk / 2] : MO[kk / 2]);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) acc[j][k] = fma2(w, d[k], acc[j][k]);
+      }
+    }
+  }
+}
+
+template <int R>
+__global__ void __launch_bounds__(256, 2)
+    k_iter_fast_c3(MsaGeom g, MsaIterConsts K, FastOm om, const float* __restrict__ c, const float* __restrict__ cb,
+                   const float* __restrict__ p, const float* __restrict__ mu, const float* __restrict__ I,
+                   float* __restrict__ c_out, float* __restrict__ cb_out, float* __restrict__ p_out) {
+  constexpr int C = 3;
+  constexpr int SH = TH + 2 * R;  // smem rows of the c tile
+  extern __shared__ __align__(16) float smem[];
+  float* sc = smem;                  // [3][SH][SW]
+  float* sp = smem + 3 * SH * SW;    // [6][TH + 1][TW + 1]   p+ with the low-side halo
+  constexpr int SPW = TW + 1, SPH = TH + 1;
+
+  const int lx = threadIdx.x & 31, strip = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * TW, y0 = g.row0 + blockIdx.y * TH, b = blockIdx.z;
+  const int W = g.W, H = g.H;
+  const int x = x0 + lx, ybase = y0 + strip * P;
+  const long long plane = g.plane;
+  const float* cimg = c + (long long)b * C * plane;
+
+  // ---- 1. c tile + halo -> smem (16-byte cp.async, zero fill outside the stored rows/pitch)
+  {
+    const int rlo = g.row0 - g.G, rhi = g.row0 + g.nrows + g.G;  // stored global rows
+    constexpr int CH4 = SW / 4;                                     // 12 float4 per smem row
+    for (int e = threadIdx.x; e < C * SH * CH4; e += 256) {
+      const int k = e / (SH * CH4), r = (e / CH4) % SH, q = e % CH4;
+      const int gy = y0 - R + r, gx = x0 - SX + 4 * q;
+      const bool ok = gy >= rlo && gy < rhi && gx >= 0 && gx + 4 <= g.pitch;
+      const float* src = ok ? cimg + (long long)k * plane + (long long)(gy - g.row0 + g.G) * g.pitch + gx : cimg;
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(sc + (k * SH + r) * SW + 4 * q);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+  }
+  __syncthreads();
+
+  // ---- 2. step 1: agent Euler step for 8 rows (4 packed pixel pairs) of column x
+  f2 ci[P / 2][3], acc[P / 2][3];
+#pragma unroll
+  for (int j = 0; j < P / 2; ++j)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const float* s = sc + (k * SH + strip * P + 2 * j + R) * SW + SX + lx;
+      ci[j][k] = pk(s[0], s[SW]);
+      acc[j][k] = pk(0.0f, 0.0f);
+    }
+  const float qc = K.kernel == 0 ? 5.0f : 3.0f;
+  const bool interior = x0 - R >= 0 && x0 + TW + R <= W && y0 - R >= 0 && y0 + TH + R <= H;
+  if (interior) {
+    float mrow[P + 2 * R], mcol[2 * R + 1];
+    agent_phase<R, false>(sc, om, K.e_c, qc, lx, strip, mrow, mcol, ci, acc);
+  } else {
+    float mrow[P + 2 * R], mcol[2 * R + 1];
+#pragma unroll
+    for (int k = 0; k < P + 2 * R; ++k) {
+      const int yy = ybase - R + k;
+      mrow[k] = (yy >= 0 && yy < H) ? 1.0f : 0.0f;
+    }
+#pragma unroll
+    for (int k = 0; k < 2 * R + 1; ++k) {
+      const int xx = x - R + k;
+      mcol[k] = (xx >= 0 && xx < W) ? 1.0f : 0.0f;
+    }
+    agent_phase<R, true>(sc, om, K.e_c, qc, lx, strip, mrow, mcol, ci, acc);
+  }
+  const f2 DT = pk(K.dt_NR, K.dt_NR);
+  float chalf[P][3];
+#pragma unroll
+  for (int j = 0; j < P / 2; ++j)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) upk(fma2(DT, acc[j][k], ci[j][k]), chalf[2 * j][k], chalf[2 * j + 1][k]);
+
+  // ---- 3. step 2: p+ for own pixels and the low-side halo (row y0-1, column x0-1) -> smem
+  auto dual_at = [&](int xx, int yy, int sx, int sy) {
+    if (xx < 0 || yy < 0 || xx >= W || yy >= H) return;
+    float gx[C], gy[C], px[C], py[C], mx[C], my[C], qx[C], qy[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const float c0 = cb[msa_idx(g, b, k, C, yy, xx)];
+      gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(cb[msa_idx(g, b, k, C, yy, xx + 1)], c0), K.inv_hx) : 0.0f;
+      gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(cb[msa_idx(g, b, k, C, yy + 1, xx)], c0), K.inv_hy) : 0.0f;
+      px[k] = p[msa_idx(g, b, k, 2 * C, yy, xx)];
+      py[k] = p[msa_idx(g, b, C + k, 2 * C, yy, xx)];
+      mx[k] = mu[msa_idx(g, b, k, 2 * C, yy, xx)];
+      my[k] = mu[msa_idx(g, b, C + k, 2 * C, yy, xx)];
+    }
+    msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      sp[(k * SPH + sy) * SPW + sx] = qx[k];
+      sp[((C + k) * SPH + sy) * SPW + sx] = qy[k];
+    }
+  };
+  const int rend = g.row0 + g.nrows;
+#pragma unroll 1
+  for (int r = 0; r < P; ++r) {
+    const int yy = ybase + r;
+    if (x < W && yy < rend) dual_at(x, yy, lx + 1, strip * P + r + 1);
+  }
+  if (strip == 0) dual_at(x, y0 - 1, lx + 1, 0);
+  if (lx == 0) {
+#pragma unroll 1
+    for (int r = 0; r < P; ++r) {
+      const int yy = ybase + r;
+      if (yy < rend) dual_at(x0 - 1, yy, 0, strip * P + r + 1);
+    }
+  }
+  __syncthreads();
+
+  // ---- 4. step 3: div p+, prox fidelity, extrapolation, stores
+  if (x >= W) return;
+#pragma unroll
+  for (int r = 0; r < P; ++r) {
+    const int yy = ybase + r;
+    if (yy >= rend) break;
+    const int sy = strip * P + r + 1, sx = lx + 1;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const float qx0 = sp[(k * SPH + sy) * SPW + sx], qy0 = sp[((C + k) * SPH + sy) * SPW + sx];
+      float ax = x < W - 1 ? qx0 : 0.0f;
+      if (x > 0) ax = __fsub_rn(ax, sp[(k * SPH + sy) * SPW + sx - 1]);
+      float ay = yy < H - 1 ? qy0 : 0.0f;
+      if (yy > 0) ay = __fsub_rn(ay, sp[((C + k) * SPH + sy - 1) * SPW + sx]);
+      const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
+      float cp, cbp;
+      msa_prox_extrap(K, chalf[r][k], d, I[msa_idx(g, b, k, C, yy, x)], cp, cbp);
+      c_out[msa_idx(g, b, k, C, yy, x)] = cp;
+      cb_out[msa_idx(g, b, k, C, yy, x)] = cbp;
+      p_out[msa_idx(g, b, k, 2 * C, yy, x)] = qx0;
+      p_out[msa_idx(g, b, C + k, 2 * C, yy, x)] = qy0;
+    }
+  }
+}
+
+template <int R>
+size_t smem_bytes() {
+  return sizeof(float) * (3 * (TH + 2 * R) * SW + 6 * (TH + 1) * (TW + 1));
+}
+
+template <int R>
+cudaError_t launch_c3(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, const float* c,
+                      const float* cb, const float* p, const float* mu, const float* I, float* co, float* cbo,
+                      float* po, cudaStream_t s) {
+  // om for every interior offset in the kernel's order; the driver's active set must be a
+  // subset of D°_R (ring offsets inactive), which the caller has checked.
+  FastOm om;
+  for (int q = 0; q < 200; ++q) om.v[q] = 0.0f;
+  for (int o = 0; o < T.n; ++o) {
+    const int idx = off_index(R, T.dx[o], T.dy[o]);
+    if (idx < 0) return cudaErrorNotSupported;
+    om.v[idx] = T.om[o];
+  }
+  // interior offsets absent from the table are inactive: om <= 1e-12 gives phi == 0 exactly
+  // in fp32 (t^4 underflows); encode them as om = 0 so t = max(-e s, 0) = 0.
+  static bool attr_set = false;
+  const size_t sm = smem_bytes<R>();
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_iter_fast_c3<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grd((g.W + TW - 1) / TW, (g.nrows + TH - 1) / TH, g.nb);
+  k_iter_fast_c3<R><<<grd, 256, sm, s>>>(g, K, om, c, cb, p, mu, I, co, cbo, po);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t msa_launch_iter_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                                 const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                                 float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
-  return cudaErrorNotSupported;
+  // test hook: MSA_FORCE_GENERIC=1 selects the generic kernel (bitwise-identical results)
+  static const bool force_generic = getenv("MSA_FORCE_GENERIC") != nullptr;
+  if (g.C != 3 || force_generic) return cudaErrorNotSupported;
+  // every active offset must lie in the interior disc (true for eps_x >= the default)
+  for (int o = 0; o < T.n; ++o)
+    if (T.dx[o] * T.dx[o] + T.dy[o] * T.dy[o] >= R * R) return cudaErrorNotSupported;
+  cudaError_t e;
+  switch (R) {
+    case 2: e = launch_c3<2>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
+    case 3: e = launch_c3<3>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
+    case 4: e = launch_c3<4>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
+    case 5: e = launch_c3<5>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
+    default: return cudaErrorNotSupported;
+  }
+  if (e == cudaSuccess) *launched = 1;
+  return e;
 }
