@@ -85,7 +85,8 @@ __device__ __forceinline__ void msa_dual_step(const MsaIterConsts& K, const floa
     n2 = __fmaf_rn(qy[k], qy[k], n2);
   }
   if (n2 > K.beta2) {
-    float f = __fdiv_rn(K.beta, __fsqrt_rn(n2));
+    // beta / |q| via the hardware reciprocal square root (R21: allowed since parity holds)
+    float f = __fmul_rn(K.beta, rsqrtf(n2));
 #pragma unroll
     for (int k = 0; k < C; ++k) {
       qx[k] = __fmul_rn(qx[k], f);

@@ -178,10 +178,13 @@ int derive(const msa_params* p, Derived* d) {
   const int R = p->radius;
   d->NR = 0;
   d->T.n = 0;
-  // offset order: dx outer, dy inner (the order of K1's column caches; both kernels sum the
-  // terms of a pixel in this order, so they agree bitwise)
+  // offset order: dx ascending; within a column the even dy ascending, then the odd dy
+  // ascending (the order of K1's two parity passes over a cached column). Both kernels sum
+  // the terms of a pixel in this order, so they agree bitwise.
   for (int dx = -R; dx <= R; ++dx)
+    for (int pass = 0; pass < 2; ++pass)
     for (int dy = -R; dy <= R; ++dy) {
+      if (((dy & 1) != 0) != (pass == 1)) continue;
       if (dx * dx + dy * dy > R * R) continue;
       ++d->NR;
       if (dx == 0 && dy == 0) continue;  // phi(r) (c - c) = 0

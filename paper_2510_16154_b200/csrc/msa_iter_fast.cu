@@ -1,20 +1,22 @@
 // msa_iter_fast.cu - K1, the specialised fused iteration kernel (sm_100a) for C = 3.
 //
-// One CTA = one 32 x 64 tile of output pixels, 256 threads: lane = column, 8 strips of
-// 8 rows. Per iteration and pixel it does the whole of SURVEY §8(a)
-// steps 1-3:
-//   step 1  the agent interaction over the interior disc D°_R (ring offsets carry phi = 0
-//           for eps_x >= the default, so they are skipped exactly), reading the c tile +
-//           R halo from shared memory (cp.async, zero-filled outside the stored rows);
-//           each thread caches one neighbour column (8 + 2m rows x 3 channels) in
-//           registers and evaluates two vertically adjacent pixels per instruction with
-//           packed f32x2 arithmetic (FFMA2/FMUL2/FADD2 - the B200 FP32 pipe does 2 lanes
-//           per issue, so loads, FMNMX and addressing issue in the freed slots);
-//   step 2  p+ for the tile and its low-side halo (row y0-1, column x0-1) into smem;
-//   step 3  div p+, prox fidelity, extrapolation; coalesced stores of c+, cbar+, p+.
-// The per-pixel arithmetic and the order of the interaction terms (dx outer, dy inner) are
-// those of the generic kernel, so both produce bitwise-identical results and no result
-// depends on tile position (P19).
+// One CTA = one 32 x 32 tile of output pixels, 256 threads: lane = column, 8 strips of
+// P = 4 rows. Per pixel it does SURVEY §8(a) steps 1-3 in one pass:
+//   prefetch  cp.async (16-byte, zero-filled outside the stored rows) of the c tile + R halo,
+//             and - landing while step 1 computes - cbar (+1 halo), p and mu (+1 low-side
+//             halo) and I for the tile;
+//   step 1    the agent interaction over the interior disc D°_R (ring offsets carry phi = 0
+//             for eps_x >= the default and are skipped exactly). Each thread caches one
+//             neighbour column in registers and evaluates two vertically adjacent pixels per
+//             instruction with packed f32x2 arithmetic (FFMA2/FMUL2/FADD2: 2 lanes per issue,
+//             so loads, FMNMX and address arithmetic fill the freed issue slots). A column is
+//             processed in two parity passes (neighbour pairs starting on even / odd cache
+//             rows) so only one set of packed pairs is live;
+//   step 2    p+ for the tile and its low-side halo (row y0-1, column x0-1) from smem;
+//   step 3    div p+, prox fidelity, extrapolation; coalesced stores of c+, cbar+, p+.
+// Term order per pixel: dx ascending; within a column first the dy of parity m(dx), then the
+// others, each ascending - the order of the driver's offset table, so the generic kernel gives
+// bitwise-identical results and no result depends on tile position (P19).
 #include <cstdlib>
 
 #include "msa_internal.h"
@@ -50,154 +52,189 @@ __device__ __forceinline__ f2 relu2(f2 v) {
   return pk(fmaxf(a, 0.0f), fmaxf(b, 0.0f));
 }
 
-constexpr int TW = 32;          // tile width (= lanes)
-constexpr int TH = 64;          // tile height
-constexpr int P = 8;            // rows per thread (4 packed pixel pairs)
-constexpr int NSTRIP = TH / P;  // 8 strips -> 256 threads
-constexpr int SX = 8;           // smem column of tile column 0 (16-byte aligned halo, >= R)
-constexpr int SW = TW + 2 * SX; // 48 smem columns
+constexpr int C = 3;
+constexpr int TW = 32;           // tile width (= lanes)
+constexpr int TH = 32;           // tile height
+constexpr int P = 4;             // rows per thread (2 packed pixel pairs)
+constexpr int NT = 256;          // threads: 8 strips of P rows
+constexpr int SX = 8;            // smem column of tile column 0 in the c tile (>= R, 16-byte aligned)
+constexpr int SW = TW + 2 * SX;  // 48
+// prefetch tiles (16-byte aligned column windows)
+constexpr int BX = 4;            // smem column of tile column 0 in the cbar / p / mu tiles
+constexpr int BW = 40;           // cbar: global columns x0-4 .. x0+35
+constexpr int BH = TH + 2;       // cbar: global rows y0-1 .. y0+32
+constexpr int QW = 36;           // p, mu: columns x0-4 .. x0+31
+constexpr int QH = TH + 1;       // p, mu: rows y0-1 .. y0+31
+constexpr int SPW = TW + 1, SPH = TH + 1;  // p+ tile with the low-side halo
 
-// interior disc D°_R = {dx^2 + dy^2 < R^2}: half-height of column dx
+// interior disc D°_R = {dx^2 + dy^2 < R^2}: half-height of column dx (-1: empty column)
 __host__ __device__ constexpr int col_m(int R, int dx) {
   int m = -1;
   for (int dy = 0; dy <= R; ++dy)
     if (dx * dx + dy * dy < R * R) m = dy;
   return m;
 }
-// index of offset (dx, dy) in the dx-outer, dy-inner enumeration of D°_R without the centre
-__host__ __device__ constexpr int off_index(int R, int dx, int dy) {
-  int n = 0;
-  for (int a = -R; a <= R; ++a) {
-    const int m = col_m(R, a);
-    for (int b = -m; b <= m; ++b) {
-      if (a == 0 && b == 0) continue;
-      if (a == dx && b == dy) return n;
-      ++n;
-    }
-  }
-  return -1;
-}
-__host__ __device__ constexpr int n_interior(int R) {
-  int n = 0;
-  for (int a = -R; a <= R; ++a) n += 2 * col_m(R, a) + 1;
-  return n - 1;
-}
 
 struct FastOm {
-  float v[200];
+  float v[128];
 };
+
+template <int R>
+struct Smem {
+  static constexpr int SH = TH + 2 * R;
+  static constexpr int c_floats = C * SH * SW;
+  static constexpr int sp_floats = 2 * C * SPH * SPW;
+  static constexpr int al(int n) { return (n + 31) / 32 * 32; }  // 128-byte aligned sub-buffers (cp.async)
+  static constexpr int u_floats = c_floats > sp_floats ? c_floats : sp_floats;  // c tile, later p+
+  static constexpr int cb_off = al(u_floats);
+  static constexpr int p_off = cb_off + al(C * BH * BW);
+  static constexpr int mu_off = p_off + al(2 * C * QH * QW);
+  static constexpr int I_off = mu_off + al(2 * C * QH * QW);
+  static constexpr int total = I_off + al(C * TH * TW);
+  static constexpr size_t bytes = sizeof(float) * total;
+};
+
+// 16-byte cp.async of a [nm][rows][4*n4] window of a planar field (zero fill outside the stored
+// rows [rlo, rhi) or the pitch)
+// Thread t copies float4 column t % N4 of rows t / N4, t / N4 + NT / N4, ... (no div/mod in the loop).
+template <int NM, int ROWS, int N4>
+__device__ __forceinline__ void prefetch(float* dst, const float* src_img, long long plane, const MsaGeom& g, int gy0,
+                                         int gx0) {
+  constexpr int RSTEP = NT / N4;
+  const int q = threadIdx.x % N4, r0 = threadIdx.x / N4;
+  if (r0 >= RSTEP) return;
+  const int gx = gx0 + 4 * q;
+  const bool okx = gx >= 0 && gx + 4 <= g.pitch;
+  const int nstored = g.nrows + 2 * g.G;
+  const int lr0 = gy0 - g.row0 + g.G;  // stored-row index of global row gy0
+  const unsigned dbase = (unsigned)__cvta_generic_to_shared(dst) + 16u * q;
+#pragma unroll
+  for (int m = 0; m < NM; ++m) {
+#pragma unroll
+    for (int r = r0; r < ROWS; r += RSTEP) {
+      const int lr = lr0 + r;
+      const bool ok = okx && lr >= 0 && lr < nstored;
+      const float* src = ok ? src_img + (long long)m * plane + (long long)lr * g.pitch + gx : src_img;
+      const unsigned d = dbase + 16u * (unsigned)((m * ROWS + r) * N4);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0));
+    }
+  }
+}
+
+// one parity pass over the neighbour pairs of column dx (pairs start at cache rows kk with
+// kk % 2 == PAR): cache Cp[q] = rows (2q + PAR, 2q + PAR + 1) of the column
+template <int R, bool MASK, int PAR>
+__device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx, int m, const FastOm& om, int& o,
+                                            f2 NE, f2 M4, f2 QC, const float (&mrow)[P + 2 * R], float cm,
+                                            const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
+  constexpr int SH = TH + 2 * R;
+  constexpr int NQ = (P + 2 * R) / 2;
+  f2 Cp[NQ][C], Mp[NQ];
+  const int nrow = P + 2 * m;  // cache rows 0 .. nrow-1
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    if (2 * q + PAR + 1 >= nrow) break;
+#pragma unroll
+    for (int k = 0; k < C; ++k) Cp[q][k] = pk(s[(k * SH + 2 * q + PAR) * SW], s[(k * SH + 2 * q + PAR + 1) * SW]);
+    if (MASK) Mp[q] = pk(mrow[R - m + 2 * q + PAR] * cm, mrow[R - m + 2 * q + PAR + 1] * cm);
+  }
+#pragma unroll
+  for (int dy = -R; dy <= R; ++dy) {
+    if (dy < -m || dy > m || dx == 0 && dy == 0) continue;
+    if (((dy + m) & 1) != PAR) continue;
+    const float omv = om.v[o++];
+    const f2 OM = pk(omv, omv);
+#pragma unroll
+    for (int j = 0; j < P / 2; ++j) {
+      const int q = (2 * j + dy + m - PAR) / 2;  // neighbour pair (rows 2j+dy, 2j+dy+1 of the strip)
+      f2 d[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) d[k] = sub2(Cp[q][k], ci[j][k]);
+      f2 sq = mul2(d[0], d[0]);
+#pragma unroll
+      for (int k = 1; k < C; ++k) sq = fma2(d[k], d[k], sq);
+      const f2 t = relu2(fma2(NE, sq, OM));
+      const f2 t2 = mul2(t, t);
+      const f2 t4 = mul2(t2, t2);
+      const f2 qv = fma2(M4, t, QC);
+      f2 w = mul2(t4, qv);
+      if (MASK) w = mul2(w, Mp[q]);
+#pragma unroll
+      for (int k = 0; k < C; ++k) acc[j][k] = fma2(w, d[k], acc[j][k]);
+    }
+  }
+}
 
 template <int R, bool MASK>
 __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const FastOm& om, float e_c, float qc,
-                                            int lx, int strip, const float (&mrow)[P + 2 * R], const float (&mcol)[2 * R + 1],
-                                            const f2 (&ci)[P / 2][3], f2 (&acc)[P / 2][3]) {
+                                            int lx, int strip, const float (&mrow)[P + 2 * R],
+                                            const float (&mcol)[2 * R + 1], const f2 (&ci)[P / 2][C],
+                                            f2 (&acc)[P / 2][C]) {
   const f2 NE = pk(-e_c, -e_c), M4 = pk(-4.0f, -4.0f), QC = pk(qc, qc);
-  int o = 0;  // offset index in the kernel's (dx outer, dy inner) order; constant after unrolling
+  int o = 0;  // offset index in the kernel's order; compile-time constant after unrolling
 #pragma unroll
   for (int dx = -R; dx <= R; ++dx) {
     const int m = col_m(R, dx);
     if (m < 0) continue;
-    // column cache: rows k = 0 .. P-1+2m of column lx+dx, relative row (strip*P - m + k)
-    f2 E[(P + 2 * R) / 2][3], O[(P + 2 * R) / 2][3];
-    f2 ME[(P + 2 * R) / 2], MO[(P + 2 * R) / 2];
-    const int base = (strip * P - m + R) * SW + SX + lx + dx;
-#pragma unroll
-    for (int q = 0; q < (P + 2 * m) / 2; ++q) {
-#pragma unroll
-      for (int k = 0; k < 3; ++k) {
-        const float* s = sc + k * (TH + 2 * R) * SW + base;
-        E[q][k] = pk(s[(2 * q) * SW], s[(2 * q + 1) * SW]);
-        if (2 * q + 2 < P + 2 * m) O[q][k] = pk(s[(2 * q + 1) * SW], s[(2 * q + 2) * SW]);
-      }
-      if (MASK) {
-        const float cm = mcol[dx + R];
-        ME[q] = pk(mrow[R - m + 2 * q] * cm, mrow[R - m + 2 * q + 1] * cm);
-        if (2 * q + 2 < P + 2 * m) MO[q] = pk(mrow[R - m + 2 * q + 1] * cm, mrow[R - m + 2 * q + 2] * cm);
-      }
-    }
-#pragma unroll
-    for (int dy = -m; dy <= m; ++dy) {
-      if (dx == 0 && dy == 0) continue;
-      const float omv = om.v[o++];
-      const f2 OM = pk(omv, omv);
-#pragma unroll
-      for (int j = 0; j < P / 2; ++j) {
-        const int kk = 2 * j + dy + m;  // first row of the neighbour pair in the cache
-        const bool even = (kk & 1) == 0;
-        f2 nb[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) nb[k] = even ? E[kk / 2][k] : O[kk / 2][k];
-        f2 d[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) d[k] = sub2(nb[k], ci[j][k]);
-        f2 s = mul2(d[0], d[0]);
-        s = fma2(d[1], d[1], s);
-        s = fma2(d[2], d[2], s);
-        const f2 t = relu2(fma2(NE, s, OM));
-        const f2 t2 = mul2(t, t);
-        const f2 t4 = mul2(t2, t2);
-        const f2 qv = fma2(M4, t, QC);
-        f2 w = mul2(t4, qv);
-        if (MASK) w = mul2(w, even ? ME[kk / 2] : MO[kk / 2]);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) acc[j][k] = fma2(w, d[k], acc[j][k]);
-      }
+    const float* s = sc + (strip * P - m + R) * SW + SX + lx + dx;
+    const float cm = MASK ? mcol[dx + R] : 1.0f;
+    if ((m & 1) == 0) {
+      column_pass<R, MASK, 0>(s, dx, m, om, o, NE, M4, QC, mrow, cm, ci, acc);
+      column_pass<R, MASK, 1>(s, dx, m, om, o, NE, M4, QC, mrow, cm, ci, acc);
+    } else {
+      column_pass<R, MASK, 1>(s, dx, m, om, o, NE, M4, QC, mrow, cm, ci, acc);
+      column_pass<R, MASK, 0>(s, dx, m, om, o, NE, M4, QC, mrow, cm, ci, acc);
     }
   }
 }
 
 template <int R>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(NT, 2)
     k_iter_fast_c3(MsaGeom g, MsaIterConsts K, FastOm om, const float* __restrict__ c, const float* __restrict__ cb,
                    const float* __restrict__ p, const float* __restrict__ mu, const float* __restrict__ I,
                    float* __restrict__ c_out, float* __restrict__ cb_out, float* __restrict__ p_out) {
-  constexpr int C = 3;
-  constexpr int SH = TH + 2 * R;  // smem rows of the c tile
+  using S = Smem<R>;
+  constexpr int SH = S::SH;
   extern __shared__ __align__(16) float smem[];
-  float* sc = smem;                  // [3][SH][SW]
-  float* sp = smem + 3 * SH * SW;    // [6][TH + 1][TW + 1]   p+ with the low-side halo
-  constexpr int SPW = TW + 1, SPH = TH + 1;
+  float* sc = smem;                 // [C][SH][SW]   c tile + halo (step 1)
+  float* sp = smem;                 // [2C][SPH][SPW] p+ (step 2-3; reuses the c tile)
+  float* scb = smem + S::cb_off;    // [C][BH][BW]
+  float* spp = smem + S::p_off;     // [2C][QH][QW]
+  float* smu = smem + S::mu_off;    // [2C][QH][QW]
+  float* sI = smem + S::I_off;      // [C][TH][TW]
 
   const int lx = threadIdx.x & 31, strip = threadIdx.x >> 5;
   const int x0 = blockIdx.x * TW, y0 = g.row0 + blockIdx.y * TH, b = blockIdx.z;
   const int W = g.W, H = g.H;
   const int x = x0 + lx, ybase = y0 + strip * P;
   const long long plane = g.plane;
-  const float* cimg = c + (long long)b * C * plane;
-
-  // ---- 1. c tile + halo -> smem (16-byte cp.async, zero fill outside the stored rows/pitch)
-  {
-    const int rlo = g.row0 - g.G, rhi = g.row0 + g.nrows + g.G;  // stored global rows
-    constexpr int CH4 = SW / 4;                                     // 12 float4 per smem row
-    for (int e = threadIdx.x; e < C * SH * CH4; e += 256) {
-      const int k = e / (SH * CH4), r = (e / CH4) % SH, q = e % CH4;
-      const int gy = y0 - R + r, gx = x0 - SX + 4 * q;
-      const bool ok = gy >= rlo && gy < rhi && gx >= 0 && gx + 4 <= g.pitch;
-      const float* src = ok ? cimg + (long long)k * plane + (long long)(gy - g.row0 + g.G) * g.pitch + gx : cimg;
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(sc + (k * SH + r) * SW + 4 * q);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0));
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
-  }
+  // ---- prefetch: group 0 = c tile (needed first), group 1 = cbar, p, mu, I
+  prefetch<C, SH, SW / 4>(sc, c + (long long)b * C * plane, plane, g, y0 - R, x0 - SX);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  prefetch<C, BH, BW / 4>(scb, cb + (long long)b * C * plane, plane, g, y0 - 1, x0 - BX);
+  prefetch<2 * C, QH, QW / 4>(spp, p + (long long)b * 2 * C * plane, plane, g, y0 - 1, x0 - BX);
+  prefetch<2 * C, QH, QW / 4>(smu, mu + (long long)b * 2 * C * plane, plane, g, y0 - 1, x0 - BX);
+  prefetch<C, TH, TW / 4>(sI, I + (long long)b * C * plane, plane, g, y0, x0);
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 1;" ::: "memory");
   __syncthreads();
 
-  // ---- 2. step 1: agent Euler step for 8 rows (4 packed pixel pairs) of column x
-  f2 ci[P / 2][3], acc[P / 2][3];
+  // ---- step 1: agent Euler step for P rows (P/2 packed pixel pairs) of column x
+  f2 ci[P / 2][C], acc[P / 2][C];
 #pragma unroll
   for (int j = 0; j < P / 2; ++j)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) {
+    for (int k = 0; k < C; ++k) {
       const float* s = sc + (k * SH + strip * P + 2 * j + R) * SW + SX + lx;
       ci[j][k] = pk(s[0], s[SW]);
       acc[j][k] = pk(0.0f, 0.0f);
     }
   const float qc = K.kernel == 0 ? 5.0f : 3.0f;
   const bool interior = x0 - R >= 0 && x0 + TW + R <= W && y0 - R >= 0 && y0 + TH + R <= H;
+  float mrow[P + 2 * R], mcol[2 * R + 1];
   if (interior) {
-    float mrow[P + 2 * R], mcol[2 * R + 1];
     agent_phase<R, false>(sc, om, K.e_c, qc, lx, strip, mrow, mcol, ci, acc);
   } else {
-    float mrow[P + 2 * R], mcol[2 * R + 1];
 #pragma unroll
     for (int k = 0; k < P + 2 * R; ++k) {
       const int yy = ybase - R + k;
@@ -211,51 +248,47 @@ __global__ void __launch_bounds__(256, 2)
     agent_phase<R, true>(sc, om, K.e_c, qc, lx, strip, mrow, mcol, ci, acc);
   }
   const f2 DT = pk(K.dt_NR, K.dt_NR);
-  float chalf[P][3];
+  float chalf[P][C];
 #pragma unroll
   for (int j = 0; j < P / 2; ++j)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) upk(fma2(DT, acc[j][k], ci[j][k]), chalf[2 * j][k], chalf[2 * j + 1][k]);
+    for (int k = 0; k < C; ++k) upk(fma2(DT, acc[j][k], ci[j][k]), chalf[2 * j][k], chalf[2 * j + 1][k]);
 
-  // ---- 3. step 2: p+ for own pixels and the low-side halo (row y0-1, column x0-1) -> smem
-  auto dual_at = [&](int xx, int yy, int sx, int sy) {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();  // prefetch landed; the c tile is dead (sp reuses it)
+
+  // ---- step 2: p+ at tile pixel (tx, ty) (tx, ty in [-1, 31]) -> sp[.][ty+1][tx+1]
+  auto dual_at = [&](int tx, int ty) {
+    const int xx = x0 + tx, yy = y0 + ty;
     if (xx < 0 || yy < 0 || xx >= W || yy >= H) return;
     float gx[C], gy[C], px[C], py[C], mx[C], my[C], qx[C], qy[C];
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      const float c0 = cb[msa_idx(g, b, k, C, yy, xx)];
-      gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(cb[msa_idx(g, b, k, C, yy, xx + 1)], c0), K.inv_hx) : 0.0f;
-      gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(cb[msa_idx(g, b, k, C, yy + 1, xx)], c0), K.inv_hy) : 0.0f;
-      px[k] = p[msa_idx(g, b, k, 2 * C, yy, xx)];
-      py[k] = p[msa_idx(g, b, C + k, 2 * C, yy, xx)];
-      mx[k] = mu[msa_idx(g, b, k, 2 * C, yy, xx)];
-      my[k] = mu[msa_idx(g, b, C + k, 2 * C, yy, xx)];
+      const float* cbk = scb + (k * BH + ty + 1) * BW + BX + tx;
+      const float c0 = cbk[0];
+      gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(cbk[1], c0), K.inv_hx) : 0.0f;
+      gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(cbk[BW], c0), K.inv_hy) : 0.0f;
+      px[k] = spp[(k * QH + ty + 1) * QW + BX + tx];
+      py[k] = spp[((C + k) * QH + ty + 1) * QW + BX + tx];
+      mx[k] = smu[(k * QH + ty + 1) * QW + BX + tx];
+      my[k] = smu[((C + k) * QH + ty + 1) * QW + BX + tx];
     }
     msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      sp[(k * SPH + sy) * SPW + sx] = qx[k];
-      sp[((C + k) * SPH + sy) * SPW + sx] = qy[k];
+      sp[(k * SPH + ty + 1) * SPW + tx + 1] = qx[k];
+      sp[((C + k) * SPH + ty + 1) * SPW + tx + 1] = qy[k];
     }
   };
-  const int rend = g.row0 + g.nrows;
-#pragma unroll 1
-  for (int r = 0; r < P; ++r) {
-    const int yy = ybase + r;
-    if (x < W && yy < rend) dual_at(x, yy, lx + 1, strip * P + r + 1);
-  }
-  if (strip == 0) dual_at(x, y0 - 1, lx + 1, 0);
-  if (lx == 0) {
-#pragma unroll 1
-    for (int r = 0; r < P; ++r) {
-      const int yy = ybase + r;
-      if (yy < rend) dual_at(x0 - 1, yy, 0, strip * P + r + 1);
-    }
-  }
+#pragma unroll
+  for (int r = 0; r < P; ++r) dual_at(lx, strip * P + r);
+  if (strip == 0) dual_at(lx, -1);      // halo row y0-1
+  else if (strip == 1) dual_at(-1, lx);  // halo column x0-1
   __syncthreads();
 
-  // ---- 4. step 3: div p+, prox fidelity, extrapolation, stores
+  // ---- step 3: div p+ (R6), prox fidelity, extrapolation (R21), stores
   if (x >= W) return;
+  const int rend = g.row0 + g.nrows;
 #pragma unroll
   for (int r = 0; r < P; ++r) {
     const int yy = ybase + r;
@@ -270,7 +303,7 @@ __global__ void __launch_bounds__(256, 2)
       if (yy > 0) ay = __fsub_rn(ay, sp[((C + k) * SPH + sy - 1) * SPW + sx]);
       const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
       float cp, cbp;
-      msa_prox_extrap(K, chalf[r][k], d, I[msa_idx(g, b, k, C, yy, x)], cp, cbp);
+      msa_prox_extrap(K, chalf[r][k], d, sI[(k * TH + strip * P + r) * TW + lx], cp, cbp);
       c_out[msa_idx(g, b, k, C, yy, x)] = cp;
       cb_out[msa_idx(g, b, k, C, yy, x)] = cbp;
       p_out[msa_idx(g, b, k, 2 * C, yy, x)] = qx0;
@@ -279,35 +312,52 @@ __global__ void __launch_bounds__(256, 2)
   }
 }
 
+// Kernel-order index of every interior offset (dx outer; within a column the dy of parity
+// m(dx) first, then the rest, each ascending).
 template <int R>
-size_t smem_bytes() {
-  return sizeof(float) * (3 * (TH + 2 * R) * SW + 6 * (TH + 1) * (TW + 1));
+int kernel_order_index(int dx, int dy) {
+  int n = 0;
+  for (int a = -R; a <= R; ++a) {
+    const int m = col_m(R, a);
+    if (m < 0) continue;
+    for (int pass = 0; pass < 2; ++pass) {
+      const int par = pass == 0 ? (m & 1) : 1 - (m & 1);
+      for (int e = -m; e <= m; ++e) {
+        if (a == 0 && e == 0) continue;
+        if (((e + m) & 1) != par) continue;
+        if (a == dx && e == dy) return n;
+        ++n;
+      }
+    }
+  }
+  return -1;
 }
 
 template <int R>
 cudaError_t launch_c3(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, const float* c,
                       const float* cb, const float* p, const float* mu, const float* I, float* co, float* cbo,
                       float* po, cudaStream_t s) {
-  // om for every interior offset in the kernel's order; the driver's active set must be a
-  // subset of D°_R (ring offsets inactive), which the caller has checked.
+  // om for every interior offset in the kernel's order. Interior offsets absent from the
+  // driver's active table have om <= 1e-12: phi is exactly 0 in fp32 either way, so they are
+  // encoded as om = 0 (t = max(-e s, 0) = 0).
   FastOm om;
-  for (int q = 0; q < 200; ++q) om.v[q] = 0.0f;
+  for (int q = 0; q < 128; ++q) om.v[q] = 0.0f;
+  int prev = -1;
   for (int o = 0; o < T.n; ++o) {
-    const int idx = off_index(R, T.dx[o], T.dy[o]);
-    if (idx < 0) return cudaErrorNotSupported;
+    const int idx = kernel_order_index<R>(T.dx[o], T.dy[o]);
+    if (idx < 0 || idx <= prev) return cudaErrorNotSupported;  // the driver's order must match
     om.v[idx] = T.om[o];
+    prev = idx;
   }
-  // interior offsets absent from the table are inactive: om <= 1e-12 gives phi == 0 exactly
-  // in fp32 (t^4 underflows); encode them as om = 0 so t = max(-e s, 0) = 0.
+  using S = Smem<R>;
   static bool attr_set = false;
-  const size_t sm = smem_bytes<R>();
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_iter_fast_c3<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaError_t e = cudaFuncSetAttribute(k_iter_fast_c3<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   dim3 grd((g.W + TW - 1) / TW, (g.nrows + TH - 1) / TH, g.nb);
-  k_iter_fast_c3<R><<<grd, 256, sm, s>>>(g, K, om, c, cb, p, mu, I, co, cbo, po);
+  k_iter_fast_c3<R><<<grd, NT, S::bytes, s>>>(g, K, om, c, cb, p, mu, I, co, cbo, po);
   return cudaGetLastError();
 }
 
