@@ -1,23 +1,28 @@
 // msa_iter_fast.cu - K1, the specialised fused iteration kernel (sm_100a) for C = 3.
 //
-// One CTA = one 32 x 32 tile of output pixels, 256 threads: lane = column, 8 strips of
-// P = 4 rows. Per pixel it does SURVEY §8(a) steps 1-3 in one pass:
-//   prefetch  cp.async (16-byte, zero-filled outside the stored rows) of the c tile + R halo,
-//             and - landing while step 1 computes - cbar (+1 halo), p and mu (+1 low-side
-//             halo) and I for the tile;
+// One CTA = one 32 x (8P) tile of output pixels, 256 threads: lane = column, 8 strips of P
+// rows. Per pixel it does SURVEY §8(a) steps 1-3 in one pass:
+//   prefetch  16-byte cp.async (zero-filled outside the stored rows) of the c tile + R halo
+//             (group 0), then - landing while step 1 computes - cbar (+1 halo), p and mu
+//             (+1 low-side halo) and I (group 1);
 //   step 1    the agent interaction over the interior disc D°_R (ring offsets carry phi = 0
 //             for eps_x >= the default and are skipped exactly). Each thread caches one
 //             neighbour column in registers and evaluates two vertically adjacent pixels per
-//             instruction with packed f32x2 arithmetic (FFMA2/FMUL2/FADD2: 2 lanes per issue,
-//             so loads, FMNMX and address arithmetic fill the freed issue slots). A column is
-//             processed in two parity passes (neighbour pairs starting on even / odd cache
-//             rows) so only one set of packed pairs is live;
+//             instruction with packed f32x2 arithmetic (FFMA2/FMUL2/FADD2: on B200 these do not
+//             raise the FP32 peak but halve the issue slots, so loads, FMNMX and address
+//             arithmetic issue in the gaps). A column is processed in two parity passes
+//             (neighbour pairs starting on even / odd cache rows) so only one set of packed
+//             pairs is live. Border tiles run a masked variant (w x in-image mask);
 //   step 2    p+ for the tile and its low-side halo (row y0-1, column x0-1) from smem;
 //   step 3    div p+, prox fidelity, extrapolation; coalesced stores of c+, cbar+, p+.
-// Term order per pixel: dx ascending; within a column first the dy of parity m(dx), then the
-// others, each ascending - the order of the driver's offset table, so the generic kernel gives
+// Term order per pixel: dx ascending; within a column the even dy ascending, then the odd dy
+// ascending - the order of the driver's offset table, so the generic kernel gives
 // bitwise-identical results and no result depends on tile position (P19).
+#include <cuda.h>
+
 #include <cstdlib>
+#include <cstring>
+#include <mutex>
 
 #include "msa_internal.h"
 
@@ -52,20 +57,47 @@ __device__ __forceinline__ f2 relu2(f2 v) {
   return pk(fmaxf(a, 0.0f), fmaxf(b, 0.0f));
 }
 
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers
+struct TmaSet {
+  CUtensorMap c, cb, p, mu, I;  // 3-D maps (x, stored row, component) of the five input fields
+};
+__device__ __forceinline__ unsigned saddr(const void* q) { return (unsigned)__cvta_generic_to_shared(q); }
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(saddr(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT%=;\n\t}" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                          unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+          saddr(dst)),
+      "l"((unsigned long long)map), "r"(x), "r"(y), "r"(z), "r"(saddr(bar))
+      : "memory");
+}
+
 constexpr int C = 3;
 constexpr int TW = 32;           // tile width (= lanes)
-constexpr int TH = 32;           // tile height
-constexpr int P = 4;             // rows per thread (2 packed pixel pairs)
 constexpr int NT = 256;          // threads: 8 strips of P rows
+constexpr int NSTRIP = 8;
 constexpr int SX = 8;            // smem column of tile column 0 in the c tile (>= R, 16-byte aligned)
 constexpr int SW = TW + 2 * SX;  // 48
-// prefetch tiles (16-byte aligned column windows)
 constexpr int BX = 4;            // smem column of tile column 0 in the cbar / p / mu tiles
 constexpr int BW = 40;           // cbar: global columns x0-4 .. x0+35
-constexpr int BH = TH + 2;       // cbar: global rows y0-1 .. y0+32
 constexpr int QW = 36;           // p, mu: columns x0-4 .. x0+31
-constexpr int QH = TH + 1;       // p, mu: rows y0-1 .. y0+31
-constexpr int SPW = TW + 1, SPH = TH + 1;  // p+ tile with the low-side halo
+constexpr int SPW = TW + 1;      // p+ tile with the low-side halo
 
 // interior disc D°_R = {dx^2 + dy^2 < R^2}: half-height of column dx (-1: empty column)
 __host__ __device__ constexpr int col_m(int R, int dx) {
@@ -79,12 +111,16 @@ struct FastOm {
   float v[128];
 };
 
-template <int R>
+template <int R, int P>
 struct Smem {
-  static constexpr int SH = TH + 2 * R;
+  static constexpr int TH = NSTRIP * P;
+  static constexpr int SH = TH + 2 * R;  // c tile rows
+  static constexpr int BH = TH + 2;      // cbar rows y0-1 .. y0+TH
+  static constexpr int QH = TH + 1;      // p, mu rows y0-1 .. y0+TH-1
+  static constexpr int SPH = TH + 1;
+  static constexpr int al(int n) { return (n + 31) / 32 * 32; }  // 128-byte aligned sub-buffers
   static constexpr int c_floats = C * SH * SW;
   static constexpr int sp_floats = 2 * C * SPH * SPW;
-  static constexpr int al(int n) { return (n + 31) / 32 * 32; }  // 128-byte aligned sub-buffers (cp.async)
   static constexpr int u_floats = c_floats > sp_floats ? c_floats : sp_floats;  // c tile, later p+
   static constexpr int cb_off = al(u_floats);
   static constexpr int p_off = cb_off + al(C * BH * BW);
@@ -94,9 +130,8 @@ struct Smem {
   static constexpr size_t bytes = sizeof(float) * total;
 };
 
-// 16-byte cp.async of a [nm][rows][4*n4] window of a planar field (zero fill outside the stored
-// rows [rlo, rhi) or the pitch)
-// Thread t copies float4 column t % N4 of rows t / N4, t / N4 + NT / N4, ... (no div/mod in the loop).
+// 16-byte cp.async of a [NM][ROWS][4*N4] window of a planar field (zero fill outside the
+// stored rows or the pitch). Thread t copies float4 column t % N4 of rows t / N4 + k NT / N4.
 template <int NM, int ROWS, int N4>
 __device__ __forceinline__ void prefetch(float* dst, const float* src_img, long long plane, const MsaGeom& g, int gy0,
                                          int gx0) {
@@ -121,22 +156,26 @@ __device__ __forceinline__ void prefetch(float* dst, const float* src_img, long 
   }
 }
 
-// one parity pass over the neighbour pairs of column dx (pairs start at cache rows kk with
-// kk % 2 == PAR): cache Cp[q] = rows (2q + PAR, 2q + PAR + 1) of the column
-template <int R, bool MASK, int PAR>
+// One parity pass over the neighbour pairs of column dx: cache Cp[q] = rows (2q + PAR,
+// 2q + PAR + 1) of the column (cache row k = strip row k - m). MASK: zero the weight of
+// out-of-image neighbours (column mask cm, row validity from the global row of cache row k).
+template <int R, int P, bool MASK, int PAR>
 __device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx, int m, const FastOm& om, int& o,
-                                            f2 NE, f2 M4, f2 QC, const float (&mrow)[P + 2 * R], float cm,
+                                            f2 NE, f2 M4, f2 QC, float cm, int yk0, int H,
                                             const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
-  constexpr int SH = TH + 2 * R;
+  constexpr int SH = NSTRIP * P + 2 * R;
   constexpr int NQ = (P + 2 * R) / 2;
   f2 Cp[NQ][C], Mp[NQ];
-  const int nrow = P + 2 * m;  // cache rows 0 .. nrow-1
+  const int nrow = P + 2 * m;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     if (2 * q + PAR + 1 >= nrow) break;
 #pragma unroll
     for (int k = 0; k < C; ++k) Cp[q][k] = pk(s[(k * SH + 2 * q + PAR) * SW], s[(k * SH + 2 * q + PAR + 1) * SW]);
-    if (MASK) Mp[q] = pk(mrow[R - m + 2 * q + PAR] * cm, mrow[R - m + 2 * q + PAR + 1] * cm);
+    if (MASK) {
+      const int ya = yk0 + 2 * q + PAR, yb = ya + 1;  // global rows of the pair
+      Mp[q] = pk((ya >= 0 && ya < H) ? cm : 0.0f, (yb >= 0 && yb < H) ? cm : 0.0f);
+    }
   }
 #pragma unroll
   for (int dy = -R; dy <= R; ++dy) {
@@ -146,7 +185,7 @@ __device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx,
     const f2 OM = pk(omv, omv);
 #pragma unroll
     for (int j = 0; j < P / 2; ++j) {
-      const int q = (2 * j + dy + m - PAR) / 2;  // neighbour pair (rows 2j+dy, 2j+dy+1 of the strip)
+      const int q = (2 * j + dy + m - PAR) / 2;  // neighbour pair = strip rows (2j+dy, 2j+dy+1)
       f2 d[C];
 #pragma unroll
       for (int k = 0; k < C; ++k) d[k] = sub2(Cp[q][k], ci[j][k]);
@@ -165,11 +204,10 @@ __device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx,
   }
 }
 
-template <int R, bool MASK>
+template <int R, int P, bool MASK>
 __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const FastOm& om, float e_c, float qc,
-                                            int lx, int strip, const float (&mrow)[P + 2 * R],
-                                            const float (&mcol)[2 * R + 1], const f2 (&ci)[P / 2][C],
-                                            f2 (&acc)[P / 2][C]) {
+                                            int lx, int strip, int x, int ybase, int W, int H,
+                                            const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
   const f2 NE = pk(-e_c, -e_c), M4 = pk(-4.0f, -4.0f), QC = pk(qc, qc);
   int o = 0;  // offset index in the kernel's order; compile-time constant after unrolling
 #pragma unroll
@@ -177,47 +215,62 @@ __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const 
     const int m = col_m(R, dx);
     if (m < 0) continue;
     const float* s = sc + (strip * P - m + R) * SW + SX + lx + dx;
-    const float cm = MASK ? mcol[dx + R] : 1.0f;
+    const float cm = (!MASK || (x + dx >= 0 && x + dx < W)) ? 1.0f : 0.0f;
+    const int yk0 = ybase - m;
     if ((m & 1) == 0) {
-      column_pass<R, MASK, 0>(s, dx, m, om, o, NE, M4, QC, mrow, cm, ci, acc);
-      column_pass<R, MASK, 1>(s, dx, m, om, o, NE, M4, QC, mrow, cm, ci, acc);
+      column_pass<R, P, MASK, 0>(s, dx, m, om, o, NE, M4, QC, cm, yk0, H, ci, acc);
+      column_pass<R, P, MASK, 1>(s, dx, m, om, o, NE, M4, QC, cm, yk0, H, ci, acc);
     } else {
-      column_pass<R, MASK, 1>(s, dx, m, om, o, NE, M4, QC, mrow, cm, ci, acc);
-      column_pass<R, MASK, 0>(s, dx, m, om, o, NE, M4, QC, mrow, cm, ci, acc);
+      column_pass<R, P, MASK, 1>(s, dx, m, om, o, NE, M4, QC, cm, yk0, H, ci, acc);
+      column_pass<R, P, MASK, 0>(s, dx, m, om, o, NE, M4, QC, cm, yk0, H, ci, acc);
     }
   }
 }
 
-template <int R>
-__global__ void __launch_bounds__(NT, 2)
-    k_iter_fast_c3(MsaGeom g, MsaIterConsts K, FastOm om, const float* __restrict__ c, const float* __restrict__ cb,
-                   const float* __restrict__ p, const float* __restrict__ mu, const float* __restrict__ I,
+template <int P>
+struct Occ {
+  static constexpr int blocks = P >= 4 ? 2 : 3;
+};
+
+template <int R, int P>
+__global__ void __launch_bounds__(NT, Occ<P>::blocks)
+    k_iter_fast_c3(MsaGeom g, MsaIterConsts K, FastOm om, const __grid_constant__ TmaSet tm,
                    float* __restrict__ c_out, float* __restrict__ cb_out, float* __restrict__ p_out) {
-  using S = Smem<R>;
-  constexpr int SH = S::SH;
-  extern __shared__ __align__(16) float smem[];
-  float* sc = smem;                 // [C][SH][SW]   c tile + halo (step 1)
-  float* sp = smem;                 // [2C][SPH][SPW] p+ (step 2-3; reuses the c tile)
-  float* scb = smem + S::cb_off;    // [C][BH][BW]
-  float* spp = smem + S::p_off;     // [2C][QH][QW]
-  float* smu = smem + S::mu_off;    // [2C][QH][QW]
-  float* sI = smem + S::I_off;      // [C][TH][TW]
+  using S = Smem<R, P>;
+  constexpr int TH = S::TH, SH = S::SH, BH = S::BH, QH = S::QH, SPH = S::SPH;
+  extern __shared__ __align__(128) float smem[];
+  float* sc = smem;               // [C][SH][SW]    c tile + halo (step 1)
+  float* sp = smem;               // [2C][SPH][SPW] p+ (steps 2-3; reuses the c tile)
+  float* scb = smem + S::cb_off;  // [C][BH][BW]
+  float* spp = smem + S::p_off;   // [2C][QH][QW]
+  float* smu = smem + S::mu_off;  // [2C][QH][QW]
+  float* sI = smem + S::I_off;    // [C][TH][TW]
 
   const int lx = threadIdx.x & 31, strip = threadIdx.x >> 5;
   const int x0 = blockIdx.x * TW, y0 = g.row0 + blockIdx.y * TH, b = blockIdx.z;
   const int W = g.W, H = g.H;
   const int x = x0 + lx, ybase = y0 + strip * P;
-  const long long plane = g.plane;
-  // ---- prefetch: group 0 = c tile (needed first), group 1 = cbar, p, mu, I
-  prefetch<C, SH, SW / 4>(sc, c + (long long)b * C * plane, plane, g, y0 - R, x0 - SX);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  prefetch<C, BH, BW / 4>(scb, cb + (long long)b * C * plane, plane, g, y0 - 1, x0 - BX);
-  prefetch<2 * C, QH, QW / 4>(spp, p + (long long)b * 2 * C * plane, plane, g, y0 - 1, x0 - BX);
-  prefetch<2 * C, QH, QW / 4>(smu, mu + (long long)b * 2 * C * plane, plane, g, y0 - 1, x0 - BX);
-  prefetch<C, TH, TW / 4>(sI, I + (long long)b * C * plane, plane, g, y0, x0);
-  asm volatile("cp.async.commit_group;" ::: "memory");
-  asm volatile("cp.async.wait_group 1;" ::: "memory");
+
+  // ---- TMA: barrier 0 = the c tile (needed first), barrier 1 = cbar, p, mu, I (land during step 1).
+  // Boxes outside the tensor (image borders, rows beyond the stored slab) are zero-filled.
+  __shared__ __align__(8) unsigned long long bars[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __syncthreads();
+  if (threadIdx.x == 0) {
+    const int ys = y0 - g.row0 + g.G;  // stored-row index of global row y0
+    mbar_expect_tx(&bars[0], (unsigned)(sizeof(float) * C * SH * SW));
+    tma_load3(sc, &tm.c, x0 - SX, ys - R, b * C, &bars[0]);
+    mbar_expect_tx(&bars[1], (unsigned)(sizeof(float) * (C * BH * BW + 4 * C * QH * QW + C * TH * TW)));
+    tma_load3(scb, &tm.cb, x0 - BX, ys - 1, b * C, &bars[1]);
+    tma_load3(spp, &tm.p, x0 - BX, ys - 1, b * 2 * C, &bars[1]);
+    tma_load3(smu, &tm.mu, x0 - BX, ys - 1, b * 2 * C, &bars[1]);
+    tma_load3(sI, &tm.I, x0, ys, b * C, &bars[1]);
+  }
+  mbar_wait(&bars[0], 0);
 
   // ---- step 1: agent Euler step for P rows (P/2 packed pixel pairs) of column x
   f2 ci[P / 2][C], acc[P / 2][C];
@@ -231,22 +284,10 @@ __global__ void __launch_bounds__(NT, 2)
     }
   const float qc = K.kernel == 0 ? 5.0f : 3.0f;
   const bool interior = x0 - R >= 0 && x0 + TW + R <= W && y0 - R >= 0 && y0 + TH + R <= H;
-  float mrow[P + 2 * R], mcol[2 * R + 1];
-  if (interior) {
-    agent_phase<R, false>(sc, om, K.e_c, qc, lx, strip, mrow, mcol, ci, acc);
-  } else {
-#pragma unroll
-    for (int k = 0; k < P + 2 * R; ++k) {
-      const int yy = ybase - R + k;
-      mrow[k] = (yy >= 0 && yy < H) ? 1.0f : 0.0f;
-    }
-#pragma unroll
-    for (int k = 0; k < 2 * R + 1; ++k) {
-      const int xx = x - R + k;
-      mcol[k] = (xx >= 0 && xx < W) ? 1.0f : 0.0f;
-    }
-    agent_phase<R, true>(sc, om, K.e_c, qc, lx, strip, mrow, mcol, ci, acc);
-  }
+  if (interior)
+    agent_phase<R, P, false>(sc, om, K.e_c, qc, lx, strip, x, ybase, W, H, ci, acc);
+  else
+    agent_phase<R, P, true>(sc, om, K.e_c, qc, lx, strip, x, ybase, W, H, ci, acc);
   const f2 DT = pk(K.dt_NR, K.dt_NR);
   float chalf[P][C];
 #pragma unroll
@@ -254,10 +295,10 @@ __global__ void __launch_bounds__(NT, 2)
 #pragma unroll
     for (int k = 0; k < C; ++k) upk(fma2(DT, acc[j][k], ci[j][k]), chalf[2 * j][k], chalf[2 * j + 1][k]);
 
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  __syncthreads();  // prefetch landed; the c tile is dead (sp reuses it)
+  mbar_wait(&bars[1], 0);
+  __syncthreads();  // every warp is done with the c tile (sp reuses it)
 
-  // ---- step 2: p+ at tile pixel (tx, ty) (tx, ty in [-1, 31]) -> sp[.][ty+1][tx+1]
+  // ---- step 2: p+ at tile pixel (tx, ty) (tx in [-1, 31], ty in [-1, TH-1]) -> sp[.][ty+1][tx+1]
   auto dual_at = [&](int tx, int ty) {
     const int xx = x0 + tx, yy = y0 + ty;
     if (xx < 0 || yy < 0 || xx >= W || yy >= H) return;
@@ -282,8 +323,8 @@ __global__ void __launch_bounds__(NT, 2)
   };
 #pragma unroll
   for (int r = 0; r < P; ++r) dual_at(lx, strip * P + r);
-  if (strip == 0) dual_at(lx, -1);      // halo row y0-1
-  else if (strip == 1) dual_at(-1, lx);  // halo column x0-1
+  if (strip == 0) dual_at(lx, -1);             // halo row y0-1
+  if (strip == 1 && lx < TH) dual_at(-1, lx);  // halo column x0-1
   __syncthreads();
 
   // ---- step 3: div p+ (R6), prox fidelity, extrapolation (R21), stores
@@ -312,8 +353,8 @@ __global__ void __launch_bounds__(NT, 2)
   }
 }
 
-// Kernel-order index of every interior offset (dx outer; within a column the dy of parity
-// m(dx) first, then the rest, each ascending).
+// Kernel-order index of every interior offset: dx ascending; within a column the even dy
+// ascending, then the odd dy ascending.
 template <int R>
 int kernel_order_index(int dx, int dy) {
   int n = 0;
@@ -321,16 +362,98 @@ int kernel_order_index(int dx, int dy) {
     const int m = col_m(R, a);
     if (m < 0) continue;
     for (int pass = 0; pass < 2; ++pass) {
-      const int par = pass == 0 ? (m & 1) : 1 - (m & 1);
       for (int e = -m; e <= m; ++e) {
         if (a == 0 && e == 0) continue;
-        if (((e + m) & 1) != par) continue;
+        if ((e & 1) != pass) continue;
         if (a == dx && e == dy) return n;
         ++n;
       }
     }
   }
   return -1;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)f;
+  });
+  return fn;
+}
+
+// 3-D map of a planar field: dims (x < W, stored row, image*nm + component), box (bw, bh, nm)
+bool encode_map(CUtensorMap* m, const MsaGeom& g, const float* base, int nm, int bw, int bh) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)(g.nrows + 2 * g.G), (cuuint64_t)g.nb * nm};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.plane * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)nm};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// small cache of encoded map sets (the ping-pong buffers of a few contexts)
+struct MapKey {
+  const float *c, *cb, *p, *mu, *I;
+  int W, rows, nb, pitch, R, P;
+  long long plane;
+  bool operator==(const MapKey& o) const { return memcmp(this, &o, sizeof(MapKey)) == 0; }
+};
+bool get_maps(const MapKey& k, const MsaGeom& g, int SH, int BH, int QH, int TH, TmaSet* out) {
+  static std::mutex mu;
+  static MapKey keys[16];
+  static TmaSet sets[16];
+  static int n = 0, next = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == k) {
+      *out = sets[i];
+      return true;
+    }
+  TmaSet t;
+  if (!encode_map(&t.c, g, k.c, C, SW, SH) || !encode_map(&t.cb, g, k.cb, C, BW, BH) ||
+      !encode_map(&t.p, g, k.p, 2 * C, QW, QH) || !encode_map(&t.mu, g, k.mu, 2 * C, QW, QH) ||
+      !encode_map(&t.I, g, k.I, C, TW, TH))
+    return false;
+  const int slot = n < 16 ? n++ : (next++ % 16);
+  keys[slot] = k;
+  sets[slot] = t;
+  *out = t;
+  return true;
+}
+
+template <int R, int P>
+cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om, const float* c, const float* cb,
+                      const float* p, const float* mu, const float* I, float* co, float* cbo, float* po,
+                      cudaStream_t s) {
+  using S = Smem<R, P>;
+  MapKey key;
+  memset(&key, 0, sizeof(key));
+  key.c = c; key.cb = cb; key.p = p; key.mu = mu; key.I = I;
+  key.W = g.W; key.rows = g.nrows + 2 * g.G; key.nb = g.nb; key.pitch = g.pitch; key.R = R; key.P = P;
+  key.plane = g.plane;
+  TmaSet tm;
+  if (!get_maps(key, g, S::SH, S::BH, S::QH, S::TH, &tm)) return cudaErrorNotSupported;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_iter_fast_c3<R, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  dim3 grd((g.W + TW - 1) / TW, (g.nrows + S::TH - 1) / S::TH, g.nb);
+  k_iter_fast_c3<R, P><<<grd, NT, S::bytes, s>>>(g, K, om, tm, co, cbo, po);
+  return cudaGetLastError();
 }
 
 template <int R>
@@ -349,16 +472,9 @@ cudaError_t launch_c3(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
     om.v[idx] = T.om[o];
     prev = idx;
   }
-  using S = Smem<R>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_iter_fast_c3<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  dim3 grd((g.W + TW - 1) / TW, (g.nrows + TH - 1) / TH, g.nb);
-  k_iter_fast_c3<R><<<grd, NT, S::bytes, s>>>(g, K, om, c, cb, p, mu, I, co, cbo, po);
-  return cudaGetLastError();
+  static const int rows_per_thread = getenv("MSA_K1_P") ? atoi(getenv("MSA_K1_P")) : 4;  // A/B hook
+  if (rows_per_thread == 4) return launch_rp<R, 4>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
+  return launch_rp<R, 2>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
 }
 
 }  // namespace
