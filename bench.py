@@ -280,13 +280,25 @@ def main():
     total_units = float(H) * W * B * cfg.iters * args.steps  # all ranks together
     value = total_units / (ms * 1e-3)
 
-    # roofline of the dominant kernel K1 (fused iteration): 44*C algorithmic bytes per pixel
+    # roofline of the dominant kernel K1 (fused iteration), DESIGN.md §5:
+    #  bytes: 44*C algorithmic bytes per pixel-iteration (11 C-float fields read or written)
+    #  ALU:   n_off*(3C+5) + 27C + 2 FP32 pipe operations per pixel-iteration (the interaction term
+    #         sub/square-sum/t/phi/accumulate per active offset, plus steps 2-3); peak = 148 SMs x
+    #         128 FP32 lanes x clocks.max.sm (B200_PROFILING.md unit counts).
     k1_avg_ms = tim["iter_ms"] / max(tim["iter_launches"], 1)
     alg_bytes = 44.0 * C * own_px
     achieved = alg_bytes / (k1_avg_ms * 1e-3) / 1e9
     peak, peak_src = _hbm_peak()
     traffic, _tr = _k1_traffic()
     k1_share = tim["iter_ms"] / ms_local if ms_local > 0 else None
+    n_off = info.active_offsets
+    alg_ops = (n_off * (3 * C + 5) + 27 * C + 2) * own_px
+    sm_count = torch.cuda.get_device_properties(local).multi_processor_count
+    alu_peak = sm_count * 128 * 1965e6 / 1e12  # T FP32 lane-ops/s at clocks.max.sm
+    alu_achieved = alg_ops / (k1_avg_ms * 1e-3) / 1e12
+    hbm_time = alg_bytes / (peak * 1e9)
+    alu_time = alg_ops / (alu_peak * 1e12)
+    bound = "alu" if alu_time > hbm_time else "hbm"
 
     # end to end through the public API with host buffers (pinned), H2D + D2H inside the timed region
     e2e = None
@@ -337,12 +349,20 @@ def main():
             "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded generator synth/, BASELINE config 4 recipe)",
             "config": _config(cfg, world),
-            "roofline": {"bound": "hbm", "kernel": "K1 msa_iter (fused agent + primal-dual iteration)",
-                         "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_src,
-                         "alg_bytes_per_launch": alg_bytes, "k1_avg_ms": k1_avg_ms,
-                         "k1_launches": tim["iter_launches"], "k1_share_of_step": k1_share,
-                         "hbm_frac_of_8TBs_spec": achieved / 8000.0},
+            "roofline": ({"bound": "alu", "achieved": alu_achieved, "peak": alu_peak,
+                          "unit": "T FP32 lane-ops/s", "frac": alu_achieved / alu_peak,
+                          "peak_source": f"derived: {sm_count} SMs x 128 FP32 lanes x 1965 MHz clocks.max.sm"}
+                         if bound == "alu" else
+                         {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                          "peak_source": peak_src}) | {
+                "kernel": "K1 msa_iter (fused agent + primal-dual iteration)", "traffic": traffic,
+                "alg_bytes_per_launch": alg_bytes, "alg_ops_per_launch": alg_ops, "k1_avg_ms": k1_avg_ms,
+                "k1_launches": tim["iter_launches"], "k1_share_of_step": k1_share,
+                "hbm": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                        "frac_of_8TBs_spec": achieved / 8000.0, "peak_source": peak_src},
+                "alu": {"achieved": alu_achieved, "peak": alu_peak, "unit": "T FP32 lane-ops/s",
+                        "frac": alu_achieved / alu_peak},
+                "floor_ms": {"hbm": hbm_time * 1e3, "alu": alu_time * 1e3}},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

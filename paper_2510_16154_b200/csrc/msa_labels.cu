@@ -32,7 +32,8 @@ struct MsaLabelScratch {
   unsigned long long* cl_sum = nullptr;   // [N][C]
   unsigned long long* cl_cnt = nullptr;   // [N]
   int32_t* scalars = nullptr;             // [4] S, K, cell_lo, cell_hi (as int bits)
-  double* dscal = nullptr;                // [2] min/max of m0
+  double* dscal = nullptr;                // [6] min/max of the hashed channel means
+  void* grid = nullptr;                   // CellGrid (device)
 };
 
 namespace {
@@ -48,10 +49,24 @@ __device__ __forceinline__ int uf_find(const int32_t* P, int x) {
   return x;
 }
 
+// find with path halving: parents only ever move to smaller ancestors, so pointing a node at
+// its grandparent (a plain store racing with other halvings or root hooks) keeps every
+// node in its set - the usual lock-free GPU union-find argument.
+__device__ __forceinline__ int uf_find_halve(int32_t* P, int x) {
+  while (true) {
+    const int p = __ldcg(P + x);
+    if (p == x) return x;
+    const int gp = __ldcg(P + p);
+    if (gp == p) return p;
+    __stcg(P + x, gp);
+    x = gp;
+  }
+}
+
 __device__ __forceinline__ void uf_unite(int32_t* P, int a, int b) {
   while (true) {
-    a = uf_find(P, a);
-    b = uf_find(P, b);
+    a = uf_find_halve(P, a);
+    b = uf_find_halve(P, b);
     if (a == b) return;
     if (a > b) { int t = a; a = b; b = t; }
     const int old = atomicCAS(P + b, b, a);  // hook the larger root under the smaller
@@ -84,7 +99,7 @@ __global__ void k_edges(MsaGeom g, const float* __restrict__ c, int b, float del
 __global__ void k_compress_flag(int32_t* P, int32_t* flag, int n) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
-  const int r = uf_find(P, x);
+  const int r = uf_find_halve(P, x);
   P[x] = r;
   flag[x] = (r == x) ? 1 : 0;
 }
@@ -137,11 +152,26 @@ __global__ void k_scan_add(int32_t* a, int n, const int32_t* off) {
 // ---- segments
 __global__ void k_seg_accum(MsaGeom g, const float* __restrict__ c, int b, const int32_t* __restrict__ P,
                             const int32_t* __restrict__ segidx, unsigned long long* sum, unsigned long long* cnt) {
+  // Exact 64-bit fixed-point sums. A warp of 32 consecutive pixels usually lies in one segment:
+  // then it reduces with shuffles and issues one atomic per value (integer sums: exact, order free).
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= g.W || j >= g.H) return;
-  const int n = j * g.W + i;
-  const int s = segidx[P[n]];
+  const bool valid = i < g.W && j < g.H;
+  const int s = valid ? segidx[P[j * g.W + i]] : -1;
+  const unsigned same = __match_any_sync(0xffffffffu, s);
+  if (same == 0xffffffffu) {
+    if (s < 0) return;
+    unsigned long long n1 = 1;
+    for (int o = 16; o > 0; o >>= 1) n1 += __shfl_xor_sync(0xffffffffu, n1, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(cnt + s, n1);
+    for (int k = 0; k < g.C; ++k) {
+      unsigned long long q = (unsigned long long)__double2ll_rn((double)c[msa_idx(g, b, k, g.C, j, i)] * 4294967296.0);
+      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+      if ((threadIdx.x & 31) == 0) atomicAdd(sum + (size_t)s * g.C + k, q);
+    }
+    return;
+  }
+  if (!valid) return;
   atomicAdd(cnt + s, 1ULL);
   for (int k = 0; k < g.C; ++k) {
     const long long q = __double2ll_rn((double)c[msa_idx(g, b, k, g.C, j, i)] * 4294967296.0);
@@ -177,24 +207,61 @@ __global__ void k_seg_mean(const int32_t* __restrict__ scal, int C, const unsign
   const double n = (double)cnt[s];
   for (int k = 0; k < C; ++k) mean[(size_t)s * C + k] = (double)(long long)sum[(size_t)s * C + k] / n * 0x1.0p-32;
   segP[s] = s;
-  atomicMinD(mm, mean[(size_t)s * C]);
-  atomicMaxD(mm + 1, mean[(size_t)s * C]);
+  for (int k = 0; k < C && k < 3; ++k) {  // bounding box of the means on the (up to 3) hashed channels
+    atomicMinD(mm + 2 * k, mean[(size_t)s * C + k]);
+    atomicMaxD(mm + 2 * k + 1, mean[(size_t)s * C + k]);
+  }
 }
 
-__device__ __forceinline__ double cell_width(double delta, const double* mm) {
-  const double span = mm[1] - mm[0];
-  const double wmin = span / (double)(NCELL_MAX - 4);
-  const double w = delta > wmin ? delta : wmin;
-  return w > 0 ? w : 1.0;
+// Stage (ii) candidate search: segments are hashed into a grid over the first D = min(C, 3)
+// channels with cell width w = delta / 2 (coarsened if the grid would exceed NCELL_MAX cells).
+// If C <= 3 and w <= delta / 2, two segments in one cell are within delta on every channel, so
+// each cell is united wholesale; otherwise every candidate pair is checked. Candidates lie in
+// cells within `reach` = ceil(delta / w) + 1 of each other per dimension (+1 guards rounding).
+struct CellGrid {
+  double lo[3];
+  double w;
+  int n[3];
+  int dims, ncells, reach, shortcut;
+};
+
+__global__ void k_cell_setup(const double* __restrict__ mm, int C, double delta, CellGrid* G) {
+  if (threadIdx.x != 0) return;
+  CellGrid g;
+  g.dims = C < 3 ? C : 3;
+  double span = 0.0;
+  for (int k = 0; k < 3; ++k) {
+    g.lo[k] = k < g.dims ? mm[2 * k] : 0.0;
+    const double sk = k < g.dims ? mm[2 * k + 1] - mm[2 * k] : 0.0;
+    span = sk > span ? sk : span;
+  }
+  double w = delta > 0 ? 0.5 * delta : 1.0;
+  const double cap = (double)(1 << (20 / g.dims));  // cells per dimension so that ncells <= 2^20
+  if (span / w + 1.0 > cap) w = span / (cap - 2.0);
+  if (!(w > 0)) w = 1.0;
+  g.w = w;
+  g.ncells = 1;
+  for (int k = 0; k < 3; ++k) {
+    g.n[k] = k < g.dims ? (int)floor((mm[2 * k + 1] - mm[2 * k]) / w) + 1 : 1;
+    g.ncells *= g.n[k];
+  }
+  g.reach = (int)ceil(delta / w) + 1;
+  g.shortcut = (C <= 3 && w <= 0.5 * delta) ? 1 : 0;
+  *G = g;
+}
+
+__device__ __forceinline__ int cell_coord(double m, double lo, double w, int n) {
+  int c = (int)floor((m - lo) / w);
+  return c < 0 ? 0 : (c >= n ? n - 1 : c);
 }
 
 __global__ void k_seg_cell(const int32_t* __restrict__ scal, int C, const double* __restrict__ mean,
-                           const double* __restrict__ mm, double delta, int32_t* seg_cell, int32_t* count) {
+                           const CellGrid* __restrict__ G, int32_t* seg_cell, int32_t* count) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= scal[0]) return;
-  const double w = cell_width(delta, mm);
-  int cell = (int)floor((mean[(size_t)s * C] - mm[0]) / w);
-  cell = cell < 0 ? 0 : (cell >= NCELL_MAX ? NCELL_MAX - 1 : cell);
+  const CellGrid g = *G;
+  int cell = 0;
+  for (int k = 0; k < g.dims; ++k) cell = cell * g.n[k] + cell_coord(mean[(size_t)s * C + k], g.lo[k], g.w, g.n[k]);
   seg_cell[s] = cell;
   atomicAdd(count + cell, 1);
 }
@@ -208,26 +275,64 @@ __global__ void k_seg_scatter(const int32_t* __restrict__ scal, const int32_t* _
   sorted[pos] = s;
 }
 
-// stage (ii): one thread per segment A; candidates B in A's cell (after A's position) and the
-// next two cells (cells are >= delta wide; +2 guards the rounding of the cell index).
+__device__ __forceinline__ bool close_means(const double* mA, const double* mB, int C, double delta) {
+  for (int k = 0; k < C; ++k)
+    if (!(fabs(mA[k] - mB[k]) <= delta)) return false;
+  return true;
+}
+
+// one thread per segment A (in cell order): unite with its cell (shortcut) or with the later
+// segments of its cell, and with the segments of the lexicographically later neighbour cells.
+// With the shortcut a thread stops scanning a neighbour cell at its first close segment (the
+// cell is already one set).
 __global__ void k_seg_pairs(const int32_t* __restrict__ scal, int C, const double* __restrict__ mean,
                             const int32_t* __restrict__ seg_cell, const int32_t* __restrict__ start,
-                            const int32_t* __restrict__ sorted, double delta, int32_t* segP) {
+                            const int32_t* __restrict__ sorted, const CellGrid* __restrict__ G, double delta,
+                            int32_t* segP) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   const int S = scal[0];
   if (q >= S) return;
+  const CellGrid g = *G;
   const int A = sorted[q];
   const int cell = seg_cell[A];
-  const int lastcell = cell + 3 <= NCELL_MAX ? cell + 3 : NCELL_MAX;
-  const int end = start[lastcell];
   const double* mA = mean + (size_t)A * C;
-  for (int r = q + 1; r < end; ++r) {
-    const int B = sorted[r];
-    const double* mB = mean + (size_t)B * C;
-    bool ok = true;
-    for (int k = 0; k < C && ok; ++k) ok = fabs(mA[k] - mB[k]) <= delta;
-    if (ok) uf_unite(segP, A, B);
+  int cc[3] = {0, 0, 0};
+  {
+    int rem = cell;
+    for (int k = g.dims - 1; k >= 0; --k) {
+      cc[k] = rem % g.n[k];
+      rem /= g.n[k];
+    }
   }
+  if (g.shortcut) {
+    const int first = sorted[start[cell]];
+    if (first != A) uf_unite(segP, A, first);
+  } else {
+    for (int r = q + 1; r < start[cell + 1]; ++r) {
+      const int B = sorted[r];
+      if (close_means(mA, mean + (size_t)B * C, C, delta)) uf_unite(segP, A, B);
+    }
+  }
+  const int R = g.reach;
+  const int r1 = g.dims > 1 ? R : 0, r2 = g.dims > 2 ? R : 0;
+  for (int d0 = -R; d0 <= R; ++d0)
+    for (int d1 = -r1; d1 <= r1; ++d1)
+      for (int d2 = -r2; d2 <= r2; ++d2) {
+        // lexicographically positive offsets only: each unordered cell pair once
+        if (d0 < 0 || (d0 == 0 && (d1 < 0 || (d1 == 0 && d2 <= 0)))) continue;
+        const int c0 = cc[0] + d0, c1 = cc[1] + d1, c2 = cc[2] + d2;
+        if (c0 < 0 || c0 >= g.n[0] || c1 < 0 || c1 >= g.n[1] || c2 < 0 || c2 >= g.n[2]) continue;
+        int nb = c0;
+        if (g.dims > 1) nb = nb * g.n[1] + c1;
+        if (g.dims > 2) nb = nb * g.n[2] + c2;
+        for (int r = start[nb]; r < start[nb + 1]; ++r) {
+          const int B = sorted[r];
+          if (close_means(mA, mean + (size_t)B * C, C, delta)) {
+            uf_unite(segP, A, B);
+            if (g.shortcut) break;
+          }
+        }
+      }
 }
 
 __global__ void k_seg_compress(const int32_t* __restrict__ scal, int32_t* segP, int32_t* seg_flag) {
@@ -304,7 +409,7 @@ void msa_labels_free(MsaLabelScratch* s) {
   if (!s) return;
   void* ptrs[] = {s->parent, s->flag, s->scan_tmp, s->seg_parent, s->seg_flag, s->flag_copy, s->seg_sum, s->seg_cnt,
                   s->seg_mean, s->cell_count, s->cell_fill, s->sorted, s->seg_cell, s->cl_sum, s->cl_cnt,
-                  s->scalars, s->dscal};
+                  s->scalars, s->dscal, s->grid};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete s;
@@ -325,7 +430,7 @@ cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delt
         (e = grow(&S->seg_cnt, n)) || (e = grow(&S->seg_mean, n * C)) ||
         (e = grow(&S->cell_count, (size_t)NCELL_MAX + 1)) || (e = grow(&S->cell_fill, (size_t)NCELL_MAX)) ||
         (e = grow(&S->sorted, n)) || (e = grow(&S->seg_cell, n)) || (e = grow(&S->cl_sum, n * C)) ||
-        (e = grow(&S->cl_cnt, n)) || (e = grow(&S->scalars, 4)) || (e = grow(&S->dscal, 2)))
+        (e = grow(&S->cl_cnt, n)) || (e = grow(&S->scalars, 4)) || (e = grow(&S->dscal, 6)) || (e = cudaMalloc(&S->grid, 256)))
       return e;
     S->cap_px = n;
     S->C = C;
@@ -347,16 +452,17 @@ cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delt
   k_seg_accum<<<grd, blk, 0, st>>>(g, c, b, S->parent, S->flag, S->seg_sum, S->seg_cnt);
   ++*launches;
   // (ii) segment means, channel-0 cells, candidate pairs
-  const double init_mm[2] = {INFINITY, -INFINITY};
+  const double init_mm[6] = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY};
   cudaMemcpyAsync(S->dscal, init_mm, sizeof(init_mm), cudaMemcpyHostToDevice, st);
   k_seg_mean<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_sum, S->seg_cnt, S->seg_mean, S->seg_parent, S->dscal);
   cudaMemsetAsync(S->cell_count, 0, sizeof(int32_t) * (NCELL_MAX + 1), st);
   cudaMemsetAsync(S->cell_fill, 0, sizeof(int32_t) * NCELL_MAX, st);
-  k_seg_cell<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, S->dscal, (double)delta, S->seg_cell, S->cell_count);
-  *launches += 2;
+  k_cell_setup<<<1, 32, 0, st>>>(S->dscal, C, (double)delta, (CellGrid*)S->grid);
+  k_seg_cell<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, (const CellGrid*)S->grid, S->seg_cell, S->cell_count);
+  *launches += 3;
   if ((e = scan_excl(S->cell_count, NCELL_MAX + 1, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
   k_seg_scatter<<<nbN, T, 0, st>>>(S->scalars, S->seg_cell, S->cell_count, S->cell_fill, S->sorted);
-  k_seg_pairs<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, S->seg_cell, S->cell_count, S->sorted, (double)delta,
+  k_seg_pairs<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, S->seg_cell, S->cell_count, S->sorted, (const CellGrid*)S->grid, (double)delta,
                                  S->seg_parent);
   k_seg_compress<<<nbN, T, 0, st>>>(S->scalars, S->seg_parent, S->seg_flag);
   *launches += 3;
