@@ -60,6 +60,7 @@ __device__ __forceinline__ f2 relu2(f2 v) {
 // ---- TMA (cp.async.bulk.tensor) + mbarrier helpers
 struct TmaSet {
   CUtensorMap c, cb, p, mu, I;  // 3-D maps (x, stored row, component) of the five input fields
+  CUtensorMap co, cbo, po;      // the three outputs (rows clipped at the slab's end)
 };
 __device__ __forceinline__ unsigned saddr(const void* q) { return (unsigned)__cvta_generic_to_shared(q); }
 __device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
@@ -78,6 +79,12 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
       "@!p bra WAIT%=;\n\t}" ::"r"(saddr(b)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void tma_store3(const CUtensorMap* map, int x, int y, int z, const void* src) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+                   (unsigned long long)map),
+               "r"(x), "r"(y), "r"(z), "r"(saddr(src))
+               : "memory");
 }
 __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int x, int y, int z,
                                           unsigned long long* bar) {
@@ -234,8 +241,7 @@ struct Occ {
 
 template <int R, int P>
 __global__ void __launch_bounds__(NT, Occ<P>::blocks)
-    k_iter_fast_c3(MsaGeom g, MsaIterConsts K, FastOm om, const __grid_constant__ TmaSet tm,
-                   float* __restrict__ c_out, float* __restrict__ cb_out, float* __restrict__ p_out) {
+    k_iter_fast_c3(MsaGeom g, MsaIterConsts K, FastOm om, const __grid_constant__ TmaSet tm) {
   using S = Smem<R, P>;
   constexpr int TH = S::TH, SH = S::SH, BH = S::BH, QH = S::QH, SPH = S::SPH;
   extern __shared__ __align__(128) float smem[];
@@ -327,29 +333,42 @@ __global__ void __launch_bounds__(NT, Occ<P>::blocks)
   if (strip == 1 && lx < TH) dual_at(-1, lx);  // halo column x0-1
   __syncthreads();
 
-  // ---- step 3: div p+ (R6), prox fidelity, extrapolation (R21), stores
-  if (x >= W) return;
-  const int rend = g.row0 + g.nrows;
+  // ---- step 3: div p+ (R6), prox fidelity, extrapolation (R21) -> output tiles in smem (the p,
+  // mu buffers are dead), then TMA tensor stores (clipped at the image / slab edges)
+  float* oc = spp;                 // [C][TH][TW] c+
+  float* ocb = spp + C * TH * TW;  // [C][TH][TW] cbar+
+  float* op = smu;                 // [2C][TH][TW] p+
+  if (x < W) {
 #pragma unroll
-  for (int r = 0; r < P; ++r) {
-    const int yy = ybase + r;
-    if (yy >= rend) break;
-    const int sy = strip * P + r + 1, sx = lx + 1;
+    for (int r = 0; r < P; ++r) {
+      const int ty = strip * P + r, yy = ybase + r;
+      const int sy = ty + 1, sx = lx + 1;
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const float qx0 = sp[(k * SPH + sy) * SPW + sx], qy0 = sp[((C + k) * SPH + sy) * SPW + sx];
-      float ax = x < W - 1 ? qx0 : 0.0f;
-      if (x > 0) ax = __fsub_rn(ax, sp[(k * SPH + sy) * SPW + sx - 1]);
-      float ay = yy < H - 1 ? qy0 : 0.0f;
-      if (yy > 0) ay = __fsub_rn(ay, sp[((C + k) * SPH + sy - 1) * SPW + sx]);
-      const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
-      float cp, cbp;
-      msa_prox_extrap(K, chalf[r][k], d, sI[(k * TH + strip * P + r) * TW + lx], cp, cbp);
-      c_out[msa_idx(g, b, k, C, yy, x)] = cp;
-      cb_out[msa_idx(g, b, k, C, yy, x)] = cbp;
-      p_out[msa_idx(g, b, k, 2 * C, yy, x)] = qx0;
-      p_out[msa_idx(g, b, C + k, 2 * C, yy, x)] = qy0;
+      for (int k = 0; k < C; ++k) {
+        const float qx0 = sp[(k * SPH + sy) * SPW + sx], qy0 = sp[((C + k) * SPH + sy) * SPW + sx];
+        float ax = x < W - 1 ? qx0 : 0.0f;
+        if (x > 0) ax = __fsub_rn(ax, sp[(k * SPH + sy) * SPW + sx - 1]);
+        float ay = yy < H - 1 ? qy0 : 0.0f;
+        if (yy > 0) ay = __fsub_rn(ay, sp[((C + k) * SPH + sy - 1) * SPW + sx]);
+        const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
+        float cp, cbp;
+        msa_prox_extrap(K, chalf[r][k], d, sI[(k * TH + ty) * TW + lx], cp, cbp);
+        oc[(k * TH + ty) * TW + lx] = cp;
+        ocb[(k * TH + ty) * TW + lx] = cbp;
+        op[(k * TH + ty) * TW + lx] = qx0;
+        op[((C + k) * TH + ty) * TW + lx] = qy0;
+      }
     }
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int ys = y0 - g.row0 + g.G;
+    tma_store3(&tm.co, x0, ys, b * C, oc);
+    tma_store3(&tm.cbo, x0, ys, b * C, ocb);
+    tma_store3(&tm.po, x0, ys, b * 2 * C, op);
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem must outlive the reads
   }
 }
 
@@ -391,10 +410,12 @@ EncodeTiledFn encode_fn() {
 }
 
 // 3-D map of a planar field: dims (x < W, stored row, image*nm + component), box (bw, bh, nm)
-bool encode_map(CUtensorMap* m, const MsaGeom& g, const float* base, int nm, int bw, int bh) {
+bool encode_map(CUtensorMap* m, const MsaGeom& g, const float* base, int nm, int bw, int bh, bool output = false) {
   EncodeTiledFn fn = encode_fn();
   if (!fn) return false;
-  const cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)(g.nrows + 2 * g.G), (cuuint64_t)g.nb * nm};
+  // inputs span every stored row (ghosts included); outputs stop at the slab's last owned row
+  const cuuint64_t rows = output ? (cuuint64_t)(g.G + g.nrows) : (cuuint64_t)(g.nrows + 2 * g.G);
+  const cuuint64_t dims[3] = {(cuuint64_t)g.W, rows, (cuuint64_t)g.nb * nm};
   const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.plane * 4};
   const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)nm};
   const cuuint32_t es[3] = {1, 1, 1};
@@ -405,7 +426,7 @@ bool encode_map(CUtensorMap* m, const MsaGeom& g, const float* base, int nm, int
 
 // small cache of encoded map sets (the ping-pong buffers of a few contexts)
 struct MapKey {
-  const float *c, *cb, *p, *mu, *I;
+  const float *c, *cb, *p, *mu, *I, *co, *cbo, *po;
   int W, rows, nb, pitch, R, P;
   long long plane;
   bool operator==(const MapKey& o) const { return memcmp(this, &o, sizeof(MapKey)) == 0; }
@@ -424,7 +445,8 @@ bool get_maps(const MapKey& k, const MsaGeom& g, int SH, int BH, int QH, int TH,
   TmaSet t;
   if (!encode_map(&t.c, g, k.c, C, SW, SH) || !encode_map(&t.cb, g, k.cb, C, BW, BH) ||
       !encode_map(&t.p, g, k.p, 2 * C, QW, QH) || !encode_map(&t.mu, g, k.mu, 2 * C, QW, QH) ||
-      !encode_map(&t.I, g, k.I, C, TW, TH))
+      !encode_map(&t.I, g, k.I, C, TW, TH) || !encode_map(&t.co, g, k.co, C, TW, TH, true) ||
+      !encode_map(&t.cbo, g, k.cbo, C, TW, TH, true) || !encode_map(&t.po, g, k.po, 2 * C, TW, TH, true))
     return false;
   const int slot = n < 16 ? n++ : (next++ % 16);
   keys[slot] = k;
@@ -440,7 +462,7 @@ cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om
   using S = Smem<R, P>;
   MapKey key;
   memset(&key, 0, sizeof(key));
-  key.c = c; key.cb = cb; key.p = p; key.mu = mu; key.I = I;
+  key.c = c; key.cb = cb; key.p = p; key.mu = mu; key.I = I; key.co = co; key.cbo = cbo; key.po = po;
   key.W = g.W; key.rows = g.nrows + 2 * g.G; key.nb = g.nb; key.pitch = g.pitch; key.R = R; key.P = P;
   key.plane = g.plane;
   TmaSet tm;
@@ -452,7 +474,7 @@ cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om
     attr_set = true;
   }
   dim3 grd((g.W + TW - 1) / TW, (g.nrows + S::TH - 1) / S::TH, g.nb);
-  k_iter_fast_c3<R, P><<<grd, NT, S::bytes, s>>>(g, K, om, tm, co, cbo, po);
+  k_iter_fast_c3<R, P><<<grd, NT, S::bytes, s>>>(g, K, om, tm);
   return cudaGetLastError();
 }
 

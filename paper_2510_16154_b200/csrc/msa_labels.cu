@@ -8,6 +8,8 @@
 // index of its set and the result is independent of thread scheduling.
 // Paper: clusters in colour space PAPER.md:55, :116; histograms PAPER.md:274, :281, :494.
 #include <math.h>
+#include <cstdio>
+#include <cstdlib>
 #include <stdint.h>
 
 #include "msa_internal.h"
@@ -99,7 +101,9 @@ __global__ void k_edges(MsaGeom g, const float* __restrict__ c, int b, float del
 __global__ void k_compress_flag(int32_t* P, int32_t* flag, int n) {
   const int x = blockIdx.x * blockDim.x + threadIdx.x;
   if (x >= n) return;
-  const int r = uf_find_halve(P, x);
+  // read-only chase: a halving store racing with another thread's final P[y] = root could leave
+  // P[y] pointing at a non-root ancestor after this kernel
+  const int r = uf_find(P, x);
   P[x] = r;
   flag[x] = (r == x) ? 1 : 0;
 }
@@ -225,7 +229,7 @@ struct CellGrid {
   int dims, ncells, reach, shortcut;
 };
 
-__global__ void k_cell_setup(const double* __restrict__ mm, int C, double delta, CellGrid* G) {
+__global__ void k_cell_setup(const double* __restrict__ mm, int C, double delta, int allow_shortcut, CellGrid* G) {
   if (threadIdx.x != 0) return;
   CellGrid g;
   g.dims = C < 3 ? C : 3;
@@ -246,7 +250,7 @@ __global__ void k_cell_setup(const double* __restrict__ mm, int C, double delta,
     g.ncells *= g.n[k];
   }
   g.reach = (int)ceil(delta / w) + 1;
-  g.shortcut = (C <= 3 && w <= 0.5 * delta) ? 1 : 0;
+  g.shortcut = (allow_shortcut && C <= 3 && w <= 0.5 * delta) ? 1 : 0;
   *G = g;
 }
 
@@ -457,7 +461,8 @@ cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delt
   k_seg_mean<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_sum, S->seg_cnt, S->seg_mean, S->seg_parent, S->dscal);
   cudaMemsetAsync(S->cell_count, 0, sizeof(int32_t) * (NCELL_MAX + 1), st);
   cudaMemsetAsync(S->cell_fill, 0, sizeof(int32_t) * NCELL_MAX, st);
-  k_cell_setup<<<1, 32, 0, st>>>(S->dscal, C, (double)delta, (CellGrid*)S->grid);
+  static const bool no_shortcut = getenv("MSA_LABELS_NO_SHORTCUT") != nullptr;  // debug hook
+  k_cell_setup<<<1, 32, 0, st>>>(S->dscal, C, (double)delta, no_shortcut ? 0 : 1, (CellGrid*)S->grid);
   k_seg_cell<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, (const CellGrid*)S->grid, S->seg_cell, S->cell_count);
   *launches += 3;
   if ((e = scan_excl(S->cell_count, NCELL_MAX + 1, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
@@ -480,5 +485,15 @@ cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delt
   const int npal = max_k > 0 ? max_k : 1;
   k_palette<<<(npal + T - 1) / T, T, 0, st>>>(S->scalars, C, S->cl_sum, S->cl_cnt, palette_dev, max_k, count_dev);
   *launches += 2;
+  if (getenv("MSA_LABELS_DEBUG")) {  // debug hook: segment / cluster counts and the cell grid
+    int32_t sc[2];
+    double g[8];
+    cudaMemcpyAsync(sc, S->scalars, sizeof(sc), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(g, S->grid, sizeof(g), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    const int* gi = (const int*)(g + 4);
+    fprintf(stderr, "msa_labels: segments %d clusters %d | lo %g %g %g w %g n %d %d %d dims %d ncells %d reach %d shortcut %d\n",
+            sc[0], sc[1], g[0], g[1], g[2], g[3], gi[0], gi[1], gi[2], gi[3], gi[4], gi[5], gi[6]);
+  }
   return cudaGetLastError();
 }

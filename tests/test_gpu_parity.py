@@ -161,6 +161,23 @@ def test_labels_bitexact_same_field():
     assert gcnt[0] == ocnt and np.array_equal(glab[0], olab)
 
 
+@pytest.mark.parametrize("name,H,W,B,delta", [("cfg3", 384, 320, None, 0.1), ("cfg3", 256, 256, None, 0.02),
+                                              ("cfg5", 96, 80, 2, 0.1), ("cfg1", 64, 64, None, 0.0),
+                                              ("cfg2", 200, 3, None, 0.1), ("cfg4", 1, 300, None, 0.15)])
+def test_labels_bitexact_raw_fields(name, H, W, B, delta):
+    """K4 vs the oracle's Q(c; delta) on unsmoothed inputs: many segments, salt-and-pepper outliers,
+    C = 16 (no same-cell shortcut), delta = 0, one-pixel-wide images."""
+    cfg, img, sp = config_case(name, H, W, B)
+    with _solver(img, sp) as s:
+        glab, gcnt, gpal = s.labels(delta, max_k=32)
+    for b in range(img.shape[0]):
+        olab, ocnt, opal = oracle.labels(img[b], delta, max_k=32)
+        assert gcnt[b] == ocnt
+        assert np.array_equal(glab[b], olab)
+        k = min(ocnt, 32)
+        assert np.array_equal(gpal[b][:k], opal[:k])
+
+
 def test_mean_preserved_gpu():
     """P8 on the GPU: the per-channel mean is preserved (fp32 drift only)."""
     cfg, img, sp = config_case("cfg1")
