@@ -34,6 +34,7 @@ struct MsaIterConsts {
   float e_c;        // eps_c / 2                     (eq:ellipsoid)
   int kernel;       // 0 Wendland t^4 (5 - 4t), 1 printed t^4 (3 - 4t)   (eq:kernel, R3)
   int n_off;        // active offsets (generic kernel)
+  int radius;       // window radius R (generic kernel's smem halo)
   float inv_hx, inv_hy;
   float a_rs;       // rho / (rho + sigma)           (step 2, R7)
   float sigma;

@@ -257,6 +257,7 @@ MsaIterConsts iter_consts(const msa_ctx* x, double rho) {
   K.e_c = (float)(0.5 * p.eps_c);
   K.kernel = p.kernel;
   K.n_off = x->T.n;
+  K.radius = p.radius;
   K.inv_hx = (float)(1.0 / x->hx);
   K.inv_hy = (float)(1.0 / x->hy);
   K.a_rs = (float)(rho / (rho + x->sigma));

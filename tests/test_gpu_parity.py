@@ -129,6 +129,54 @@ def test_config_parity(case):
     assert len(gst) == cfg.rounds
 
 
+@pytest.mark.parametrize("over,C", [
+    (dict(radius=8), 16),            # maximum radius and channel count (generic kernel)
+    (dict(radius=0), 3),             # no interaction at all (N_R = 1)
+    (dict(radius=1), 3),             # R = 1: every neighbour on the ring, phi = 0 (R22)
+    (dict(dt=0.0), 3),               # pure primal-dual (P14-P17 regime)
+    (dict(alpha=0.0), 2),            # no fidelity: D and gap NaN by definition
+    (dict(beta=0.0), 3),             # no TV: p stays 0
+    (dict(kappa=1.7, theta=0.0), 3), # penalty growth, no extrapolation
+    (dict(eps_x=50.0, radius=4), 3), # small eps_x: ring offsets active -> generic kernel
+    (dict(kernel=1), 1),             # printed (repulsive) kernel, grey
+])
+def test_degenerate_and_extreme_params(over, C):
+    rng = np.random.default_rng(len(str(over)) + C)
+    H, W = 29, 35
+    img = rng.random((1, H, W, C), dtype=np.float32)
+    h = 1.0 / (W - 1)
+    sp = dict(alpha=8.0 / h, beta=1.0, radius=3, kernel=0, eps_x=0.0, eps_c=57.0, dt=0.25, rho=2.5 * h,
+              gamma=2.5 * h, kappa=1.0, tau=0.0, sigma=0.0, theta=1.0, iters_per_round=7, rounds=3)
+    sp.update(over)
+    with _solver(img, sp) as s:
+        st = s.solve()
+        gc = s.get_field(msa.FIELD_C)[0]
+    ref = run_oracle(img, sp)[0]
+    assert np.max(rel_err_per_pixel(gc, ref.c)) <= 1e-4
+    if sp["alpha"] == 0:
+        assert all(np.isnan(r["dual"]) and np.isnan(r["gap"]) for r in st)
+    else:
+        for r, o in zip(st, ref.stats):
+            assert r["primal"] == pytest.approx(o[2], rel=1e-3, abs=1e-6)
+            assert r["rho"] == pytest.approx(o[6], rel=1e-12)
+    if sp["beta"] == 0:
+        with _solver(img, sp) as s:
+            s.solve()
+            assert not np.any(s.get_field(msa.FIELD_P))
+
+
+def test_invalid_shapes_rejected():
+    """Empty images and over-size parameters fail with MSA_EINVAL (no partial state)."""
+    sp = synth.solver_params(synth.CONFIGS["cfg1"])
+    for shape in [(1, 0, 8, 3), (1, 8, 0, 3), (0, 8, 8, 3)]:
+        img = np.zeros((max(shape[0], 1), max(shape[1], 1), max(shape[2], 1), 3), np.float32)
+        p = gpu_params(img, sp)
+        p.batch, p.height, p.width = shape[0], shape[1], shape[2]
+        with pytest.raises(msa.MsaError) as e:
+            msa.Solver(p, img)
+        assert e.value.code == msa.MSA_EINVAL
+
+
 def test_constant_image_is_fixed_point_bitwise():
     """P9 on the GPU: I constant => c = cbar = I, p = mu = 0 bitwise after every iteration."""
     img = np.full((1, 24, 30, 3), 0.375, dtype=np.float32)
