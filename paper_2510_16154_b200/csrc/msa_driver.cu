@@ -453,6 +453,22 @@ int do_round(msa_ctx* x) {
   return MSA_OK;
 }
 
+// K1 variant (A/B and test hook, environment MSA_K1 = tile | sweep | generic; MSA_FORCE_GENERIC=1
+// is the old spelling of generic). Default: the tiled kernel where it applies, else the generic
+// one; the pair-symmetric sweep kernel is opt-in until it is the faster one. All variants compute
+// the same iteration.
+enum { K1_SWEEP = 0, K1_TILE = 1, K1_GENERIC = 2 };
+int k1_variant() {
+  static const int v = [] {
+    if (getenv("MSA_FORCE_GENERIC")) return (int)K1_GENERIC;
+    const char* e = getenv("MSA_K1");
+    if (!e || !strcmp(e, "tile")) return (int)K1_TILE;
+    if (!strcmp(e, "sweep")) return (int)K1_SWEEP;
+    return (int)K1_GENERIC;
+  }();
+  return v;
+}
+
 int do_steps(msa_ctx* x, int64_t n) {
   const msa_params& P = x->prm;
   const int K = P.iters_per_round;
@@ -467,7 +483,14 @@ int do_steps(msa_ctx* x, int64_t n) {
     }
     iter_batch_begin(x);
     int launched = 0;
-    cudaError_t e = msa_launch_iter_fast(x->g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
+    cudaError_t e = cudaErrorNotSupported;
+    if (k1_variant() == K1_SWEEP)
+      e = msa_launch_iter_sweep(x->g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
+                                x->cb[o], x->p[o], x->stream, &launched);
+    if (!launched && e != cudaErrorNotSupported && e != cudaSuccess)
+      return set_err(MSA_ECUDA, "sweep iteration kernel: %s", cudaGetErrorString(e));
+    if (!launched && k1_variant() != K1_GENERIC)
+      e = msa_launch_iter_fast(x->g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
                                          x->cb[o], x->p[o], x->stream, &launched);
     if (!launched) {
       if (e != cudaErrorNotSupported && e != cudaSuccess)

@@ -23,6 +23,12 @@ cudaError_t msa_launch_iter_fast(const MsaGeom& g, const MsaIterConsts& K, const
                                  const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                  float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched);
 
+// Pair-symmetric sweep form of the fused iteration (msa_iter_sweep.cu), C = 3, R in [2,5].
+// Same contract as msa_launch_iter_fast.
+cudaError_t msa_launch_iter_sweep(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                                  const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                                  float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched);
+
 // Round update (steps 4-5): writes mu_out (may alias mu) and per-block fp64 partial sums
 // [nb][nblk][MSA_NSUM]; *nblk receives the number of blocks per image.
 cudaError_t msa_launch_round(const MsaGeom& g, const MsaRoundConsts& R, const float* c, const float* p,

@@ -25,75 +25,17 @@
 #include <mutex>
 
 #include "msa_internal.h"
+#include "msa_f32x2.cuh"
+#include "msa_tma.cuh"
 
 namespace {
 
-typedef unsigned long long f2;  // two fp32 lanes in one 64-bit register pair
-
-__device__ __forceinline__ f2 pk(float a, float b) {
-  f2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ void upk(f2 v, float& a, float& b) { asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v)); }
-__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
-  f2 d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
-  f2 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
-  f2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ f2 relu2(f2 v) {
-  float a, b;
-  upk(v, a, b);
-  return pk(fmaxf(a, 0.0f), fmaxf(b, 0.0f));
-}
-
-// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers
 struct TmaSet {
   CUtensorMap c, cb, p, mu, I;  // 3-D maps (x, stored row, component) of the five input fields
   CUtensorMap co, cbo, po;      // the three outputs (rows clipped at the slab's end)
 };
-__device__ __forceinline__ unsigned saddr(const void* q) { return (unsigned)__cvta_generic_to_shared(q); }
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(saddr(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT%=;\n\t}" ::"r"(saddr(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_store3(const CUtensorMap* map, int x, int y, int z, const void* src) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
-                   (unsigned long long)map),
-               "r"(x), "r"(y), "r"(z), "r"(saddr(src))
-               : "memory");
-}
-__device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int x, int y, int z,
-                                          unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
-          saddr(dst)),
-      "l"((unsigned long long)map), "r"(x), "r"(y), "r"(z), "r"(saddr(bar))
-      : "memory");
-}
+using namespace msa_tma;
+using namespace msa_f32x2;
 
 constexpr int C = 3;
 constexpr int TW = 32;           // tile width (= lanes)
@@ -390,38 +332,6 @@ int kernel_order_index(int dx, int dy) {
     }
   }
   return -1;
-}
-
-// cuTensorMapEncodeTiled through the runtime's driver entry point (no libcuda link)
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = nullptr;
-  static std::once_flag once;
-  std::call_once(once, [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      fn = (EncodeTiledFn)f;
-  });
-  return fn;
-}
-
-// 3-D map of a planar field: dims (x < W, stored row, image*nm + component), box (bw, bh, nm)
-bool encode_map(CUtensorMap* m, const MsaGeom& g, const float* base, int nm, int bw, int bh, bool output = false) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn) return false;
-  // inputs span every stored row (ghosts included); outputs stop at the slab's last owned row
-  const cuuint64_t rows = output ? (cuuint64_t)(g.G + g.nrows) : (cuuint64_t)(g.nrows + 2 * g.G);
-  const cuuint64_t dims[3] = {(cuuint64_t)g.W, rows, (cuuint64_t)g.nb * nm};
-  const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.plane * 4};
-  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)nm};
-  const cuuint32_t es[3] = {1, 1, 1};
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // small cache of encoded map sets (the ping-pong buffers of a few contexts)

@@ -1,5 +1,5 @@
 """Subprocess helper for kernel-variant tests: runs one case through the C ABI and saves the
-fields. The kernel variant is chosen by the environment of the process (MSA_FORCE_GENERIC)."""
+fields. The kernel variant is chosen by the environment of the process (MSA_K1 = sweep | tile | generic)."""
 import json
 import os
 import sys

@@ -1,6 +1,11 @@
-"""The specialised K1 (msa_iter_fast.cu) against the generic kernel: bitwise-identical fields
-(same per-pixel arithmetic and term order), over tile-aligned, ragged and tiny shapes, every
-specialised radius, both kernel forms, and across a multiplier round."""
+"""K1 variants against the generic kernel (msa_kernels.cu), over tile-aligned, ragged and tiny
+shapes, every specialised radius, both kernel forms, and across a multiplier round:
+  * the tiled kernel (msa_iter_fast.cu) has the generic kernel's per-pixel arithmetic and term order:
+    bitwise-identical fields;
+  * the pair-symmetric sweep kernel (msa_iter_sweep.cu) evaluates each pair weight once and sums the
+    terms in another (fixed) order: p+ of one iteration is bitwise equal (it does not depend on the
+    agent sums), c and cbar agree to fp32 rounding, and its results are bitwise independent of the
+    segment length (MSA_SWEEP_SEG) and reproducible run to run."""
 import json
 import os
 import subprocess
@@ -14,13 +19,15 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(spec, generic: bool, tmp_path):
-    out = str(tmp_path / ("gen.npz" if generic else "fast.npz"))
+def _run(spec, variant: str, tmp_path, seg: int = 0):
+    out = str(tmp_path / f"{variant}_{seg}.npz")
     env = dict(os.environ)
-    if generic:
-        env["MSA_FORCE_GENERIC"] = "1"
+    env.pop("MSA_FORCE_GENERIC", None)
+    env["MSA_K1"] = variant
+    if seg:
+        env["MSA_SWEEP_SEG"] = str(seg)
     else:
-        env.pop("MSA_FORCE_GENERIC", None)
+        env.pop("MSA_SWEEP_SEG", None)
     subprocess.run([sys.executable, os.path.join(HERE, "_run_case.py"), json.dumps(spec), out], check=True, env=env)
     return np.load(out)
 
@@ -31,14 +38,55 @@ CASES = [
 ]
 
 
-@pytest.mark.parametrize("shape,R,ker", CASES)
-def test_fast_equals_generic_bitwise(shape, R, ker, tmp_path):
+def _spec(shape, R, ker, iters=3):
     B, H, W, C = shape
     h = 1.0 / (W - 1) if W > 1 else 1.0
-    spec = dict(seed=H * 1000 + W + R, shape=list(shape), iters=3,
+    return dict(seed=H * 1000 + W + R, shape=list(shape), iters=iters,
                 params=dict(alpha=8.0 / h, beta=1.0, radius=R, kernel=ker, eps_c=20.0, dt=0.25, rho=2.5 * h,
                             gamma=2.5 * h, iters_per_round=2, rounds=1))
-    a = _run(spec, True, tmp_path)
-    b = _run(spec, False, tmp_path)
+
+
+@pytest.mark.parametrize("shape,R,ker", CASES)
+def test_tile_equals_generic_bitwise(shape, R, ker, tmp_path):
+    spec = _spec(shape, R, ker)
+    a = _run(spec, "generic", tmp_path)
+    b = _run(spec, "tile", tmp_path)
     for k in ("c", "cbar", "p", "mu"):
         assert np.array_equal(a[k], b[k]), (k, float(np.max(np.abs(a[k] - b[k]))))
+
+
+SWEEP_CASES = CASES + [((1, 97, 131, 3), 5, 0), ((3, 45, 61, 3), 3, 1), ((1, 33, 28, 3), 5, 0), ((1, 4, 200, 3), 2, 0)]
+
+
+@pytest.mark.parametrize("shape,R,ker", SWEEP_CASES)
+def test_sweep_matches_generic(shape, R, ker, tmp_path):
+    # one iteration: p+ does not depend on the agent sums -> bitwise; c, cbar to fp32 rounding
+    spec1 = _spec(shape, R, ker, iters=1)
+    a = _run(spec1, "generic", tmp_path)
+    b = _run(spec1, "sweep", tmp_path)
+    assert np.array_equal(a["p"], b["p"])
+    assert np.array_equal(a["mu"], b["mu"])
+    for k in ("c", "cbar"):
+        err = np.max(np.abs(a[k] - b[k]))
+        assert err <= 2e-6, (k, float(err))
+    # three iterations across a multiplier round
+    spec = _spec(shape, R, ker)
+    a = _run(spec, "generic", tmp_path)
+    b = _run(spec, "sweep", tmp_path)
+    for k in ("c", "cbar", "p", "mu"):
+        scale = max(1.0, float(np.max(np.abs(a[k]))))
+        err = np.max(np.abs(a[k] - b[k])) / scale
+        assert err <= 2e-5, (k, float(err))
+
+
+@pytest.mark.parametrize("shape,R", [((1, 130, 97, 3), 5), ((2, 70, 66, 3), 3), ((1, 37, 29, 3), 2)])
+def test_sweep_segment_invariant_and_reproducible(shape, R, tmp_path):
+    spec = _spec(shape, R, 0)
+    ref = _run(spec, "sweep", tmp_path)
+    again = _run(spec, "sweep", tmp_path, seg=0)
+    for seg in (1, 3, 7):
+        other = _run(spec, "sweep", tmp_path, seg=seg)
+        for k in ("c", "cbar", "p", "mu"):
+            assert np.array_equal(ref[k], other[k]), (seg, k)
+    for k in ("c", "cbar", "p", "mu"):
+        assert np.array_equal(ref[k], again[k]), k
