@@ -15,7 +15,8 @@ from dataclasses import dataclass, asdict, field
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libmsa.so")
+# MSA_LIB: A/B hook for variant builds of the same sources (tools/build_variant.py); default in-tree
+LIB_PATH = os.environ.get("MSA_LIB") or os.path.join(_PKG, "libmsa.so")
 
 MSA_OK, MSA_EINVAL, MSA_ENOMEM, MSA_ECUDA, MSA_ENCCL, MSA_EDIVERGED, MSA_ESTATE = 0, -1, -2, -3, -4, -5, -6
 SHARD_NONE, SHARD_ROWS, SHARD_BATCH = 0, 1, 2

@@ -85,14 +85,13 @@ __device__ __forceinline__ void msa_dual_step(const MsaIterConsts& K, const floa
     n2 = __fmaf_rn(qx[k], qx[k], n2);
     n2 = __fmaf_rn(qy[k], qy[k], n2);
   }
-  if (n2 > K.beta2) {
-    // beta / |q| via the hardware reciprocal square root (R21: allowed since parity holds)
-    float f = __fmul_rn(K.beta, rsqrtf(n2));
+  // beta / |q| via the hardware reciprocal square root (R21: allowed since parity holds).
+  // Branch-free: inside the ball f = 1 and q * 1 = q exactly.
+  const float f = n2 > K.beta2 ? __fmul_rn(K.beta, rsqrtf(n2)) : 1.0f;
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-      qx[k] = __fmul_rn(qx[k], f);
-      qy[k] = __fmul_rn(qy[k], f);
-    }
+  for (int k = 0; k < C; ++k) {
+    qx[k] = __fmul_rn(qx[k], f);
+    qy[k] = __fmul_rn(qy[k], f);
   }
 }
 

@@ -45,12 +45,30 @@ using namespace msa_f32x2;
 
 constexpr int C = 3;
 constexpr int P = 4;       // rows per chunk
-constexpr int NW = 4;      // warps (independent sweep units) per CTA
+#ifndef MSA_SWEEP_NW
+#define MSA_SWEEP_NW 8
+#endif
+#ifndef MSA_SWEEP_OCC
+#define MSA_SWEEP_OCC 1
+#endif
+#ifndef MSA_SWEEP_NOFIN
+#define MSA_SWEEP_NOFIN 0
+#endif
+#ifndef MSA_SWEEP_STAGGER
+#define MSA_SWEEP_STAGGER 0
+#endif
+#ifndef MSA_SWEEP_LOCKSTEP
+#define MSA_SWEEP_LOCKSTEP 0
+#endif
+constexpr int NW = MSA_SWEEP_NW;  // warps (independent sweep units) per CTA
 // Box x starts are rounded down to a multiple of 4 floats (16 bytes, which the TMA unit needs):
 // smem column = global column - xa, xa = xb & ~3, so lane l reads column l + cofs (cofs = xb - xa < 4).
 constexpr int RW = 40;     // c / cbar box width: 32 lanes + up to 4 right neighbours + cofs
 constexpr int LW = 36;     // p, mu, I box width: 32 lanes + cofs
-constexpr int OCC = 2;     // CTAs per SM the register budget is sized for
+constexpr int OW = 28;     // output columns per band (a multiple of 4: the output boxes start 16-byte aligned)
+constexpr int OUT_CB = 352, OUT_P = 704;  // staged-output sub-buffers, 128-byte aligned (TMA store sources)
+static_assert(OUT_CB >= C * P * OW && OUT_P - OUT_CB >= C * P * OW && OUT_CB % 32 == 0 && OUT_P % 32 == 0, "staging");
+constexpr int OCC = MSA_SWEEP_OCC;  // CTAs per SM the register budget is sized for
 constexpr float SENT = 1e18f;
 constexpr unsigned FULL = 0xffffffffu;
 
@@ -60,11 +78,12 @@ struct __align__(128) WarpSmem {
   float p[2 * C * P * LW];     // [2C][P][LW]
   float mu[2 * C * P * LW];    // [2C][P][LW]
   float I[448];                // [C][P][LW] (432 used)
+  float out[OUT_P + 2 * C * P * OW];  // staged outputs of one chunk: c+ [C][P][OW] at 0, cbar+ at OUT_CB, p+ [2C][P][OW] at OUT_P
   unsigned long long bar[16];  // 0..3 c slots, 4 step-2/3 slot
 };
 static_assert(sizeof(WarpSmem) % 128 == 0, "warp smem must stay 128-byte aligned");
 static_assert(sizeof(float) * C * P * RW % 128 == 0, "ring slots must stay 128-byte aligned");
-static_assert(offsetof(WarpSmem, cb) % 128 == 0 && offsetof(WarpSmem, p) % 128 == 0 &&
+static_assert(offsetof(WarpSmem, out) % 128 == 0 && offsetof(WarpSmem, cb) % 128 == 0 && offsetof(WarpSmem, p) % 128 == 0 &&
                   offsetof(WarpSmem, mu) % 128 == 0 && offsetof(WarpSmem, I) % 128 == 0,
               "TMA destinations must be 128-byte aligned");
 constexpr unsigned C_BYTES = C * P * RW * 4;
@@ -94,14 +113,15 @@ struct SweepPlan {
 };
 struct SweepMaps {
   CUtensorMap c, cb, p, mu, I;
+  CUtensorMap co, cbo, po;  // outputs: owned rows only, row 0 = the slab's first owned row
 };
 
 template <int R>
 __global__ void __launch_bounds__(NW * 32, OCC)
-    k_iter_sweep_c3(MsaGeom g, MsaIterConsts K, SweepOm om, SweepPlan pl, float* __restrict__ c_out,
-                    float* __restrict__ cb_out, float* __restrict__ p_out, const __grid_constant__ SweepMaps tm) {
+    k_iter_sweep_c3(MsaGeom g, MsaIterConsts K, SweepOm om, SweepPlan pl, const __grid_constant__ SweepMaps tm) {
   constexpr int HL = R - 1;    // halo lanes = largest |dx| in the interior disc
-  constexpr int BS = 32 - HL;  // output columns per band
+  constexpr int BS = OW;       // output columns per band: lanes HL .. HL+27 (lanes past that idle for R < 5)
+  static_assert(HL + OW <= 32, "band too wide");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   WarpSmem& sm = reinterpret_cast<WarpSmem*>(smem_raw)[warp];
@@ -132,6 +152,9 @@ __global__ void __launch_bounds__(NW * 32, OCC)
   }
   __syncwarp();
   unsigned ph = 0;  // expected parity per barrier
+#if MSA_SWEEP_STAGGER
+  if (warp & 1) __nanosleep(MSA_SWEEP_STAGGER);  // A/B: odd warps start half a step late
+#endif
 
   auto load_c = [&](int q) {
     unsigned long long* bar = &sm.bar[q & 3];
@@ -213,8 +236,13 @@ __global__ void __launch_bounds__(NW * 32, OCC)
     msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
   };
 
+  // Every warp of a CTA runs the same number of steps (a shorter last segment idles through the
+  // tail) so that, with MSA_SWEEP_LOCKSTEP, a CTA barrier per step keeps the warps on the same
+  // stretch of the (long, fully unrolled) step code: they then share the instruction cache.
 #pragma unroll 1
-  for (int j = jlo - 1; j <= jhi + 1; ++j) {
+  for (int t = 0; t < pl.seg_chunks + 2; ++t) {
+    const int j = jlo - 1 + t;
+    if (j <= jhi + 1) {
     // (a) prefetch chunk j+2 into the slot chunk j-2 used (last read in the previous step)
     __syncwarp();
     if (lane == 0 && j + 2 <= jhi + 1) load_c(j + 2);
@@ -321,39 +349,64 @@ __global__ void __launch_bounds__(NW * 32, OCC)
 #undef CV
     }
 
-    // (d) finalise chunk j-1 (its sums are complete): c_half, steps 2-3, stores
+    // (d) finalise chunk j-1 (its sums are complete): c_half, steps 2-3, outputs staged in smem
+    // and written by three TMA tensor stores (clipped at the image edge and the slab's rows)
     if (j - 1 >= jlo) {
       wait_pd();
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
+      __syncwarp();
       const int q = j - 1;
       const float* cr = sm.cring[q & 3];
+      const bool st = lane >= HL && lane < HL + OW;
+      float* oc = sm.out + (lane - HL);
+      // the four rows' dual steps are independent: all first (latency overlaps), then div + prox
+      float qx[P][C], qy[P][C], qxl[P][C];
+#if MSA_SWEEP_NOFIN  // timing experiment only: wrong results
+#pragma unroll
+      for (int r = 0; r < P; ++r)
+#pragma unroll
+        for (int k = 0; k < C; ++k) { qx[r][k] = sm.p[(k * P + r) * LW + cl]; qy[r][k] = sm.mu[(k * P + r) * LW + cl]; }
+#else
+#pragma unroll
+      for (int r = 0; r < P; ++r) dual_row(r, 4 * q + r, qx[r], qy[r]);
+#endif
+#pragma unroll
+      for (int r = 0; r < P; ++r)
+#pragma unroll
+        for (int k = 0; k < C; ++k) qxl[r][k] = __shfl_up_sync(FULL, qx[r][k], 1);
 #pragma unroll
       for (int r = 0; r < P; ++r) {
         const int y = 4 * q + r;
-        float qx[C], qy[C];
-        dual_row(r, y, qx, qy);
-        const bool st = lane >= HL && x < W && y >= g.row0 && y < g.row0 + g.nrows;
-        const long long row_off = (long long)(y + so) * g.pitch + x;
 #pragma unroll
         for (int k = 0; k < C; ++k) {
-          const float qxl = __shfl_up_sync(FULL, qx[k], 1);
-          float ax = x < W - 1 ? qx[k] : 0.0f;
-          if (x > 0) ax = __fsub_rn(ax, qxl);
-          float ay = y < H - 1 ? qy[k] : 0.0f;
-          if (y > 0) ay = __fsub_rn(ay, qyp[k]);
+          float ax = x < W - 1 ? qx[r][k] : 0.0f;
+          if (x > 0) ax = __fsub_rn(ax, qxl[r][k]);
+          float ay = y < H - 1 ? qy[r][k] : 0.0f;
+          if (y > 0) ay = __fsub_rn(ay, r == 0 ? qyp[k] : qy[r - 1][k]);
           const float dv = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
           float s0, s1;
           upk(S[r >> 1][k], s0, s1);
           const float chalf = __fmaf_rn(K.dt_NR, (r & 1) ? s1 : s0, cr[(k * P + r) * RW + cl]);
           float cp, cbp;
           msa_prox_extrap(K, chalf, dv, sm.I[(k * P + r) * LW + cl], cp, cbp);
-          if (st && active) {
-            c_out[((long long)b * C + k) * g.plane + row_off] = cp;
-            cb_out[((long long)b * C + k) * g.plane + row_off] = cbp;
-            p_out[((long long)b * 2 * C + k) * g.plane + row_off] = qx[k];
-            p_out[((long long)b * 2 * C + C + k) * g.plane + row_off] = qy[k];
+          if (st) {
+            oc[(k * P + r) * OW] = cp;
+            oc[OUT_CB + (k * P + r) * OW] = cbp;
+            oc[OUT_P + (k * P + r) * OW] = qx[r][k];
+            oc[OUT_P + ((C + k) * P + r) * OW] = qy[r][k];
           }
-          qyp[k] = qy[k];
         }
+      }
+#pragma unroll
+      for (int k = 0; k < C; ++k) qyp[k] = qy[P - 1][k];
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic smem writes -> async proxy
+      __syncwarp();
+      if (lane == 0 && active) {
+        const int xo = band * BS, yo = 4 * q - g.row0;
+        tma_store3(&tm.co, xo, yo, b * C, sm.out);
+        tma_store3(&tm.cbo, xo, yo, b * C, sm.out + OUT_CB);
+        tma_store3(&tm.po, xo, yo, b * 2 * C, sm.out + OUT_P);
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
     } else if (j == jlo - 1 && prow) {  // halo step: p+_y of row 4 jlo - 1 only
       wait_pd();
@@ -374,13 +427,19 @@ __global__ void __launch_bounds__(NW * 32, OCC)
     for (int i = 4; i < 6; ++i)
 #pragma unroll
       for (int k = 0; k < C; ++k) S[i][k] = pk(0.0f, 0.0f);
+    }
+#if MSA_SWEEP_LOCKSTEP
+    __syncthreads();
+#endif
   }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem must outlive the reads
 }
 
 // ---------------- host side
 
 struct SweepKey {
   const float *c, *cb, *p, *mu, *I;
+  float *co, *cbo, *po;
   int W, rows, nb, pitch, R;
   long long plane;
   bool operator==(const SweepKey& o) const { return memcmp(this, &o, sizeof(SweepKey)) == 0; }
@@ -400,7 +459,8 @@ bool get_maps(const SweepKey& k, const MsaGeom& g, SweepMaps* out) {
   SweepMaps t;
   if (!encode_map(&t.c, g, k.c, C, RW, P) || !encode_map(&t.cb, g, k.cb, C, RW, P + 1) ||
       !encode_map(&t.p, g, k.p, 2 * C, LW, P) || !encode_map(&t.mu, g, k.mu, 2 * C, LW, P) ||
-      !encode_map(&t.I, g, k.I, C, LW, P))
+      !encode_map(&t.I, g, k.I, C, LW, P) || !encode_owned_map(&t.co, g, k.co, C, OW, P) ||
+      !encode_owned_map(&t.cbo, g, k.cbo, C, OW, P) || !encode_owned_map(&t.po, g, k.po, 2 * C, OW, P))
     return false;
   const int slot = n < 16 ? n++ : (next++ % 16);
   keys[slot] = k;
@@ -443,7 +503,7 @@ cudaError_t launch_r(const MsaGeom& g, const MsaIterConsts& K, const SweepOm& om
                      cudaStream_t s) {
   SweepKey key;
   memset(&key, 0, sizeof(key));
-  key.c = c; key.cb = cb; key.p = p; key.mu = mu; key.I = I;
+  key.c = c; key.cb = cb; key.p = p; key.mu = mu; key.I = I; key.co = co; key.cbo = cbo; key.po = po;
   key.W = g.W; key.rows = g.nrows + 2 * g.G; key.nb = g.nb; key.pitch = g.pitch; key.R = R;
   key.plane = g.plane;
   SweepMaps tm;
@@ -460,9 +520,9 @@ cudaError_t launch_r(const MsaGeom& g, const MsaIterConsts& K, const SweepOm& om
     if (e != cudaSuccess) return e;
     slots = std::max(1, nsm * per_sm * NW);
   }
-  const SweepPlan pl = make_plan(g, 32 - (R - 1), slots);
+  const SweepPlan pl = make_plan(g, OW, slots);
   const int grid = (pl.units + NW - 1) / NW;
-  k_iter_sweep_c3<R><<<grid, NW * 32, smem, s>>>(g, K, om, pl, co, cbo, po, tm);
+  k_iter_sweep_c3<R><<<grid, NW * 32, smem, s>>>(g, K, om, pl, tm);
   return cudaGetLastError();
 }
 

@@ -78,4 +78,18 @@ inline bool encode_map(CUtensorMap* m, const MsaGeom& g, const float* base, int 
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Output map whose row 0 is the slab's first owned row (stored row G) and which spans exactly the
+// owned rows: stores to rows outside the slab (ghost rows, rows past the image) are clipped.
+inline bool encode_owned_map(CUtensorMap* m, const MsaGeom& g, float* field, int nm, int bw, int bh) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.W, (cuuint64_t)g.nrows, (cuuint64_t)g.nb * nm};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.pitch * 4, (cuuint64_t)g.plane * 4};
+  const cuuint32_t box[3] = {(cuuint32_t)bw, (cuuint32_t)bh, (cuuint32_t)nm};
+  const cuuint32_t es[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)(field + (size_t)g.G * g.pitch), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace msa_tma
