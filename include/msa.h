@@ -167,8 +167,13 @@ int msa_solve(msa_ctx* ctx, msa_round_stats* stats);
  *  (ii) union segments whose means differ by <= delta in every channel (means from exact
  *       64-bit fixed-point sums, m = (double)sum llrint(c 2^32) / count * 2^-32);
  *  (iii) label = rank of the cluster's smallest member index j*W + i; palette = cluster mean.
- * labels: int32 [nimages][H][W] of this rank's images (rows mode: world must be 1 in this
- * ABI version); n_clusters: int32 [nimages]; palette: float32 [nimages][max_k][C] or NULL.
+ * labels: int32 [nimages][rows][W] of this rank's images, rows = H, or this rank's slab rows in
+ * rows mode; n_clusters: int32 [nimages]; palette: float32 [nimages][max_k][C] or NULL.
+ * Rows mode with world > 1: every rank runs stage (i) on its slab (the row above
+ * is refreshed by a halo exchange first), the slabs' segment tables and boundary rows meet by
+ * ncclAllGather, every rank runs the same merge (cross-slab edges, exact integer sums, stages
+ * (ii)-(iii)), so ids, counts and palettes are global and equal on all ranks and match the
+ * single-GPU rule bit for bit. Collective: all ranks must call it.
  * All three are host pointers unless out_on_device. Synchronises. */
 int msa_labels(msa_ctx* ctx, float delta, int32_t* labels, int32_t* n_clusters, float* palette, int32_t max_k,
                int out_on_device);

@@ -286,9 +286,10 @@ class Solver:
         return [buf[r].as_dict(self.params.channels) for r in range(self.params.rounds)]
 
     def labels(self, delta: float = 0.1, max_k: int = 0, out=None):
-        """Returns (labels int32 [nb][H][W], n_clusters int32 [nb], palette [nb][max_k][C] or None)."""
+        """Returns (labels int32 [nb][rows][W], n_clusters int32 [nb], palette [nb][max_k][C] or None);
+        rows = this rank's slab rows in rows mode, else H. Cluster ids and palettes are global."""
         info = self.query()
-        nb, H, W, C = info.nimages, self.params.height, self.params.width, self.params.channels
+        nb, H, W, C = info.nimages, info.nrows, self.params.width, self.params.channels
         if out is None:
             lab = np.empty((nb, H, W), dtype=np.int32)
             cnt = np.empty(nb, dtype=np.int32)

@@ -43,6 +43,7 @@ struct NcclApi {
   ncclResult_t (*GroupEnd)() = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
@@ -63,10 +64,12 @@ bool nccl_load() {
   LOADSYM(GroupStart, "ncclGroupStart");
   LOADSYM(GroupEnd, "ncclGroupEnd");
   LOADSYM(AllReduce, "ncclAllReduce");
+  LOADSYM(AllGather, "ncclAllGather");
   LOADSYM(GetErrorString, "ncclGetErrorString");
 #undef LOADSYM
   g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.Send && g_nccl.Recv &&
-              g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.AllReduce && g_nccl.GetErrorString;
+              g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.AllReduce && g_nccl.AllGather &&
+              g_nccl.GetErrorString;
   return g_nccl.ok;
 }
 #define NCCL_TRY(x)                                                                                            \
@@ -720,16 +723,153 @@ int msa_solve(msa_ctx* x, msa_round_stats* stats) {
   return MSA_OK;
 }
 
+// Q(c; delta) of image b over row parts: stage (i) per part, the parts' segment
+// tables concatenated in row order, one merge (identical on every rank), relabel of own pixels.
+//  * rows mode, world > 1: the part is this rank's slab; tables meet by ncclAllGather (padded to
+//    the largest table); labels_dev receives this rank's rows.
+//  * otherwise nparts virtual parts of the whole image on this GPU (test hook MSA_LABELS_PARTS):
+//    the result must equal the single-pass rule bit for bit.
+int labels_parts(msa_ctx* x, int b, float delta, int nparts, int32_t* labels_dev, int32_t* count_dev, float* pal_dev,
+                 int max_k) {
+  const MsaGeom& g = x->g;
+  const int W = g.W, C = g.C;
+  const bool dist = x->prm.world > 1 && x->prm.shard == MSA_SHARD_ROWS;
+  cudaStream_t st = x->stream;
+  long long launches = 0;
+  std::vector<int> r0(nparts), nr(nparts), S(nparts), off(nparts + 1, 0);
+  if (dist) {
+    if (!g_nccl.AllGather) return set_err(MSA_ENCCL, "ncclAllGather not available");
+    for (int p = 0; p < nparts; ++p) {
+      msa_params q = x->prm;
+      q.rank = p;
+      const Part pt = partition(&q);
+      r0[p] = pt.row0;
+      nr[p] = pt.nrows;
+    }
+  } else {
+    for (int p = 0; p < nparts; ++p) {
+      r0[p] = (int)((long long)g.H * p / nparts);
+      nr[p] = (int)((long long)g.H * (p + 1) / nparts) - r0[p];
+    }
+  }
+  const size_t npix = dist ? (size_t)g.nrows * W : (size_t)g.H * W;  // pixels this GPU labels
+  const size_t cap_tab = dist ? (size_t)x->prm.height * W : npix;     // concatenated segments <= pixels
+  int32_t *roots = nullptr, *bounds = nullptr, *cl = nullptr, *sop = nullptr, *nseg = nullptr;
+  unsigned long long *cnt = nullptr, *sum = nullptr;
+  auto cleanup = [&]() {
+    void* ps[] = {roots, bounds, cl, sop, nseg, cnt, sum};
+    for (void* q : ps)
+      if (q) cudaFreeAsync(q, st);
+  };
+#define LB_TRY(expr)                                                                        \
+  do {                                                                                      \
+    cudaError_t e_ = (expr);                                                                \
+    if (e_ != cudaSuccess) {                                                                \
+      cleanup();                                                                            \
+      return set_err(MSA_ECUDA, "labels (parts): %s: %s", #expr, cudaGetErrorString(e_));   \
+    }                                                                                       \
+  } while (0)
+  LB_TRY(cudaMallocAsync((void**)&roots, sizeof(int32_t) * (cap_tab + 1), st));
+  LB_TRY(cudaMallocAsync((void**)&cl, sizeof(int32_t) * (cap_tab + 1), st));
+  LB_TRY(cudaMallocAsync((void**)&cnt, sizeof(unsigned long long) * (cap_tab + 1), st));
+  LB_TRY(cudaMallocAsync((void**)&sum, sizeof(unsigned long long) * (cap_tab + 1) * C, st));
+  LB_TRY(cudaMallocAsync((void**)&bounds, sizeof(int32_t) * 3 * W * nparts, st));
+  LB_TRY(cudaMallocAsync((void**)&sop, sizeof(int32_t) * (npix + 1), st));
+  LB_TRY(cudaMallocAsync((void**)&nseg, sizeof(int32_t) * nparts, st));
+  if (!dist) {
+    for (int p = 0; p < nparts; ++p) {
+      MsaLabelPart part;
+      part.seg_of_pix = sop + (size_t)r0[p] * W;
+      part.roots = roots + off[p];
+      part.cnt = cnt + off[p];
+      part.sum = sum + (size_t)off[p] * C;
+      part.bounds = bounds + (size_t)p * 3 * W;
+      part.nseg = nseg + p;
+      LB_TRY(msa_labels_part(g, x->c[x->cur], b, r0[p], nr[p], delta, part, &x->lab, st, &launches));
+      LB_TRY(cudaMemcpyAsync(&S[p], nseg + p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      LB_TRY(cudaStreamSynchronize(st));
+      off[p + 1] = off[p] + S[p];
+    }
+  } else {
+    // own slab into the slots of the largest possible table, then gather counts, tables, bounds
+    const int me = x->prm.rank;
+    const size_t own = (size_t)g.nrows * W;
+    int32_t *o_roots = nullptr, *o_bounds = nullptr, *o_n = nullptr, *g_roots = nullptr, *g_n = nullptr;
+    unsigned long long *o_cnt = nullptr, *o_sum = nullptr, *g_cnt = nullptr, *g_sum = nullptr;
+    LB_TRY(cudaMallocAsync((void**)&o_roots, sizeof(int32_t) * (own + 1), st));
+    LB_TRY(cudaMallocAsync((void**)&o_cnt, sizeof(unsigned long long) * (own + 1), st));
+    LB_TRY(cudaMallocAsync((void**)&o_sum, sizeof(unsigned long long) * (own + 1) * C, st));
+    LB_TRY(cudaMallocAsync((void**)&o_bounds, sizeof(int32_t) * 3 * W, st));
+    LB_TRY(cudaMallocAsync((void**)&o_n, sizeof(int32_t), st));
+    MsaLabelPart part{sop, o_roots, o_cnt, o_sum, o_bounds, o_n};
+    LB_TRY(msa_labels_part(g, x->c[x->cur], b, g.row0, g.nrows, delta, part, &x->lab, st, &launches));
+    LB_TRY(cudaMallocAsync((void**)&g_n, sizeof(int32_t) * nparts, st));
+    NCCL_TRY(g_nccl.AllGather(o_n, g_n, 1, ncclInt32, x->comm, st));
+    NCCL_TRY(g_nccl.AllGather(o_bounds, bounds, 3 * (size_t)W, ncclInt32, x->comm, st));
+    LB_TRY(cudaMemcpyAsync(S.data(), g_n, sizeof(int32_t) * nparts, cudaMemcpyDeviceToHost, st));
+    LB_TRY(cudaStreamSynchronize(st));
+    int maxS = 1;
+    for (int p = 0; p < nparts; ++p) {
+      off[p + 1] = off[p] + S[p];
+      maxS = std::max(maxS, S[p]);
+    }
+    // padded tables: own table copied into a maxS-slot send buffer (own capacity may be smaller)
+    int32_t* s_roots = nullptr;
+    unsigned long long *s_cnt = nullptr, *s_sum = nullptr;
+    LB_TRY(cudaMallocAsync((void**)&s_roots, sizeof(int32_t) * maxS, st));
+    LB_TRY(cudaMallocAsync((void**)&s_cnt, sizeof(unsigned long long) * maxS, st));
+    LB_TRY(cudaMallocAsync((void**)&s_sum, sizeof(unsigned long long) * maxS * C, st));
+    LB_TRY(cudaMemcpyAsync(s_roots, o_roots, sizeof(int32_t) * S[me], cudaMemcpyDeviceToDevice, st));
+    LB_TRY(cudaMemcpyAsync(s_cnt, o_cnt, sizeof(unsigned long long) * S[me], cudaMemcpyDeviceToDevice, st));
+    LB_TRY(cudaMemcpyAsync(s_sum, o_sum, sizeof(unsigned long long) * S[me] * C, cudaMemcpyDeviceToDevice, st));
+    LB_TRY(cudaMallocAsync((void**)&g_roots, sizeof(int32_t) * (size_t)maxS * nparts, st));
+    LB_TRY(cudaMallocAsync((void**)&g_cnt, sizeof(unsigned long long) * (size_t)maxS * nparts, st));
+    LB_TRY(cudaMallocAsync((void**)&g_sum, sizeof(unsigned long long) * (size_t)maxS * C * nparts, st));
+    NCCL_TRY(g_nccl.GroupStart());
+    NCCL_TRY(g_nccl.AllGather(s_roots, g_roots, maxS, ncclInt32, x->comm, st));
+    NCCL_TRY(g_nccl.AllGather(s_cnt, g_cnt, maxS, ncclUint64, x->comm, st));
+    NCCL_TRY(g_nccl.AllGather(s_sum, g_sum, (size_t)maxS * C, ncclUint64, x->comm, st));
+    NCCL_TRY(g_nccl.GroupEnd());
+    for (int p = 0; p < nparts; ++p) {  // compact in rank (= row) order
+      LB_TRY(cudaMemcpyAsync(roots + off[p], g_roots + (size_t)p * maxS, sizeof(int32_t) * S[p],
+                             cudaMemcpyDeviceToDevice, st));
+      LB_TRY(cudaMemcpyAsync(cnt + off[p], g_cnt + (size_t)p * maxS, sizeof(unsigned long long) * S[p],
+                             cudaMemcpyDeviceToDevice, st));
+      LB_TRY(cudaMemcpyAsync(sum + (size_t)off[p] * C, g_sum + (size_t)p * maxS * C,
+                             sizeof(unsigned long long) * S[p] * C, cudaMemcpyDeviceToDevice, st));
+    }
+    void* tmp[] = {o_roots, o_cnt, o_sum, o_bounds, o_n, g_n, s_roots, s_cnt, s_sum, g_roots, g_cnt, g_sum};
+    for (void* q : tmp) cudaFreeAsync(q, st);
+  }
+  LB_TRY(msa_labels_merge(nparts, off[nparts], W, C, roots, cnt, sum, bounds, delta, cl, count_dev, pal_dev, max_k,
+                          &x->lab, st, &launches));
+  if (dist) {
+    LB_TRY(msa_labels_relabel((int)npix, sop, off[x->prm.rank], cl, labels_dev, st));
+  } else {
+    for (int p = 0; p < nparts; ++p)
+      LB_TRY(msa_labels_relabel(nr[p] * W, sop + (size_t)r0[p] * W, off[p], cl, labels_dev + (size_t)r0[p] * W, st));
+  }
+  x->launches += launches + (dist ? 1 : nparts);
+  cleanup();
+#undef LB_TRY
+  return MSA_OK;
+}
+
 int msa_labels(msa_ctx* x, float delta, int32_t* labels, int32_t* n_clusters, float* palette, int32_t max_k,
                int out_on_device) {
   if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
   if (!(delta >= 0) || !isfinite(delta)) return set_err(MSA_EINVAL, "delta must be finite and >= 0");
   if (!labels || !n_clusters) return set_err(MSA_EINVAL, "labels and n_clusters must not be NULL");
   if (max_k < 0 || (max_k > 0 && !palette)) return set_err(MSA_EINVAL, "palette needs max_k > 0 and a buffer");
-  if (x->prm.world > 1 && x->prm.shard == MSA_SHARD_ROWS)
-    return set_err(MSA_EINVAL, "labels need the whole image on one rank (rows mode with world > 1 unsupported)");
+  const bool dist = x->prm.world > 1 && x->prm.shard == MSA_SHARD_ROWS;
+  static const int test_parts = getenv("MSA_LABELS_PARTS") ? atoi(getenv("MSA_LABELS_PARTS")) : 0;  // test hook
   const MsaGeom& g = x->g;
-  const size_t N = (size_t)g.H * g.W;
+  const int nparts = dist ? x->prm.world : std::min(test_parts, g.H);
+  if (dist) {  // stage (i) across the slab boundary needs the current c row above each slab
+    int rc = halo_exchange(x, MSA_HALO_ROUND);
+    if (rc != MSA_OK) return rc;
+  }
+  const size_t N = (size_t)g.nrows * g.W;  // this rank's pixels per image
   const int C = g.C;
   if (!out_on_device && !x->lab_buf) CUDA_TRY(cudaMalloc((void**)&x->lab_buf, N * sizeof(int32_t)));
   if (!x->lab_count) CUDA_TRY(cudaMalloc((void**)&x->lab_count, sizeof(int32_t) * 2));
@@ -743,9 +883,14 @@ int msa_labels(msa_ctx* x, float delta, int32_t* labels, int32_t* n_clusters, fl
     int32_t* cdev = out_on_device ? n_clusters + b : x->lab_count;
     float* pdev = max_k > 0 ? (out_on_device ? palette + (size_t)b * max_k * C : x->lab_pal) : nullptr;
     long long launches = 0;
-    cudaError_t e = msa_labels_image(g, x->c[x->cur], b, delta, ldev, cdev, pdev, max_k, &x->lab, x->stream, &launches);
-    x->launches += launches;
-    if (e != cudaSuccess) return set_err(MSA_ECUDA, "labels: %s", cudaGetErrorString(e));
+    if (nparts >= 2) {
+      int rc = labels_parts(x, b, delta, nparts, ldev, cdev, pdev, max_k);
+      if (rc != MSA_OK) return rc;
+    } else {
+      cudaError_t e = msa_labels_image(g, x->c[x->cur], b, delta, ldev, cdev, pdev, max_k, &x->lab, x->stream, &launches);
+      x->launches += launches;
+      if (e != cudaSuccess) return set_err(MSA_ECUDA, "labels: %s", cudaGetErrorString(e));
+    }
     if (!out_on_device) {
       CUDA_TRY(cudaMemcpyAsync(labels + N * b, ldev, N * sizeof(int32_t), cudaMemcpyDeviceToHost, x->stream));
       CUDA_TRY(cudaMemcpyAsync(n_clusters + b, cdev, sizeof(int32_t), cudaMemcpyDeviceToHost, x->stream));

@@ -56,3 +56,26 @@ cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delt
                              int32_t* count_dev, float* palette_dev, int max_k, MsaLabelScratch** scratch,
                              cudaStream_t s, long long* launches);
 void msa_labels_free(MsaLabelScratch* s);
+
+// Labels over row slabs (rows mode): stage (i) of Q on rows [r0, r0 + nr) of one
+// image (the slab, or a virtual part on one GPU), then a merge of all parts' tables that every
+// rank runs identically, then each rank relabels its own pixels. The merge reproduces the
+// whole-image rule exactly (same segments, exact integer sums, same orders).
+struct MsaLabelPart {             // device buffers, capacity nr * W segments / pixels
+  int32_t* seg_of_pix;            // [nr*W] segment index (in the part's root order) of each pixel
+  int32_t* roots;                 // [S] global pixel index of each segment's smallest member
+  unsigned long long* cnt;        // [S]
+  unsigned long long* sum;        // [S][C] round(c 2^32) sums
+  int32_t* bounds;                // [3][W] roots of the first / last row, joined-to-the-row-above flags
+  int32_t* nseg;                  // [1] S
+};
+cudaError_t msa_labels_part(const MsaGeom& g, const float* c, int b, int r0, int nr, float delta,
+                            const MsaLabelPart& out, MsaLabelScratch** scratch, cudaStream_t st, long long* launches);
+// tables of nparts parts concatenated in part (row) order, bounds [nparts][3][W]; writes the
+// cluster rank of every concatenated segment, the count and the palette
+cudaError_t msa_labels_merge(int nparts, int S_total, int W, int C, const int32_t* roots, const unsigned long long* cnt,
+                             const unsigned long long* sum, const int32_t* bounds, float delta, int32_t* cl_of_seg,
+                             int32_t* count_dev, float* palette_dev, int max_k, MsaLabelScratch** scratch,
+                             cudaStream_t st, long long* launches);
+cudaError_t msa_labels_relabel(int npix, const int32_t* seg_of_pix, int seg_off, const int32_t* cl_of_seg,
+                               int32_t* labels, cudaStream_t st);

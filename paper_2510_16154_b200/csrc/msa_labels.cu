@@ -36,6 +36,7 @@ struct MsaLabelScratch {
   int32_t* scalars = nullptr;             // [4] S, K, cell_lo, cell_hi (as int bits)
   double* dscal = nullptr;                // [6] min/max of the hashed channel means
   void* grid = nullptr;                   // CellGrid (device)
+  int32_t* merge_idx = nullptr;           // [N] slab merge: merged index of every concatenated segment
 };
 
 namespace {
@@ -82,13 +83,14 @@ __global__ void k_iota(int32_t* P, int n) {
   if (x < n) P[x] = x;
 }
 
-// stage (i): 4-neighbour edges (right, up)
-__global__ void k_edges(MsaGeom g, const float* __restrict__ c, int b, float delta, int32_t* P) {
+// stage (i): 4-neighbour edges (right, up) among rows [r0, r0 + nr) (local index (j - r0) W + i)
+__global__ void k_edges(MsaGeom g, const float* __restrict__ c, int b, int r0, int nr, float delta, int32_t* P) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  if (i >= g.W || j >= g.H) return;
-  const int n = j * g.W + i;
-  bool right = i + 1 < g.W, up = j + 1 < g.H;
+  const int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  if (i >= g.W || jl >= nr) return;
+  const int j = r0 + jl;
+  const int n = jl * g.W + i;
+  bool right = i + 1 < g.W, up = jl + 1 < nr;
   for (int k = 0; k < g.C; ++k) {
     const float a = c[msa_idx(g, b, k, g.C, j, i)];
     if (right && !(fabsf(__fsub_rn(a, c[msa_idx(g, b, k, g.C, j, i + 1)])) <= delta)) right = false;
@@ -154,14 +156,16 @@ __global__ void k_scan_add(int32_t* a, int n, const int32_t* off) {
 }
 
 // ---- segments
-__global__ void k_seg_accum(MsaGeom g, const float* __restrict__ c, int b, const int32_t* __restrict__ P,
-                            const int32_t* __restrict__ segidx, unsigned long long* sum, unsigned long long* cnt) {
+__global__ void k_seg_accum(MsaGeom g, const float* __restrict__ c, int b, int r0, int nr,
+                            const int32_t* __restrict__ P, const int32_t* __restrict__ segidx, unsigned long long* sum,
+                            unsigned long long* cnt) {
   // Exact 64-bit fixed-point sums. A warp of 32 consecutive pixels usually lies in one segment:
   // then it reduces with shuffles and issues one atomic per value (integer sums: exact, order free).
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int j = blockIdx.y * blockDim.y + threadIdx.y;
-  const bool valid = i < g.W && j < g.H;
-  const int s = valid ? segidx[P[j * g.W + i]] : -1;
+  const int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  const int j = r0 + jl;
+  const bool valid = i < g.W && jl < nr;
+  const int s = valid ? segidx[P[jl * g.W + i]] : -1;
   const unsigned same = __match_any_sync(0xffffffffu, s);
   if (same == 0xffffffffu) {
     if (s < 0) return;
@@ -384,6 +388,86 @@ __global__ void k_palette(const int32_t* __restrict__ scal, int C, const unsigne
     palette[(size_t)l * C + k] = (float)((double)(long long)csum[(size_t)l * C + k] / (double)ccnt[l] * 0x1.0p-32);
 }
 
+
+// ---- slabs (rows mode): stage (i) per part, tables merged identically on every rank
+
+// segment table of a part: root (global pixel index) per segment, segment index per pixel
+__global__ void k_part_tables(int np, int base, const int32_t* __restrict__ P, const int32_t* __restrict__ segidx,
+                              const int32_t* __restrict__ is_root, int32_t* roots, int32_t* seg_of_pix) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= np) return;
+  const int s = segidx[P[n]];
+  seg_of_pix[n] = s;
+  if (is_root[n]) roots[s] = base + n;
+}
+
+// boundary rows of a part: roots of its first and last row, and whether each pixel of the last
+// row is stage-(i) joined to the pixel above it (the next part's first row)
+__global__ void k_part_bounds(MsaGeom g, const float* __restrict__ c, int b, int r0, int nr, float delta,
+                              const int32_t* __restrict__ P, int32_t* bounds) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= g.W) return;
+  const int W = g.W, top = r0 + nr - 1;
+  bounds[i] = r0 * W + P[i];
+  bounds[W + i] = r0 * W + P[(nr - 1) * W + i];
+  bool up = top + 1 < g.H;
+  for (int k = 0; up && k < g.C; ++k)
+    if (!(fabsf(__fsub_rn(c[msa_idx(g, b, k, g.C, top, i)], c[msa_idx(g, b, k, g.C, top + 1, i)])) <= delta))
+      up = false;
+  bounds[2 * W + i] = up ? 1 : 0;
+}
+
+__device__ __forceinline__ int find_root_index(const int32_t* __restrict__ roots, int n, int key) {
+  int lo = 0, hi = n - 1;  // roots ascending; key is present
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (roots[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+// stage (i) across part boundaries: unite the segments of vertically joined boundary pixels
+__global__ void k_cross_edges(int nparts, int W, const int32_t* __restrict__ bounds, const int32_t* __restrict__ roots,
+                              const int32_t* __restrict__ scal, int32_t* mP) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (nparts - 1) * W) return;
+  const int p = t / W, i = t % W;
+  const int32_t* lo = bounds + (size_t)p * 3 * W;
+  const int32_t* hi = bounds + (size_t)(p + 1) * 3 * W;
+  if (!lo[2 * W + i]) return;
+  const int n = scal[2];
+  uf_unite(mP, find_root_index(roots, n, lo[W + i]), find_root_index(roots, n, hi[i]));
+}
+
+__global__ void k_iota_n(const int32_t* __restrict__ scal, int32_t* P) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x < scal[2]) P[x] = x;
+}
+
+__global__ void k_merged_index(const int32_t* __restrict__ scal, const int32_t* __restrict__ mP,
+                               const int32_t* __restrict__ midx, int32_t* m_of_seg) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < scal[2]) m_of_seg[s] = midx[mP[s]];
+}
+
+__global__ void k_cluster_of_seg(const int32_t* __restrict__ scal, const int32_t* __restrict__ m_of_seg,
+                                 const int32_t* __restrict__ segP, const int32_t* __restrict__ rank,
+                                 int32_t* cl_of_seg) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < scal[2]) cl_of_seg[s] = rank[segP[m_of_seg[s]]];
+}
+
+__global__ void k_relabel(int np, const int32_t* __restrict__ seg_of_pix, int off, const int32_t* __restrict__ cl_of_seg,
+                          int32_t* labels) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n < np) labels[n] = cl_of_seg[off + seg_of_pix[n]];
+}
+
+__global__ void k_set_scalar(int32_t* scal, int idx, int v) {
+  if (threadIdx.x == 0) scal[idx] = v;
+}
+
 // exclusive scan of `flags` -> `out` (may alias), returns total in *total_dev
 cudaError_t scan_excl(int32_t* a, int n, int32_t* tmp, size_t tmp_n, cudaStream_t s, long long* launches) {
   if (n <= 0) return cudaSuccess;
@@ -407,54 +491,35 @@ cudaError_t grow(T** p, size_t n) {
   return cudaMalloc((void**)p, n * sizeof(T) + 16);
 }
 
-}  // namespace
 
-void msa_labels_free(MsaLabelScratch* s) {
-  if (!s) return;
-  void* ptrs[] = {s->parent, s->flag, s->scan_tmp, s->seg_parent, s->seg_flag, s->flag_copy, s->seg_sum, s->seg_cnt,
-                  s->seg_mean, s->cell_count, s->cell_fill, s->sorted, s->seg_cell, s->cl_sum, s->cl_cnt,
-                  s->scalars, s->dscal, s->grid};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
-  delete s;
-}
-
-cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delta, int32_t* labels_dev,
-                             int32_t* count_dev, float* palette_dev, int max_k, MsaLabelScratch** scratch,
-                             cudaStream_t st, long long* launches) {
-  const int N = g.H * g.W, C = g.C;
+cudaError_t ensure_scratch(MsaLabelScratch** scratch, size_t n, int C) {
   MsaLabelScratch* S = *scratch;
   if (!S) S = *scratch = new MsaLabelScratch();
   cudaError_t e = cudaSuccess;
-  if (S->cap_px < (size_t)N || S->C != C) {
-    const size_t n = (size_t)N;
+  if (S->cap_px < n || S->C != C) {
     S->scan_tmp_n = 2 * ((n + 1023) / 1024) + 2 * ((NCELL_MAX + 1 + 1023) / 1024) + 64;
     if ((e = grow(&S->parent, n)) || (e = grow(&S->flag, n)) || (e = grow(&S->scan_tmp, S->scan_tmp_n)) ||
-        (e = grow(&S->seg_parent, n)) || (e = grow(&S->seg_flag, n)) || (e = grow(&S->flag_copy, n)) || (e = grow(&S->seg_sum, n * C)) ||
-        (e = grow(&S->seg_cnt, n)) || (e = grow(&S->seg_mean, n * C)) ||
+        (e = grow(&S->seg_parent, n)) || (e = grow(&S->seg_flag, n)) || (e = grow(&S->flag_copy, n)) ||
+        (e = grow(&S->seg_sum, n * C)) || (e = grow(&S->seg_cnt, n)) || (e = grow(&S->seg_mean, n * C)) ||
         (e = grow(&S->cell_count, (size_t)NCELL_MAX + 1)) || (e = grow(&S->cell_fill, (size_t)NCELL_MAX)) ||
         (e = grow(&S->sorted, n)) || (e = grow(&S->seg_cell, n)) || (e = grow(&S->cl_sum, n * C)) ||
-        (e = grow(&S->cl_cnt, n)) || (e = grow(&S->scalars, 4)) || (e = grow(&S->dscal, 6)) || (e = cudaMalloc(&S->grid, 256)))
+        (e = grow(&S->cl_cnt, n)) || (e = grow(&S->scalars, 4)) || (e = grow(&S->dscal, 6)) ||
+        (e = grow(&S->merge_idx, n)) ||
+        (S->grid == nullptr && (e = cudaMalloc(&S->grid, 256))))
       return e;
     S->cap_px = n;
     S->C = C;
   }
-  const int T = 256, nbN = (N + T - 1) / T;
-  dim3 blk(32, 8), grd((g.W + 31) / 32, (g.H + 7) / 8);
-  // (i) segments
-  k_iota<<<nbN, T, 0, st>>>(S->parent, N);
-  k_edges<<<grd, blk, 0, st>>>(g, c, b, delta, S->parent);
-  k_compress_flag<<<nbN, T, 0, st>>>(S->parent, S->flag, N);
-  *launches += 3;
-  // flag -> exclusive scan gives the segment index of each root; total S -> scalars[0]
-  cudaMemcpyAsync(S->flag_copy, S->flag, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st);  // keep flags
-  if ((e = scan_excl(S->flag, N, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
-  k_totals<<<1, 32, 0, st>>>(nullptr, N, S->flag, S->flag_copy, S->scalars + 0);
-  ++*launches;
-  cudaMemsetAsync(S->seg_sum, 0, sizeof(unsigned long long) * (size_t)N * C, st);
-  cudaMemsetAsync(S->seg_cnt, 0, sizeof(unsigned long long) * (size_t)N, st);
-  k_seg_accum<<<grd, blk, 0, st>>>(g, c, b, S->parent, S->flag, S->seg_sum, S->seg_cnt);
-  ++*launches;
+  return cudaSuccess;
+}
+
+// Stages (ii)-(iii) on the segment table in S->seg_sum / S->seg_cnt: S->scalars[0] segments in
+// smallest-member order, n >= that count (sizes the launches). Afterwards the cluster rank of
+// segment s is S->seg_flag[S->seg_parent[s]], the count is in S->scalars[1] and *count_dev.
+cudaError_t stage23(int n, int C, float delta, int32_t* count_dev, float* palette_dev, int max_k, MsaLabelScratch* S,
+                    cudaStream_t st, long long* launches) {
+  const int T = 256, nbN = (n + T - 1) / T;
+  cudaError_t e;
   // (ii) segment means, channel-0 cells, candidate pairs
   const double init_mm[6] = {INFINITY, -INFINITY, INFINITY, -INFINITY, INFINITY, -INFINITY};
   cudaMemcpyAsync(S->dscal, init_mm, sizeof(init_mm), cudaMemcpyHostToDevice, st);
@@ -473,18 +538,58 @@ cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delt
   *launches += 3;
   // (iii) cluster ranks = exclusive scan of cluster-root flags over segments (segment order =
   // smallest-member order), count, labels, palette
-  cudaMemcpyAsync(S->flag_copy, S->seg_flag, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st);  // flags copy
-  if ((e = scan_excl(S->seg_flag, N, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
-  k_totals<<<1, 32, 0, st>>>(S->scalars + 0, N, S->seg_flag, S->flag_copy, S->scalars + 1);
-  k_write_labels<<<nbN, T, 0, st>>>(N, S->parent, S->flag, S->seg_parent, S->seg_flag, labels_dev);
-  *launches += 2;
-  cudaMemsetAsync(S->cl_sum, 0, sizeof(unsigned long long) * (size_t)N * C, st);
-  cudaMemsetAsync(S->cl_cnt, 0, sizeof(unsigned long long) * (size_t)N, st);
+  cudaMemcpyAsync(S->flag_copy, S->seg_flag, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st);  // flags copy
+  if ((e = scan_excl(S->seg_flag, n, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
+  k_totals<<<1, 32, 0, st>>>(S->scalars + 0, n, S->seg_flag, S->flag_copy, S->scalars + 1);
+  *launches += 1;
+  cudaMemsetAsync(S->cl_sum, 0, sizeof(unsigned long long) * (size_t)n * C, st);
+  cudaMemsetAsync(S->cl_cnt, 0, sizeof(unsigned long long) * (size_t)n, st);
   k_cluster_sums<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_parent, S->seg_flag, S->seg_sum, S->seg_cnt, S->cl_sum,
                                     S->cl_cnt);
   const int npal = max_k > 0 ? max_k : 1;
   k_palette<<<(npal + T - 1) / T, T, 0, st>>>(S->scalars, C, S->cl_sum, S->cl_cnt, palette_dev, max_k, count_dev);
   *launches += 2;
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+void msa_labels_free(MsaLabelScratch* s) {
+  if (!s) return;
+  void* ptrs[] = {s->parent, s->flag, s->scan_tmp, s->seg_parent, s->seg_flag, s->flag_copy, s->seg_sum, s->seg_cnt,
+                  s->seg_mean, s->cell_count, s->cell_fill, s->sorted, s->seg_cell, s->cl_sum, s->cl_cnt,
+                  s->scalars, s->dscal, s->grid, s->merge_idx};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete s;
+}
+
+cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delta, int32_t* labels_dev,
+                             int32_t* count_dev, float* palette_dev, int max_k, MsaLabelScratch** scratch,
+                             cudaStream_t st, long long* launches) {
+  const int N = g.H * g.W, C = g.C;
+  cudaError_t e = ensure_scratch(scratch, (size_t)N, C);
+  if (e != cudaSuccess) return e;
+  MsaLabelScratch* S = *scratch;
+  const int T = 256, nbN = (N + T - 1) / T;
+  dim3 blk(32, 8), grd((g.W + 31) / 32, (g.H + 7) / 8);
+  // (i) segments
+  k_iota<<<nbN, T, 0, st>>>(S->parent, N);
+  k_edges<<<grd, blk, 0, st>>>(g, c, b, 0, g.H, delta, S->parent);
+  k_compress_flag<<<nbN, T, 0, st>>>(S->parent, S->flag, N);
+  *launches += 3;
+  // flag -> exclusive scan gives the segment index of each root; total S -> scalars[0]
+  cudaMemcpyAsync(S->flag_copy, S->flag, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st);  // keep flags
+  if ((e = scan_excl(S->flag, N, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
+  k_totals<<<1, 32, 0, st>>>(nullptr, N, S->flag, S->flag_copy, S->scalars + 0);
+  ++*launches;
+  cudaMemsetAsync(S->seg_sum, 0, sizeof(unsigned long long) * (size_t)N * C, st);
+  cudaMemsetAsync(S->seg_cnt, 0, sizeof(unsigned long long) * (size_t)N, st);
+  k_seg_accum<<<grd, blk, 0, st>>>(g, c, b, 0, g.H, S->parent, S->flag, S->seg_sum, S->seg_cnt);
+  ++*launches;
+  if ((e = stage23(N, C, delta, count_dev, palette_dev, max_k, S, st, launches))) return e;
+  k_write_labels<<<nbN, T, 0, st>>>(N, S->parent, S->flag, S->seg_parent, S->seg_flag, labels_dev);
+  ++*launches;
   if (getenv("MSA_LABELS_DEBUG")) {  // debug hook: segment / cluster counts and the cell grid
     int32_t sc[2];
     double g[8];
@@ -495,5 +600,73 @@ cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delt
     fprintf(stderr, "msa_labels: segments %d clusters %d | lo %g %g %g w %g n %d %d %d dims %d ncells %d reach %d shortcut %d\n",
             sc[0], sc[1], g[0], g[1], g[2], g[3], gi[0], gi[1], gi[2], gi[3], gi[4], gi[5], gi[6]);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t msa_labels_part(const MsaGeom& g, const float* c, int b, int r0, int nr, float delta,
+                            const MsaLabelPart& out, MsaLabelScratch** scratch, cudaStream_t st, long long* launches) {
+  const int W = g.W, Np = nr * W;
+  cudaError_t e = ensure_scratch(scratch, (size_t)Np, g.C);
+  if (e != cudaSuccess) return e;
+  MsaLabelScratch* S = *scratch;
+  const int T = 256, nb = (Np + T - 1) / T;
+  dim3 blk(32, 8), grd((W + 31) / 32, (nr + 7) / 8);
+  k_iota<<<nb, T, 0, st>>>(S->parent, Np);
+  k_edges<<<grd, blk, 0, st>>>(g, c, b, r0, nr, delta, S->parent);
+  k_compress_flag<<<nb, T, 0, st>>>(S->parent, S->flag, Np);
+  *launches += 3;
+  cudaMemcpyAsync(S->flag_copy, S->flag, sizeof(int32_t) * Np, cudaMemcpyDeviceToDevice, st);
+  if ((e = scan_excl(S->flag, Np, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
+  k_totals<<<1, 32, 0, st>>>(nullptr, Np, S->flag, S->flag_copy, out.nseg);
+  cudaMemsetAsync(out.sum, 0, sizeof(unsigned long long) * (size_t)Np * g.C, st);
+  cudaMemsetAsync(out.cnt, 0, sizeof(unsigned long long) * (size_t)Np, st);
+  k_seg_accum<<<grd, blk, 0, st>>>(g, c, b, r0, nr, S->parent, S->flag, out.sum, out.cnt);
+  k_part_tables<<<nb, T, 0, st>>>(Np, r0 * W, S->parent, S->flag, S->flag_copy, out.roots, out.seg_of_pix);
+  k_part_bounds<<<(W + T - 1) / T, T, 0, st>>>(g, c, b, r0, nr, delta, S->parent, out.bounds);
+  *launches += 4;
+  return cudaGetLastError();
+}
+
+cudaError_t msa_labels_merge(int nparts, int S_total, int W, int C, const int32_t* roots, const unsigned long long* cnt,
+                             const unsigned long long* sum, const int32_t* bounds, float delta, int32_t* cl_of_seg,
+                             int32_t* count_dev, float* palette_dev, int max_k, MsaLabelScratch** scratch,
+                             cudaStream_t st, long long* launches) {
+  const size_t n = S_total > 0 ? (size_t)S_total : 1;
+  cudaError_t e = ensure_scratch(scratch, n, C);
+  if (e != cudaSuccess) return e;
+  MsaLabelScratch* S = *scratch;
+  const int T = 256, nb = ((int)n + T - 1) / T;
+  int32_t* mP = S->parent;       // union-find over the concatenated segments
+  int32_t* midx = S->flag;       // representative flags -> merged index (exclusive scan)
+  int32_t* m_of_seg = S->merge_idx;  // merged index of every concatenated segment
+  k_set_scalar<<<1, 32, 0, st>>>(S->scalars, 2, S_total);
+  k_iota_n<<<nb, T, 0, st>>>(S->scalars, mP);
+  *launches += 2;
+  if (nparts > 1 && W > 0) {
+    k_cross_edges<<<((nparts - 1) * W + T - 1) / T, T, 0, st>>>(nparts, W, bounds, roots, S->scalars, mP);
+    ++*launches;
+  }
+  // compress, representative flags (the smallest segment = smallest root of each merged set)
+  k_compress_flag<<<nb, T, 0, st>>>(mP, midx, (int)n);
+  cudaMemcpyAsync(S->flag_copy, midx, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st);
+  *launches += 1;
+  if ((e = scan_excl(midx, (int)n, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
+  k_totals<<<1, 32, 0, st>>>(S->scalars + 2, (int)n, midx, S->flag_copy, S->scalars + 0);  // merged segments
+  // exact merged sums in merged (smallest-member) order
+  cudaMemsetAsync(S->seg_sum, 0, sizeof(unsigned long long) * n * C, st);
+  cudaMemsetAsync(S->seg_cnt, 0, sizeof(unsigned long long) * n, st);
+  k_cluster_sums<<<nb, T, 0, st>>>(S->scalars + 2, C, mP, midx, sum, cnt, S->seg_sum, S->seg_cnt);
+  k_merged_index<<<nb, T, 0, st>>>(S->scalars, mP, midx, m_of_seg);
+  *launches += 3;
+  if ((e = stage23((int)n, C, delta, count_dev, palette_dev, max_k, S, st, launches))) return e;
+  k_cluster_of_seg<<<nb, T, 0, st>>>(S->scalars, m_of_seg, S->seg_parent, S->seg_flag, cl_of_seg);
+  ++*launches;
+  return cudaGetLastError();
+}
+
+cudaError_t msa_labels_relabel(int npix, const int32_t* seg_of_pix, int seg_off, const int32_t* cl_of_seg,
+                               int32_t* labels, cudaStream_t st) {
+  if (npix <= 0) return cudaSuccess;
+  k_relabel<<<(npix + 255) / 256, 256, 0, st>>>(npix, seg_of_pix, seg_off, cl_of_seg, labels);
   return cudaGetLastError();
 }
