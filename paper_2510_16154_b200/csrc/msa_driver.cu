@@ -495,6 +495,9 @@ int do_steps(msa_ctx* x, int64_t n) {
     if (!launched && k1_variant() != K1_GENERIC)
       e = msa_launch_iter_fast(x->g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
                                          x->cb[o], x->p[o], x->stream, &launched);
+    if (!launched && k1_variant() != K1_GENERIC && (e == cudaErrorNotSupported || e == cudaSuccess))
+      e = msa_launch_iter_cn(x->g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
+                             x->p[o], x->stream, &launched);
     if (!launched) {
       if (e != cudaErrorNotSupported && e != cudaSuccess)
         return set_err(MSA_ECUDA, "fast iteration kernel: %s", cudaGetErrorString(e));

@@ -29,6 +29,12 @@ cudaError_t msa_launch_iter_sweep(const MsaGeom& g, const MsaIterConsts& K, cons
                                   const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                   float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched);
 
+// Tiled TMA kernel for many channels (msa_iter_cn.cu): C = 16, R in [1,4]; bitwise equal to the
+// generic kernel. Same contract as msa_launch_iter_fast.
+cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                               const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                               float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched);
+
 // Round update (steps 4-5): writes mu_out (may alias mu) and per-block fp64 partial sums
 // [nb][nblk][MSA_NSUM]; *nblk receives the number of blocks per image.
 cudaError_t msa_launch_round(const MsaGeom& g, const MsaRoundConsts& R, const float* c, const float* p,

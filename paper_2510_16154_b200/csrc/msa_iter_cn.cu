@@ -1,0 +1,261 @@
+// msa_iter_cn.cu - K1 for many channels (C = 16: BASELINE config 5), sm_100a.
+//
+// At C = 16 the iteration moves 704 bytes per pixel against ~1600 FP32 operations, so it is
+// HBM-bound (3.6 ms HBM floor vs 1.5 ms ALU floor per 32 x 1024^2 iteration): the
+// kernel is organised for bytes in flight, not for ALU tricks.
+//   * CTA = 32 x 8 pixels, one thread per pixel (256 threads), 2 CTAs per SM. Measured
+//     alternatives that ran slower at cfg5: 32 x 4 tiles at 4-5 CTAs per SM, a packed two-pixel
+//     f32x2 form (half the issue slots, lower occupancy), unrolled offsets with a streamed dual.
+//   * One elected thread issues two TMA tensor loads: the c tile with an R-row / 4-column halo
+//     ([C][TH+2R][40]) and the cbar tile with one row below / above ([C][TH+2][40]); out-of-image
+//     boxes are zero-filled and masked by coordinates (R20).
+//   * Step 1 (eq:MAsystem, windowed, R2): neighbours from shared memory, the driver's offset order
+//     and msa_agent_term, so results equal the generic kernel bit for bit.
+//   * Step 2 (dual ascent + projection, R7): p+ for the tile and its low-side halo (33 x TH+1), with
+//     p and mu read straight from global memory (coalesced: a warp reads consecutive columns of
+//     one component row), written to shared memory (reusing the c tile).
+//   * Step 3 (div, prox fidelity, extrapolation, R6/R21): coalesced loads of I and stores of
+//     c+, cbar+, p+.
+#include <cuda.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "msa_internal.h"
+#include "msa_tma.cuh"
+
+namespace {
+
+using namespace msa_tma;
+
+
+#ifndef MSA_CN_TH
+#define MSA_CN_TH 8
+#endif
+constexpr int TW = 32, TH = MSA_CN_TH, NT = TW * TH;  // one pixel per thread
+#ifndef MSA_CN_OCC
+#define MSA_CN_OCC 2
+#endif
+constexpr int CN_OCC = MSA_CN_OCC;
+constexpr int CX = 4;           // smem column of tile column 0 (box starts 16-byte aligned)
+constexpr int CW = TW + 2 * CX; // 40
+constexpr int QW = TW + 1;      // p+ tile: columns x0-1 .. x0+31
+constexpr int QH = TH + 1;      // rows y0-1 .. y0+7
+
+struct CnOffsets {
+  int n;
+  signed char dx[MSA_MAXOFF], dy[MSA_MAXOFF];
+  float om[MSA_MAXOFF];
+};
+struct CnMaps {
+  CUtensorMap c, cb;
+  CUtensorMap p, mu, I;  // L2 prefetch boxes of the step-2/3 inputs
+};
+
+template <int C, int R>
+struct CnSmem {
+  static constexpr int c_floats = C * (TH + 2 * R) * CW;
+  static constexpr int q_floats = 2 * C * QH * QW;
+  static constexpr int u_floats = ((c_floats > q_floats ? c_floats : q_floats) + 31) / 32 * 32;
+  static constexpr int cb_off = u_floats;
+  static constexpr int cb_floats = C * (TH + 2) * CW;
+  static constexpr size_t bytes = sizeof(float) * (cb_off + cb_floats);
+};
+
+template <int C, int R, int KER>
+__global__ void __launch_bounds__(NT, CN_OCC)
+    k_iter_cn(MsaGeom g, MsaIterConsts K, const __grid_constant__ CnOffsets T, const __grid_constant__ CnMaps tm,
+              const float* __restrict__ p, const float* __restrict__ mu, const float* __restrict__ I,
+              float* __restrict__ c_out, float* __restrict__ cb_out, float* __restrict__ p_out) {
+  using S = CnSmem<C, R>;
+  constexpr int SH = TH + 2 * R, BH = TH + 2;
+  extern __shared__ __align__(128) float smem[];
+  float* sc = smem;             // [C][SH][CW] c tile (step 1)
+  float* sq = smem;             // [2C][QH][QW] p+ (steps 2-3, reuses the c tile)
+  float* scb = smem + S::cb_off;  // [C][BH][CW] cbar rows y0-1 .. y0+TH
+  __shared__ __align__(8) unsigned long long bar;
+
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * TW, y0 = g.row0 + blockIdx.y * TH, b = blockIdx.z;
+  const int W = g.W, H = g.H;
+  const int x = x0 + tx;
+  const int ys = y0 - g.row0 + g.G;  // stored row of y0
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, (unsigned)(sizeof(float) * (C * SH * CW + C * BH * CW)));
+    tma_load3(sc, &tm.c, x0 - CX, ys - R, b * C, &bar);
+    tma_load3(scb, &tm.cb, x0 - CX, ys - 1, b * C, &bar);
+    // steps 2-3 read p, mu (tile + low-side halo) and I straight from global memory: pull them
+    // into L2 now, so those loads wait for L2 rather than HBM after step 1
+    tma_prefetch3(&tm.p, x0 - CX, ys - 1, b * 2 * C);
+    tma_prefetch3(&tm.mu, x0 - CX, ys - 1, b * 2 * C);
+    tma_prefetch3(&tm.I, x0, ys, b * C);
+  }
+  mbar_wait(&bar, 0);
+
+  const int y = y0 + ty;
+  // ---- step 1: agent Euler step (the driver's offset order, msa_agent_term: bitwise equal to the
+  // generic kernel)
+  float chalf[C];
+  {
+    float ci[C], acc[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      ci[k] = sc[(k * SH + ty + R) * CW + CX + tx];
+      acc[k] = 0.0f;
+    }
+    for (int o = 0; o < T.n; ++o) {
+      const int dx = T.dx[o], dy = T.dy[o];
+      const int xx = x + dx, yy = y + dy;
+      if (xx < 0 || xx >= W || yy < 0 || yy >= H) continue;  // excluded, not padded (R20)
+      float cj[C];
+      const float* src = sc + (ty + R + dy) * CW + CX + tx + dx;
+#pragma unroll
+      for (int k = 0; k < C; ++k) cj[k] = src[k * SH * CW];
+      msa_agent_term<C, KER>(ci, cj, T.om[o], K.e_c, acc);
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+  }
+  __syncthreads();  // the c tile is dead: sq reuses it
+
+  // ---- step 2: p+ at tile coordinates (hx - 1, hy - 1), hx < 33, hy < TH + 1
+  for (int idx = threadIdx.x; idx < QW * QH; idx += NT) {
+    const int hy = idx / QW, hx = idx - hy * QW;
+    const int xx = x0 + hx - 1, yy = y0 + hy - 1;
+    if (xx < 0 || yy < 0 || xx >= W || yy >= H) continue;  // never read (div masks those terms)
+    float gx[C], gy[C], px[C], py[C], mx[C], my[C], qx[C], qy[C];
+    const long long o0 = msa_idx(g, b, 0, 2 * C, yy, xx);
+    const float* pp = p + o0;
+    const float* mp = mu + o0;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const float* cbk = scb + (k * BH + hy) * CW + CX + hx - 1;
+      const float c0 = cbk[0];
+      gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(cbk[1], c0), K.inv_hx) : 0.0f;
+      gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(cbk[CW], c0), K.inv_hy) : 0.0f;
+      px[k] = __ldg(pp + k * g.plane);
+      py[k] = __ldg(pp + (C + k) * g.plane);
+      mx[k] = __ldg(mp + k * g.plane);
+      my[k] = __ldg(mp + (C + k) * g.plane);
+    }
+    msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      sq[(k * QH + hy) * QW + hx] = qx[k];
+      sq[((C + k) * QH + hy) * QW + hx] = qy[k];
+    }
+  }
+  __syncthreads();
+
+  // ---- step 3: div p+ (R6), prox fidelity, extrapolation (R21), coalesced stores
+  if (x >= W || y >= g.row0 + g.nrows) return;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const float qx0 = sq[(k * QH + ty + 1) * QW + tx + 1], qy0 = sq[((C + k) * QH + ty + 1) * QW + tx + 1];
+    float ax = x < W - 1 ? qx0 : 0.0f;
+    if (x > 0) ax = __fsub_rn(ax, sq[(k * QH + ty + 1) * QW + tx]);
+    float ay = y < H - 1 ? qy0 : 0.0f;
+    if (y > 0) ay = __fsub_rn(ay, sq[((C + k) * QH + ty) * QW + tx + 1]);
+    const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
+    float cp, cbp;
+    msa_prox_extrap(K, chalf[k], d, __ldg(I + msa_idx(g, b, k, C, y, x)), cp, cbp);
+    c_out[msa_idx(g, b, k, C, y, x)] = cp;
+    cb_out[msa_idx(g, b, k, C, y, x)] = cbp;
+    p_out[msa_idx(g, b, k, 2 * C, y, x)] = qx0;
+    p_out[msa_idx(g, b, C + k, 2 * C, y, x)] = qy0;
+  }
+}
+
+struct CnKey {
+  const float *c, *cb, *p, *mu, *I;
+  int W, rows, nb, pitch, C, R;
+  long long plane;
+  bool operator==(const CnKey& o) const { return memcmp(this, &o, sizeof(CnKey)) == 0; }
+};
+
+bool get_maps(const CnKey& k, const MsaGeom& g, int R, CnMaps* out) {
+  static std::mutex mu;
+  static CnKey keys[16];
+  static CnMaps sets[16];
+  static int n = 0, next = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int i = 0; i < n; ++i)
+    if (keys[i] == k) {
+      *out = sets[i];
+      return true;
+    }
+  CnMaps t;
+  if (!encode_map(&t.c, g, k.c, g.C, CW, TH + 2 * R) || !encode_map(&t.cb, g, k.cb, g.C, CW, TH + 2) ||
+      !encode_map(&t.p, g, k.p, 2 * g.C, CW - CX, TH + 1) || !encode_map(&t.mu, g, k.mu, 2 * g.C, CW - CX, TH + 1) ||
+      !encode_map(&t.I, g, k.I, g.C, TW, TH))
+    return false;
+  const int slot = n < 16 ? n++ : (next++ % 16);
+  keys[slot] = k;
+  sets[slot] = t;
+  *out = t;
+  return true;
+}
+
+template <int C, int R, int KER>
+cudaError_t launch_k(const MsaGeom& g, const MsaIterConsts& K, const CnOffsets& T, const CnMaps& tm, const float* p,
+                     const float* mu, const float* I, float* co, float* cbo, float* po, cudaStream_t s) {
+  using S = CnSmem<C, R>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_iter_cn<C, R, KER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grd((g.W + TW - 1) / TW, (g.nrows + TH - 1) / TH, g.nb);
+  k_iter_cn<C, R, KER><<<grd, NT, S::bytes, s>>>(g, K, T, tm, p, mu, I, co, cbo, po);
+  return cudaGetLastError();
+}
+
+template <int C>
+cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, const CnOffsets& T, const CnMaps& tm, int R,
+                     const float* p, const float* mu, const float* I, float* co, float* cbo, float* po, cudaStream_t s) {
+#define CN_CASE(RR)                                                                                   \
+  case RR:                                                                                            \
+    return K.kernel == 0 ? launch_k<C, RR, 0>(g, K, T, tm, p, mu, I, co, cbo, po, s)                  \
+                         : launch_k<C, RR, 1>(g, K, T, tm, p, mu, I, co, cbo, po, s);
+  switch (R) {
+    CN_CASE(1)
+    CN_CASE(2)
+    CN_CASE(3)
+    CN_CASE(4)
+    default: return cudaErrorNotSupported;
+  }
+#undef CN_CASE
+}
+
+}  // namespace
+
+cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                               const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                               float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
+  *launched = 0;
+  if (g.C != 16 || R < 1 || R > 4) return cudaErrorNotSupported;
+  CnOffsets off;
+  off.n = T.n;
+  for (int o = 0; o < T.n; ++o) {
+    if (T.dx[o] < -R || T.dx[o] > R || T.dy[o] < -R || T.dy[o] > R) return cudaErrorNotSupported;
+    off.dx[o] = (signed char)T.dx[o];
+    off.dy[o] = (signed char)T.dy[o];
+    off.om[o] = T.om[o];
+  }
+  CnKey key;
+  memset(&key, 0, sizeof(key));
+  key.c = c; key.cb = cb; key.p = p; key.mu = mu; key.I = I;
+  key.W = g.W; key.rows = g.nrows + 2 * g.G; key.nb = g.nb; key.pitch = g.pitch; key.C = g.C; key.R = R;
+  key.plane = g.plane;
+  CnMaps tm;
+  if (!get_maps(key, g, R, &tm)) return cudaErrorNotSupported;
+  cudaError_t e = launch_c<16>(g, K, off, tm, R, p, mu, I, c_out, cb_out, p_out, s);
+  if (e == cudaSuccess) *launched = 1;
+  return e;
+}

@@ -36,6 +36,8 @@ CASES = [
     ((1, 64, 32, 3), 5, 0), ((1, 130, 97, 3), 5, 0), ((1, 37, 29, 3), 3, 0), ((2, 70, 66, 3), 2, 1),
     ((1, 5, 7, 3), 4, 0), ((1, 1, 50, 3), 2, 0), ((1, 200, 3, 3), 3, 0), ((1, 256, 256, 3), 5, 1),
 ]
+# many-channel tiled kernel (msa_iter_cn.cu, C = 16): same contract, bitwise equal to the generic one
+CN_CASES = [((2, 40, 36, 16), 3, 0), ((1, 33, 70, 16), 4, 1), ((1, 9, 5, 16), 2, 0), ((1, 64, 64, 16), 1, 0)]
 
 
 def _spec(shape, R, ker, iters=3):
@@ -46,7 +48,7 @@ def _spec(shape, R, ker, iters=3):
                             gamma=2.5 * h, iters_per_round=2, rounds=1))
 
 
-@pytest.mark.parametrize("shape,R,ker", CASES)
+@pytest.mark.parametrize("shape,R,ker", CASES + CN_CASES)
 def test_tile_equals_generic_bitwise(shape, R, ker, tmp_path):
     spec = _spec(shape, R, ker)
     a = _run(spec, "generic", tmp_path)
