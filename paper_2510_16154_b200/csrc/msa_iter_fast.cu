@@ -39,8 +39,11 @@ using namespace msa_f32x2;
 
 constexpr int C = 3;
 constexpr int TW = 32;           // tile width (= lanes)
-constexpr int NT = 256;          // threads: 8 strips of P rows
-constexpr int NSTRIP = 8;
+#ifndef MSA_TILE_NS
+#define MSA_TILE_NS 8
+#endif
+constexpr int NSTRIP = MSA_TILE_NS;  // warps = strips of P rows
+constexpr int NT = 32 * NSTRIP;
 constexpr int SX = 8;            // smem column of tile column 0 in the c tile (>= R, 16-byte aligned)
 constexpr int SW = TW + 2 * SX;  // 48
 constexpr int BX = 4;            // smem column of tile column 0 in the cbar / p / mu tiles
@@ -178,7 +181,11 @@ __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const 
 
 template <int P>
 struct Occ {
+#ifdef MSA_TILE_OCC
+  static constexpr int blocks = MSA_TILE_OCC;
+#else
   static constexpr int blocks = P >= 4 ? 2 : 3;
+#endif
 };
 
 template <int R, int P>

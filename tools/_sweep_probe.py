@@ -12,7 +12,7 @@ for shape, R in cases:
                 params=dict(alpha=8.0 / h, beta=1.0, radius=R, kernel=0, eps_c=20.0, dt=0.25, rho=2.5 * h,
                             gamma=2.5 * h, iters_per_round=2, rounds=1))
     outs = {}
-    for v in ("generic", "sweep"):
+    for v in ("generic", os.environ.get("PROBE_VARIANT", "sweep")):
         env = dict(os.environ, MSA_K1=v)
         out = f"/tmp/probe_{v}.npz"
         r = subprocess.run([sys.executable, RUN, json.dumps(spec), out], env=env, capture_output=True, text=True, timeout=120)
@@ -20,10 +20,11 @@ for shape, R in cases:
             outs[v] = r.stderr.strip().splitlines()[-1][:200]
         else:
             outs[v] = np.load(out)
-    if isinstance(outs["sweep"], str) or isinstance(outs["generic"], str):
-        print(shape, R, "FAIL", outs["sweep"] if isinstance(outs["sweep"], str) else outs["generic"], flush=True)
+    vv = os.environ.get("PROBE_VARIANT", "sweep")
+    if isinstance(outs[vv], str) or isinstance(outs["generic"], str):
+        print(shape, R, "FAIL", outs[vv] if isinstance(outs[vv], str) else outs["generic"], flush=True)
         continue
-    a, b = outs["generic"], outs["sweep"]
+    a, b = outs["generic"], outs[vv]
     d = np.abs(a["c"] - b["c"])
     idx = np.unravel_index(np.argmax(d), d.shape)
     print(shape, R, "c maxdiff", float(d.max()), "at", idx, "p eq", bool(np.array_equal(a["p"], b["p"])),
