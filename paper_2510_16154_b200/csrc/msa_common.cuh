@@ -22,7 +22,10 @@ struct MsaGeom {
   long long plane; // floats per component plane = (nrows + 2G) * pitch
   int nb;          // images held by this rank
   int C;           // channels
+  int k1_lo, k1_hi;  // K1 launches cover local rows [k1_lo, k1_hi) (k1_hi = 0: all owned rows);
+                     // rows mode splits an iteration into interior and boundary launches (§8(e))
 };
+__host__ __device__ __forceinline__ int msa_k1_hi(const MsaGeom& g) { return g.k1_hi > 0 ? g.k1_hi : g.nrows; }
 
 __device__ __forceinline__ long long msa_idx(const MsaGeom& g, int b, int m, int nm, int j, int i) {
   return ((long long)b * nm + m) * g.plane + (long long)(j - g.row0 + g.G) * g.pitch + i;

@@ -114,6 +114,9 @@ struct msa_ctx {
   int64_t iter_launches_t = 0, round_launches_t = 0;
   // nccl
   ncclComm_t comm = nullptr;
+  // rows mode: halo exchange on its own stream, overlapped with the interior K1 launch (§8(e))
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
   // labels
   MsaLabelScratch* lab = nullptr;
   int32_t* lab_buf = nullptr;
@@ -371,7 +374,8 @@ int halo_plan(int H, int world, int rank, int R, int phase, std::vector<msa_halo
 }
 
 // --- halo exchange of the current state (rows mode, world > 1): the plan's ops as one NCCL group
-int halo_exchange(msa_ctx* x, int phase) {
+int halo_exchange(msa_ctx* x, int phase, cudaStream_t st = nullptr) {
+  if (!st) st = x->stream;
   const msa_params& P = x->prm;
   if (!(P.world > 1 && P.shard == MSA_SHARD_ROWS)) return MSA_OK;
   std::vector<msa_halo_op> ops;
@@ -389,9 +393,9 @@ int halo_exchange(msa_ctx* x, int phase) {
         float* rows = f + ((size_t)b * nm + m) * g.plane + (size_t)(op.row0 - g.row0 + g.G) * g.pitch;
         const size_t n = (size_t)op.nrows * g.pitch;
         if (op.send)
-          NCCL_TRY(g_nccl.Send(rows, n, ncclFloat, op.peer, x->comm, x->stream));
+          NCCL_TRY(g_nccl.Send(rows, n, ncclFloat, op.peer, x->comm, st));
         else
-          NCCL_TRY(g_nccl.Recv(rows, n, ncclFloat, op.peer, x->comm, x->stream));
+          NCCL_TRY(g_nccl.Recv(rows, n, ncclFloat, op.peer, x->comm, st));
       }
   }
   NCCL_TRY(g_nccl.GroupEnd());
@@ -472,41 +476,85 @@ int k1_variant() {
   return v;
 }
 
+// One K1 launch over the rows of geometry g (the whole slab, or an interior / boundary part):
+// the variant cascade sweep (opt-in) -> tiled C = 3 -> C = 16 -> generic.
+int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int o) {
+  const msa_params& P = x->prm;
+  int launched = 0;
+  cudaError_t e = cudaErrorNotSupported;
+  if (k1_variant() == K1_SWEEP)
+    e = msa_launch_iter_sweep(g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
+                              x->p[o], x->stream, &launched);
+  if (!launched && e != cudaErrorNotSupported && e != cudaSuccess)
+    return set_err(MSA_ECUDA, "sweep iteration kernel: %s", cudaGetErrorString(e));
+  if (!launched && k1_variant() != K1_GENERIC)
+    e = msa_launch_iter_fast(g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
+                             x->p[o], x->stream, &launched);
+  if (!launched && k1_variant() != K1_GENERIC && (e == cudaErrorNotSupported || e == cudaSuccess))
+    e = msa_launch_iter_cn(g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
+                           x->p[o], x->stream, &launched);
+  if (!launched) {
+    if (e != cudaErrorNotSupported && e != cudaSuccess)
+      return set_err(MSA_ECUDA, "fast iteration kernel: %s", cudaGetErrorString(e));
+    e = msa_launch_iter_generic(g, KC, x->d_off, x->d_om, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
+                                x->cb[o], x->p[o], x->stream);
+  }
+  if (e != cudaSuccess) return set_err(MSA_ECUDA, "iteration kernel launch: %s", cudaGetErrorString(e));
+  ++x->launches;
+  if (x->timing) ++x->iter_launches_t;
+  return MSA_OK;
+}
+
+// Interior / boundary split of a slab: rows within SPLIT of either slab edge read ghost rows (or,
+// for the top edge, produce the rows the exchange sends), the rest do not. SPLIT = 32 is a
+// multiple of every K1 tile height, so the parts are whole tile rows.
+constexpr int SPLIT = 32;
+bool split_rows(const MsaGeom& g, int* lo, int* hi) {
+  if (g.nrows < 3 * SPLIT) return false;
+  *lo = SPLIT;
+  *hi = SPLIT + (g.nrows - 2 * SPLIT) / SPLIT * SPLIT;
+  return true;
+}
+
 int do_steps(msa_ctx* x, int64_t n) {
   const msa_params& P = x->prm;
   const int K = P.iters_per_round;
   MsaIterConsts KC = iter_consts(x, x->rho_cur);
+  const bool rows = P.world > 1 && P.shard == MSA_SHARD_ROWS;
+  // test hook: MSA_K1_SPLIT=1 runs the interior / boundary launches on one GPU (no exchange)
+  static const bool force_split = getenv("MSA_K1_SPLIT") != nullptr;
+  int lo = 0, hi = 0;
+  const bool split = (rows && x->comm_stream) || force_split ? split_rows(x->g, &lo, &hi) : false;
   int rc;
   for (int64_t t = 0; t < n; ++t) {
     const int s = x->cur, o = 1 - s;
-    if (P.world > 1 && P.shard == MSA_SHARD_ROWS) {
+    if (rows && split) {
+      // exchange on the comm stream once everything before (the previous boundary launch, a
+      // round) is done; the interior launch runs meanwhile; the boundary launch waits for it
+      CUDA_TRY(cudaEventRecord(x->ev_ready, x->stream));
+      CUDA_TRY(cudaStreamWaitEvent(x->comm_stream, x->ev_ready, 0));
+      if (x->halo_mu_dirty && (rc = halo_exchange(x, MSA_HALO_MU, x->comm_stream)) != MSA_OK) return rc;
+      x->halo_mu_dirty = false;
+      if ((rc = halo_exchange(x, MSA_HALO_ITER, x->comm_stream)) != MSA_OK) return rc;
+      CUDA_TRY(cudaEventRecord(x->ev_halo, x->comm_stream));
+    } else if (rows) {
       if (x->halo_mu_dirty && (rc = halo_exchange(x, MSA_HALO_MU)) != MSA_OK) return rc;
       x->halo_mu_dirty = false;
       if ((rc = halo_exchange(x, MSA_HALO_ITER)) != MSA_OK) return rc;
     }
     iter_batch_begin(x);
-    int launched = 0;
-    cudaError_t e = cudaErrorNotSupported;
-    if (k1_variant() == K1_SWEEP)
-      e = msa_launch_iter_sweep(x->g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
-                                x->cb[o], x->p[o], x->stream, &launched);
-    if (!launched && e != cudaErrorNotSupported && e != cudaSuccess)
-      return set_err(MSA_ECUDA, "sweep iteration kernel: %s", cudaGetErrorString(e));
-    if (!launched && k1_variant() != K1_GENERIC)
-      e = msa_launch_iter_fast(x->g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
-                                         x->cb[o], x->p[o], x->stream, &launched);
-    if (!launched && k1_variant() != K1_GENERIC && (e == cudaErrorNotSupported || e == cudaSuccess))
-      e = msa_launch_iter_cn(x->g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
-                             x->p[o], x->stream, &launched);
-    if (!launched) {
-      if (e != cudaErrorNotSupported && e != cudaSuccess)
-        return set_err(MSA_ECUDA, "fast iteration kernel: %s", cudaGetErrorString(e));
-      e = msa_launch_iter_generic(x->g, KC, x->d_off, x->d_om, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
-                                  x->cb[o], x->p[o], x->stream);
+    if (split) {
+      MsaGeom gi = x->g, gb0 = x->g, gb1 = x->g;
+      gi.k1_lo = lo; gi.k1_hi = hi;
+      gb0.k1_lo = 0; gb0.k1_hi = lo;
+      gb1.k1_lo = hi; gb1.k1_hi = x->g.nrows;
+      if ((rc = launch_k1(x, gi, KC, s, o)) != MSA_OK) return rc;
+      if (rows) CUDA_TRY(cudaStreamWaitEvent(x->stream, x->ev_halo, 0));
+      if ((rc = launch_k1(x, gb0, KC, s, o)) != MSA_OK) return rc;
+      if ((rc = launch_k1(x, gb1, KC, s, o)) != MSA_OK) return rc;
+    } else {
+      if ((rc = launch_k1(x, x->g, KC, s, o)) != MSA_OK) return rc;
     }
-    if (e != cudaSuccess) return set_err(MSA_ECUDA, "iteration kernel launch: %s", cudaGetErrorString(e));
-    ++x->launches;
-    if (x->timing) ++x->iter_launches_t;
     x->cur = o;
     ++x->iters_done;
     if (x->iters_done % K == 0) {
@@ -554,7 +602,11 @@ void free_ctx(msa_ctx* x) {
   if (x->stream) cudaStreamSynchronize(x->stream);
   for (auto& e : x->iter_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (auto& e : x->round_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  if (x->comm_stream) cudaStreamSynchronize(x->comm_stream);
   if (x->comm) g_nccl.CommDestroy(x->comm);
+  if (x->comm_stream) cudaStreamDestroy(x->comm_stream);
+  if (x->ev_ready) cudaEventDestroy(x->ev_ready);
+  if (x->ev_halo) cudaEventDestroy(x->ev_halo);
   msa_labels_free(x->lab);
   if (x->lab_buf) cudaFree(x->lab_buf);
   if (x->lab_count) cudaFree(x->lab_count);
@@ -691,6 +743,12 @@ int msa_init(const msa_params* params, const float* image, int image_on_device, 
     memcpy(&id, params->nccl_id, sizeof(id));
     ncclResult_t r = g_nccl.CommInitRank(&x->comm, params->world, id, params->rank);
     if (r != ncclSuccess) return fail(set_err(MSA_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)));
+    if (!getenv("MSA_NO_OVERLAP")) {  // A/B hook: serial exchange -> K1
+      cudaError_t e1 = cudaStreamCreateWithFlags(&x->comm_stream, cudaStreamNonBlocking);
+      if (e1 == cudaSuccess) e1 = cudaEventCreateWithFlags(&x->ev_ready, cudaEventDisableTiming);
+      if (e1 == cudaSuccess) e1 = cudaEventCreateWithFlags(&x->ev_halo, cudaEventDisableTiming);
+      if (e1 != cudaSuccess) return fail(set_err(MSA_ECUDA, "comm stream: %s", cudaGetErrorString(e1)));
+    }
   }
   if ((rc = upload_image(x, image, image_on_device)) != MSA_OK) return fail(rc);
   cudaError_t e = cudaStreamSynchronize(x->stream);

@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(NT, CN_OCC)
   __shared__ __align__(8) unsigned long long bar;
 
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int x0 = blockIdx.x * TW, y0 = g.row0 + blockIdx.y * TH, b = blockIdx.z;
+  const int x0 = blockIdx.x * TW, y0 = g.row0 + g.k1_lo + blockIdx.y * TH, b = blockIdx.z;
   const int W = g.W, H = g.H;
   const int x = x0 + tx;
   const int ys = y0 - g.row0 + g.G;  // stored row of y0
@@ -211,7 +211,9 @@ cudaError_t launch_k(const MsaGeom& g, const MsaIterConsts& K, const CnOffsets& 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grd((g.W + TW - 1) / TW, (g.nrows + TH - 1) / TH, g.nb);
+  const int nr = msa_k1_hi(g) - g.k1_lo;
+  if (nr <= 0) return cudaSuccess;
+  dim3 grd((g.W + TW - 1) / TW, (nr + TH - 1) / TH, g.nb);
   k_iter_cn<C, R, KER><<<grd, NT, S::bytes, s>>>(g, K, T, tm, p, mu, I, co, cbo, po);
   return cudaGetLastError();
 }

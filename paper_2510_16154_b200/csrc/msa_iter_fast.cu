@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(NT, Occ<P>::blocks)
   float* sI = smem + S::I_off;    // [C][TH][TW]
 
   const int lx = threadIdx.x & 31, strip = threadIdx.x >> 5;
-  const int x0 = blockIdx.x * TW, y0 = g.row0 + blockIdx.y * TH, b = blockIdx.z;
+  const int x0 = blockIdx.x * TW, y0 = g.row0 + g.k1_lo + blockIdx.y * TH, b = blockIdx.z;
   const int W = g.W, H = g.H;
   const int x = x0 + lx, ybase = y0 + strip * P;
 
@@ -390,7 +390,9 @@ cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  dim3 grd((g.W + TW - 1) / TW, (g.nrows + S::TH - 1) / S::TH, g.nb);
+  const int nr = msa_k1_hi(g) - g.k1_lo;
+  if (nr <= 0) return cudaSuccess;
+  dim3 grd((g.W + TW - 1) / TW, (nr + S::TH - 1) / S::TH, g.nb);
   k_iter_fast_c3<R, P><<<grd, NT, S::bytes, s>>>(g, K, om, tm);
   return cudaGetLastError();
 }

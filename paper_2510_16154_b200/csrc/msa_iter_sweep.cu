@@ -568,7 +568,7 @@ cudaError_t msa_launch_iter_sweep(const MsaGeom& g, const MsaIterConsts& K, cons
                                   const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                   float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
-  if (g.C != 3) return cudaErrorNotSupported;
+  if (g.C != 3 || g.k1_lo != 0 || msa_k1_hi(g) != g.nrows) return cudaErrorNotSupported;  // whole slab only
   // the sentinel needs eps_c > 0: with e_c * (1e18)^2 >= 1e6 an out-of-image partner has t < 0
   if (!(K.e_c >= 1e-30f)) return cudaErrorNotSupported;
   for (int o = 0; o < T.n; ++o)

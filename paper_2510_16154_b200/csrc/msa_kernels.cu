@@ -21,9 +21,9 @@ __global__ void __launch_bounds__(256) k_iter_generic(MsaGeom g, MsaIterConsts K
                                                       float* __restrict__ c_out, float* __restrict__ cb_out,
                                                       float* __restrict__ p_out) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  const int jl = g.k1_lo + blockIdx.y * blockDim.y + threadIdx.y;
   const int b = blockIdx.z;
-  if (i >= g.W || jl >= g.nrows) return;
+  if (i >= g.W || jl >= msa_k1_hi(g)) return;
   const int j = g.row0 + jl;
   const int W = g.W, H = g.H;
   // step 1: agent Euler step (eq:MAsystem windowed, R2)
@@ -91,7 +91,9 @@ template <int C>
 cudaError_t launch_iter_generic_c(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
                                   const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                   float* co, float* cbo, float* po, cudaStream_t s) {
-  dim3 blk(32, 8), grd((g.W + 31) / 32, (g.nrows + 7) / 8, g.nb);
+  const int nr = msa_k1_hi(g) - g.k1_lo;
+  if (nr <= 0) return cudaSuccess;
+  dim3 blk(32, 8), grd((g.W + 31) / 32, (nr + 7) / 8, g.nb);
   if (K.kernel == 0)
     k_iter_generic<C, 0><<<grd, blk, 0, s>>>(g, K, off, om, c, cb, p, mu, I, co, cbo, po);
   else

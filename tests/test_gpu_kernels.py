@@ -19,11 +19,15 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(spec, variant: str, tmp_path, seg: int = 0):
-    out = str(tmp_path / f"{variant}_{seg}.npz")
+def _run(spec, variant: str, tmp_path, seg: int = 0, split: bool = False):
+    out = str(tmp_path / f"{variant}_{seg}_{int(split)}.npz")
     env = dict(os.environ)
     env.pop("MSA_FORCE_GENERIC", None)
     env["MSA_K1"] = variant
+    if split:
+        env["MSA_K1_SPLIT"] = "1"
+    else:
+        env.pop("MSA_K1_SPLIT", None)
     if seg:
         env["MSA_SWEEP_SEG"] = str(seg)
     else:
@@ -92,3 +96,16 @@ def test_sweep_segment_invariant_and_reproducible(shape, R, tmp_path):
             assert np.array_equal(ref[k], other[k]), (seg, k)
     for k in ("c", "cbar", "p", "mu"):
         assert np.array_equal(ref[k], again[k]), k
+
+
+# Rows mode runs K1 as an interior launch (overlapped with the NCCL halo exchange) plus two
+# boundary launches. MSA_K1_SPLIT=1 runs that split on one GPU: every pixel is
+# computed by the same kernel with the same arithmetic, so the fields must be bitwise equal.
+@pytest.mark.parametrize("shape,R,variant", [((1, 130, 97, 3), 5, "tile"), ((1, 200, 64, 3), 3, "generic"),
+                                             ((2, 100, 36, 16), 3, "tile"), ((1, 96, 40, 3), 2, "tile")])
+def test_k1_interior_boundary_split_bitwise(shape, R, variant, tmp_path):
+    spec = _spec(shape, R, 0, iters=3)
+    a = _run(spec, variant, tmp_path)
+    b = _run(spec, variant, tmp_path, split=True)
+    for k in ("c", "cbar", "p", "mu"):
+        assert np.array_equal(a[k], b[k]), k
