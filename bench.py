@@ -238,9 +238,10 @@ def main():
     solver = msa.Solver(params, dev_img, stream=stream)
     info = solver.query()
     own_px = info.nrows * W * info.nimages
-    lab_dev = torch.empty((info.nimages, H, W), dtype=torch.int32, device="cuda")
+    # labels of this rank's rows (rows mode: per-slab stage (i), all-gathered tables, identical merge)
+    lab_dev = torch.empty((info.nimages, info.nrows, W), dtype=torch.int32, device="cuda")
     cnt_dev = torch.empty(info.nimages, dtype=torch.int32, device="cuda")
-    labels_ok = world == 1
+    labels_ok = True
 
     def step():
         solver.reset(dev_img)
@@ -285,7 +286,7 @@ def main():
     #  ALU:   n_off*(3C+5) + 27C + 2 FP32 pipe operations per pixel-iteration (the interaction term
     #         sub/square-sum/t/phi/accumulate per active offset, plus steps 2-3); peak = 148 SMs x
     #         128 FP32 lanes x clocks.max.sm (B200_PROFILING.md unit counts).
-    k1_avg_ms = tim["iter_ms"] / max(tim["iter_launches"], 1)
+    k1_avg_ms = tim["iter_ms"] / max(tim["iter_launches"], 1)  # per iteration (rows mode: 3 launches)
     alg_bytes = 44.0 * C * own_px
     achieved = alg_bytes / (k1_avg_ms * 1e-3) / 1e9
     peak, peak_src = _hbm_peak()
@@ -304,7 +305,7 @@ def main():
     e2e = None
     if not args.no_e2e:
         host_img = torch.from_numpy(img).pin_memory()
-        host_lab = torch.empty((info.nimages, H, W), dtype=torch.int32).pin_memory()
+        host_lab = torch.empty((info.nimages, info.nrows, W), dtype=torch.int32).pin_memory()
         host_cnt = np.empty(info.nimages, dtype=np.int32)
 
         def step_e2e():

@@ -196,8 +196,10 @@ int msa_set_state(msa_ctx* ctx, const void* host_blob, size_t bytes);
 int msa_query(msa_ctx* ctx, msa_info* info);
 
 /* Kernel timing with CUDA events on the context stream: when enabled, one event pair
- * brackets every batch of consecutive iteration-kernel launches, another every round
- * update. msa_get_timing returns totals since the last msa_set_timing(ctx, 1). */
+ * brackets every batch of consecutive iterations, another every round update.
+ * msa_get_timing returns totals since the last msa_set_timing(ctx, 1); iter_launches counts
+ * iterations (in rows mode an iteration is an interior and two boundary launches, and the
+ * bracket includes the wait for the overlapped halo exchange). */
 int msa_set_timing(msa_ctx* ctx, int enable);
 int msa_get_timing(msa_ctx* ctx, double* iter_ms, int64_t* iter_launches, double* round_ms,
                    int64_t* round_launches);

@@ -501,7 +501,6 @@ int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int 
   }
   if (e != cudaSuccess) return set_err(MSA_ECUDA, "iteration kernel launch: %s", cudaGetErrorString(e));
   ++x->launches;
-  if (x->timing) ++x->iter_launches_t;
   return MSA_OK;
 }
 
@@ -555,6 +554,7 @@ int do_steps(msa_ctx* x, int64_t n) {
     } else {
       if ((rc = launch_k1(x, x->g, KC, s, o)) != MSA_OK) return rc;
     }
+    if (x->timing) ++x->iter_launches_t;  // iterations timed (a split iteration is three launches)
     x->cur = o;
     ++x->iters_done;
     if (x->iters_done % K == 0) {
