@@ -39,7 +39,7 @@ def build(force: bool = False) -> str:
 class _Params(ctypes.Structure):
     _fields_ = [("height", ctypes.c_int32), ("width", ctypes.c_int32), ("channels", ctypes.c_int32),
                 ("radius", ctypes.c_int32), ("kernel", ctypes.c_int32), ("iters_per_round", ctypes.c_int32),
-                ("rounds", ctypes.c_int32), ("pad_", ctypes.c_int32)] + [
+                ("rounds", ctypes.c_int32), ("scheme", ctypes.c_int32)] + [
         (n, ctypes.c_double) for n in ("hx", "hy", "alpha", "beta", "eps_x", "eps_c", "dt", "rho", "gamma",
                                        "kappa", "tau", "sigma", "theta")]
 
@@ -66,11 +66,12 @@ class Params:
     tau: float = 0.0
     sigma: float = 0.0
     theta: float = 1.0
+    scheme: int = 0  # 0: CP iterations + multiplier rounds; 1: single-loop linearised ADMM (NEXT-2)
 
     def c(self) -> _Params:
         d = asdict(self)
         return _Params(**{k: d[k] for k in ("height", "width", "channels", "radius", "kernel", "iters_per_round",
-                                            "rounds")}, pad_=0,
+                                            "rounds", "scheme")},
                        **{k: float(d[k]) for k in ("hx", "hy", "alpha", "beta", "eps_x", "eps_c", "dt", "rho",
                                                    "gamma", "kappa", "tau", "sigma", "theta")})
 
@@ -79,7 +80,8 @@ class Params:
         return Params(height=H, width=W, channels=C, radius=sp["radius"], kernel=sp["kernel"],
                       iters_per_round=sp["iters_per_round"], rounds=sp["rounds"], alpha=sp["alpha"],
                       beta=sp["beta"], eps_x=sp["eps_x"], eps_c=sp["eps_c"], dt=sp["dt"], rho=sp["rho"],
-                      gamma=sp["gamma"], kappa=sp["kappa"], tau=sp["tau"], sigma=sp["sigma"], theta=sp["theta"])
+                      gamma=sp["gamma"], kappa=sp["kappa"], tau=sp["tau"], sigma=sp["sigma"], theta=sp["theta"],
+                      scheme=sp.get("scheme", 0))
 
 
 _D = ctypes.c_void_p
@@ -103,6 +105,8 @@ def _load():
             "mo_iteration": ([P, ctypes.c_double, _D, _D, _D, _D, _D], None),
             "mo_round_stats": ([P, ctypes.c_double, _D, _D, _D, _D, _D], None),
             "mo_round_update": ([P, ctypes.c_double, _D, _D], None),
+            "mo_iteration_lin": ([P, ctypes.c_double, _D, _D, _D], None),
+            "mo_round_stats_lin": ([P, ctypes.c_double, _D, _D, _D, _D], None),
             "mo_run": ([P, _D, _D, _D, _D, _D, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(ctypes.c_double), _D,
                         ctypes.c_int32], ctypes.c_int),
             "mo_energy_K": ([P, _D, _D], ctypes.c_double),
@@ -132,7 +136,7 @@ def derive(p: Params) -> Params:
     out = _Params()
     if _load().mo_derive(ctypes.byref(p.c()), ctypes.byref(out)) != 0:
         raise ValueError(f"invalid oracle params {p}")
-    d = {f[0]: getattr(out, f[0]) for f in _Params._fields_ if f[0] != "pad_"}
+    d = {f[0]: getattr(out, f[0]) for f in _Params._fields_}
     return Params(**d)
 
 

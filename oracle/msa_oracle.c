@@ -46,6 +46,13 @@ int mo_derive(const mo_params* in, mo_params* out) {
     out->eps_x = 2.0 / (Rh * Rh);
   }
   double L = sqrt(4.0 / (out->hx * out->hx) + 4.0 / (out->hy * out->hy));            /* ||grad|| <= L */
+  if (in->scheme != 0 && in->scheme != 1) return -1;
+  if (in->scheme == 1) {
+    /* single-loop linearised ADMM: the primal step needs tau rho L^2 < 1; rho must not grow */
+    if (in->kappa > 1.0) return -1;
+    if (out->tau <= 0) out->tau = 0.99 / (in->rho * L * L);
+    if (out->tau * in->rho * L * L >= 1.0) return -1;
+  }
   if (out->tau <= 0) out->tau = 0.99 / L;                                             /* R7 */
   if (out->sigma <= 0) out->sigma = 0.99 / L;
   if (out->theta < 0) out->theta = 1.0;
@@ -294,6 +301,74 @@ void mo_round_update(const mo_params* prm, double rho, const double* c, double* 
   free(g); free(v);
 }
 
+
+/* ------------------------------------------- single-loop linearised ADMM (NEXT-2)
+ *
+ * Alg. 2 with its u-step replaced by ONE linearised proximal step and the
+ * multiplier updated every iteration, gamma = rho (rho = gamma), in the order
+ * v, mu, u:
+ *   c_half = c + dt F(c)                                           (step 1, as in mo_iteration)
+ *   v      = S_{beta/rho}(grad c - mu/rho)                         (eq:soft_threshold)
+ *   mu+    = mu + rho (v - grad c) = Pi_beta(mu - rho grad c)      (Alg. 2 line 7; P12 identity)
+ *   c+     = prox_{tau alpha/2 |. - I|^2}( c_half - tau L~'(c) )   with the smooth part of
+ *            L~'(u) = div(mu + rho v - rho grad u) (eq:new_adjoint) = div(2 mu+ - mu):
+ *   c+     = c_half + (-tau div(2 mu+ - mu) + tau alpha (I - c_half)) / (1 + tau alpha)
+ * With dt = 0 this is the Chambolle-Pock iteration for min_u alpha/2 |u - I|^2 + beta TV(u) with
+ * dual variable p = -mu, sigma = rho and the extrapolation on the dual side, so it converges for
+ * tau rho |grad|^2 < 1 to the ROF minimiser (pinned in tests). State: c, mu (no cbar, no p). */
+void mo_iteration_lin(const mo_params* prm, double rho, const double* I, double* c, double* mu) {
+  const int H = prm->height, W = prm->width, C = prm->channels;
+  const size_t n1 = (size_t)H * W * C, n2 = 2 * n1;
+  const double dt = prm->dt, tau = prm->tau, alpha = prm->alpha;
+  double* F = (double*)malloc(n1 * sizeof(double));
+  double* g = (double*)malloc(n2 * sizeof(double));
+  double* mb = (double*)malloc(n2 * sizeof(double));
+  double* d = (double*)malloc(n1 * sizeof(double));
+  mo_agent_rhs(prm, c, F);
+  mo_grad(c, g, H, W, C, prm->hx, prm->hy);
+  for (size_t n = 0; n < (size_t)H * W; ++n) {
+    double q[128];
+    for (int m = 0; m < 2 * C; ++m) q[m] = mu[n * 2 * C + m] - rho * g[n * 2 * C + m];
+    project_ball(q, 2 * C, prm->beta);
+    for (int m = 0; m < 2 * C; ++m) {
+      const size_t e = n * 2 * C + m;
+      mb[e] = 2.0 * q[m] - mu[e];
+      mu[e] = q[m];
+    }
+  }
+  mo_div(mb, d, H, W, C, prm->hx, prm->hy);
+  for (size_t q = 0; q < n1; ++q) {
+    const double chalf = c[q] + dt * F[q];
+    c[q] = chalf + (-tau * d[q] + tau * alpha * (I[q] - chalf)) / (1.0 + tau * alpha);
+  }
+  free(F); free(g); free(mb); free(d);
+}
+
+/* Round record of the single-loop scheme (the round only records; mu moves every iteration):
+ *   E_TV, E_fid as in mo_round_stats;  P = E_TV + E_fid  (the ROF energy K, eq:cost_TV)
+ *   D = -<I, div p> - ||div p||^2/(2 alpha) with p = -mu  (ROF dual; |p| <= beta holds, so D <= P)
+ *   gap = P - D >= 0;  res = ||v - grad c||_w, v = S_{beta/rho}(grad c - mu/rho) (= |mu+ - mu|/rho) */
+void mo_round_stats_lin(const mo_params* prm, double rho, const double* I, const double* c, const double* mu,
+                        double* stats) {
+  const int H = prm->height, W = prm->width, C = prm->channels;
+  const size_t npx = (size_t)H * W, n2 = npx * 2 * C;
+  const double w = prm->hx * prm->hy, alpha = prm->alpha;
+  double* p = (double*)malloc(n2 * sizeof(double));
+  for (size_t e = 0; e < n2; ++e) p[e] = -mu[e];
+  mo_round_stats(prm, rho, I, c, p, mu, stats);  /* E_TV, E_fid, res, mean, nonfinite as defined there */
+  double* dv = (double*)malloc(npx * C * sizeof(double));
+  mo_div(p, dv, H, W, C, prm->hx, prm->hy);
+  double idp = 0, dp2 = 0;
+  for (size_t e = 0; e < npx * C; ++e) {
+    idp += I[e] * dv[e];
+    dp2 += dv[e] * dv[e];
+  }
+  stats[MO_STAT_P] = stats[MO_STAT_ETV] + stats[MO_STAT_EFID];
+  stats[MO_STAT_D] = alpha > 0 ? -w * idp - w * dp2 / (2.0 * alpha) : NAN;
+  stats[MO_STAT_GAP] = stats[MO_STAT_P] - stats[MO_STAT_D];
+  free(p); free(dv);
+}
+
 /* Runs n_iters iterations starting at global iteration iter0. After every iteration that
  * completes a round ((iter+1) % K == 0) it records the stats with the pre-update mu, applies
  * the multiplier update and rho <- kappa rho (R8, R9). Returns the number of rounds recorded
@@ -306,6 +381,15 @@ int mo_run(const mo_params* prm_in, const double* I, double* c, double* cbar, do
   double rho = *rho_inout;
   int nr = 0;
   for (int64_t it = iter0; it < iter0 + n_iters; ++it) {
+    if (prm.scheme == 1) {  /* NEXT-2: mu moves every iteration; a round only records (cbar, p unused) */
+      mo_iteration_lin(&prm, rho, I, c, mu);
+      if ((it + 1) % prm.iters_per_round == 0) {
+        if (stats && nr < stats_cap) mo_round_stats_lin(&prm, rho, I, c, mu, stats + (size_t)nr * MO_NSTAT(C));
+        ++nr;
+        rho = prm.kappa * rho;
+      }
+      continue;
+    }
     mo_iteration(&prm, rho, I, c, cbar, p, mu);
     if ((it + 1) % prm.iters_per_round == 0) {
       if (stats && nr < stats_cap) mo_round_stats(&prm, rho, I, c, p, mu, stats + (size_t)nr * MO_NSTAT(C));

@@ -27,7 +27,8 @@ typedef struct {
   int32_t kernel;           /* 0 = standard Wendland (4r+1)(1-r)^4, 1 = as printed (4r-1)(1-r)^4 (R3) */
   int32_t iters_per_round;  /* K (reading R8) */
   int32_t rounds;
-  int32_t pad_;
+  int32_t scheme;           /* 0: CP iterations + multiplier rounds (Alg. 2, reading R1);
+                               1: single-loop linearised ADMM (see mo_iteration_lin) */
   double hx, hy;            /* grid spacing; <= 0 -> 1/(W-1), 1/(H-1) (1 if the size is 1)  (R5) */
   double alpha, beta;       /* fidelity weight (eq:cost_TV), TV weight (R27) */
   double eps_x, eps_c;      /* eq:ellipsoid controls; eps_x <= 0 -> 2/(R*min(hx,hy))^2 (R2) */
@@ -55,6 +56,9 @@ void mo_iteration(const mo_params* prm, double rho, const double* I, double* c, 
 void mo_round_stats(const mo_params* prm, double rho, const double* I, const double* c, const double* p,
                     const double* mu, double* stats);
 void mo_round_update(const mo_params* prm, double rho, const double* c, double* mu);
+void mo_iteration_lin(const mo_params* prm, double rho, const double* I, double* c, double* mu);
+void mo_round_stats_lin(const mo_params* prm, double rho, const double* I, const double* c, const double* mu,
+                        double* stats);
 int mo_run(const mo_params* prm, const double* I, double* c, double* cbar, double* p, double* mu,
            int64_t iter0, int64_t n_iters, double* rho_inout, double* stats, int32_t stats_cap);
 
