@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define MSA_ABI_VERSION 1
+#define MSA_ABI_VERSION 2 /* 2: msa_params.scheme */
 
 enum {
   MSA_OK = 0,
@@ -55,6 +55,21 @@ enum {
 enum { MSA_SHARD_NONE = 0, MSA_SHARD_ROWS = 1, MSA_SHARD_BATCH = 2 };
 enum { MSA_FIELD_C = 0, MSA_FIELD_CBAR = 1, MSA_FIELD_P = 2, MSA_FIELD_MU = 3, MSA_FIELD_I = 4 };
 enum { MSA_KERNEL_WENDLAND = 0, MSA_KERNEL_PRINTED = 1 };
+/* Iteration scheme.
+ *  MSA_SCHEME_CP_ROUNDS (0): the steps above - Chambolle-Pock iterations on L~(.; mu) with the
+ *    multiplier update every K iterations (Alg. 2 with the fused iteration of reading R1).
+ *  MSA_SCHEME_LINEARISED_ADMM (1): SURVEY §8(f) NEXT-2 - Alg. 2 with gamma = rho, the multiplier
+ *    updated EVERY iteration and the u-step replaced by one linearised proximal step, in the
+ *    order v, mu, u:  c_half = c + dt F(c);  mu+ = Pi_beta(mu - rho grad c)  (= mu + rho (v - grad c),
+ *    v = S_{beta/rho}(grad c - mu/rho), eq:soft_threshold, Alg. 2 line 7);
+ *    c+ = c_half + (-tau div(2 mu+ - mu) + tau alpha (I - c_half)) / (1 + tau alpha)
+ *    (div(mu + rho v - rho grad u) of eq:new_adjoint at the updated mu, v). State c, mu only:
+ *    7 C floats of traffic per pixel-iteration instead of 11 C. Needs gamma = rho (the value of
+ *    gamma is ignored), kappa <= 1 and tau rho L^2 < 1 (tau <= 0 -> 0.99 / (rho L^2)). Rounds
+ *    only record statistics: P = E_TV + E_fid (the ROF energy), D = the ROF dual value of
+ *    p = -mu, gap = P - D >= 0, al_residual = |v - grad c|. mu is stored in the p buffers:
+ *    MSA_FIELD_MU and MSA_FIELD_P both address it; MSA_FIELD_CBAR is unused. */
+enum { MSA_SCHEME_CP_ROUNDS = 0, MSA_SCHEME_LINEARISED_ADMM = 1 };
 
 /* All real quantities in the paper's normalised units: Omega = [0,1]^2,
  * pixel spacing h_x = 1/(W-1), h_y = 1/(H-1) (1 for a size-1 axis; reading R5). */
@@ -76,6 +91,7 @@ typedef struct {
   int32_t rounds;          /* multiplier rounds per msa_solve call (>= 0) */
   int32_t shard, rank, world, device; /* MSA_SHARD_*, this rank, number of ranks, CUDA device */
   const void* nccl_id;     /* 128-byte ncclUniqueId (from rank 0's msa_nccl_unique_id) when world > 1 */
+  int32_t scheme;          /* MSA_SCHEME_* (ABI 2) */
 } msa_params;
 
 /* One record per multiplier round, reduced over the rank's images (batch mode: per rank;

@@ -22,6 +22,7 @@ MSA_OK, MSA_EINVAL, MSA_ENOMEM, MSA_ECUDA, MSA_ENCCL, MSA_EDIVERGED, MSA_ESTATE 
 SHARD_NONE, SHARD_ROWS, SHARD_BATCH = 0, 1, 2
 FIELD_C, FIELD_CBAR, FIELD_P, FIELD_MU, FIELD_I = 0, 1, 2, 3, 4
 KERNEL_WENDLAND, KERNEL_PRINTED = 0, 1
+SCHEME_CP_ROUNDS, SCHEME_LINEARISED_ADMM = 0, 1
 
 # every symbol include/msa.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["msa_abi_version", "msa_last_error", "msa_workspace_bytes", "msa_partition_rows",
@@ -44,7 +45,8 @@ class _CParams(ctypes.Structure):
                 ("gamma", ctypes.c_double), ("kappa", ctypes.c_double), ("tau", ctypes.c_double),
                 ("sigma", ctypes.c_double), ("theta", ctypes.c_double), ("iters_per_round", ctypes.c_int32),
                 ("rounds", ctypes.c_int32), ("shard", ctypes.c_int32), ("rank", ctypes.c_int32),
-                ("world", ctypes.c_int32), ("device", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
+                ("world", ctypes.c_int32), ("device", ctypes.c_int32), ("nccl_id", ctypes.c_void_p),
+                ("scheme", ctypes.c_int32)]
 
 
 class RoundStats(ctypes.Structure):
@@ -95,11 +97,14 @@ class Params:
     world: int = 1
     device: int = 0
     nccl_id: bytes | None = field(default=None, repr=False)
+    scheme: int = SCHEME_CP_ROUNDS
 
     @staticmethod
     def from_solver(B: int, H: int, W: int, C: int, sp: dict, **kw) -> "Params":
         keys = ("alpha", "beta", "radius", "kernel", "eps_x", "eps_c", "dt", "rho", "gamma", "kappa", "tau",
                 "sigma", "theta", "iters_per_round", "rounds")
+        if "scheme" in sp and "scheme" not in kw:
+            kw = dict(kw, scheme=sp["scheme"])
         return Params(batch=B, height=H, width=W, channels=C, **{k: sp[k] for k in keys}, **kw)
 
     def c(self) -> tuple[_CParams, object]:

@@ -44,6 +44,7 @@ struct MsaIterConsts {
   float b_rs;       // sigma / (rho + sigma)
   float beta, beta2;
   float tau, tau_alpha, inv_1ta, theta;  // step 3 (R7, R21)
+  float rho;        // single-loop scheme (NEXT-2): mu+ = Pi_beta(mu - rho grad c)
 };
 
 // phi as a function of t = max(1 - r, 0) (eq:kernel PAPER.md:259-267; R3, R21):
@@ -90,6 +91,29 @@ __device__ __forceinline__ void msa_dual_step(const MsaIterConsts& K, const floa
   }
   // beta / |q| via the hardware reciprocal square root (R21: allowed since parity holds).
   // Branch-free: inside the ball f = 1 and q * 1 = q exactly.
+  const float f = n2 > K.beta2 ? __fmul_rn(K.beta, rsqrtf(n2)) : 1.0f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    qx[k] = __fmul_rn(qx[k], f);
+    qy[k] = __fmul_rn(qy[k], f);
+  }
+}
+
+// Single-loop linearised ADMM (msa.h MSA_SCHEME_LINEARISED_ADMM), one pixel:
+// mu+ = Pi_beta(mu - rho grad c) over the whole 2C-vector (v-step + multiplier step with gamma = rho),
+// then the dual extrapolation mb = 2 mu+ - mu used by the primal step's divergence.
+template <int C>
+__device__ __forceinline__ void msa_lin_dual(const MsaIterConsts& K, const float (&gx)[C], const float (&gy)[C],
+                                             const float (&mx)[C], const float (&my)[C], float (&qx)[C],
+                                             float (&qy)[C]) {
+  float n2 = 0.0f;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    qx[k] = __fmaf_rn(-K.rho, gx[k], mx[k]);
+    qy[k] = __fmaf_rn(-K.rho, gy[k], my[k]);
+    n2 = __fmaf_rn(qx[k], qx[k], n2);
+    n2 = __fmaf_rn(qy[k], qy[k], n2);
+  }
   const float f = n2 > K.beta2 ? __fmul_rn(K.beta, rsqrtf(n2)) : 1.0f;
 #pragma unroll
   for (int k = 0; k < C; ++k) {

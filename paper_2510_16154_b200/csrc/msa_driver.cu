@@ -161,6 +161,10 @@ int validate(const msa_params* p) {
     if (!p->nccl_id) return set_err(MSA_EINVAL, "rows mode with world > 1 needs nccl_id");
   }
   if (p->device < 0) return set_err(MSA_EINVAL, "device must be >= 0");
+  if (p->scheme != MSA_SCHEME_CP_ROUNDS && p->scheme != MSA_SCHEME_LINEARISED_ADMM)
+    return set_err(MSA_EINVAL, "scheme must be MSA_SCHEME_CP_ROUNDS or MSA_SCHEME_LINEARISED_ADMM");
+  if (p->scheme == MSA_SCHEME_LINEARISED_ADMM && p->kappa > 1.0)
+    return set_err(MSA_EINVAL, "the linearised scheme needs kappa <= 1 (tau rho L^2 < 1 must keep holding)");
   return MSA_OK;
 }
 
@@ -177,10 +181,17 @@ int derive(const msa_params* p, Derived* d) {
   const double Rh = (p->radius > 0 ? p->radius : 1) * h;
   d->eps_x = p->eps_x > 0 ? p->eps_x : 2.0 / (Rh * Rh);         // R2
   const double L = sqrt(4.0 / (d->hx * d->hx) + 4.0 / (d->hy * d->hy));
-  d->tau = p->tau > 0 ? p->tau : 0.99 / L;                         // R7
-  d->sigma = p->sigma > 0 ? p->sigma : 0.99 / L;
-  d->theta = p->theta >= 0 ? p->theta : 1.0;
-  if (d->tau * d->sigma * L * L >= 1.0) return set_err(MSA_EINVAL, "tau*sigma*L^2 must be < 1 (L^2 = 4/hx^2+4/hy^2)");
+  if (p->scheme == MSA_SCHEME_LINEARISED_ADMM) {  // the dual step is sigma = rho: tau rho L^2 < 1
+    d->tau = p->tau > 0 ? p->tau : 0.99 / (p->rho * L * L);
+    d->sigma = p->rho;
+    d->theta = 0.0;
+    if (d->tau * p->rho * L * L >= 1.0) return set_err(MSA_EINVAL, "tau*rho*L^2 must be < 1 (L^2 = 4/hx^2+4/hy^2)");
+  } else {
+    d->tau = p->tau > 0 ? p->tau : 0.99 / L;                       // R7
+    d->sigma = p->sigma > 0 ? p->sigma : 0.99 / L;
+    d->theta = p->theta >= 0 ? p->theta : 1.0;
+    if (d->tau * d->sigma * L * L >= 1.0) return set_err(MSA_EINVAL, "tau*sigma*L^2 must be < 1 (L^2 = 4/hx^2+4/hy^2)");
+  }
   const int R = p->radius;
   d->NR = 0;
   d->T.n = 0;
@@ -275,6 +286,7 @@ MsaIterConsts iter_consts(const msa_ctx* x, double rho) {
   K.tau_alpha = (float)(x->tau * p.alpha);
   K.inv_1ta = (float)(1.0 / (1.0 + x->tau * p.alpha));
   K.theta = (float)x->theta;
+  K.rho = (float)rho;
   return K;
 }
 
@@ -292,7 +304,7 @@ float* field_ptr(msa_ctx* x, int which, int set) {
     case MSA_FIELD_C: return x->c[set];
     case MSA_FIELD_CBAR: return x->cb[set];
     case MSA_FIELD_P: return x->p[set];
-    case MSA_FIELD_MU: return x->mu;
+    case MSA_FIELD_MU: return x->prm.scheme == MSA_SCHEME_LINEARISED_ADMM ? x->p[set] : x->mu;
     case MSA_FIELD_I: return x->I;
   }
   return nullptr;
@@ -426,7 +438,10 @@ int do_round(msa_ctx* x) {
   R.beta = P.beta;
   R.alpha = P.alpha;
   int nblk = 0;
-  CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->mu, x->I, x->mu, x->partials, &nblk, x->stream));
+  if (P.scheme == MSA_SCHEME_LINEARISED_ADMM)  // statistics only (mu moves every iteration); p := mu
+    CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->p[s], x->I, nullptr, x->partials, &nblk, x->stream));
+  else
+    CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->mu, x->I, x->mu, x->partials, &nblk, x->stream));
   CUDA_TRY(msa_launch_reduce(x->partials, x->g.nb, nblk, x->sums, x->stream));
   x->launches += 2;
   if (P.world > 1 && P.shard == MSA_SHARD_ROWS)
@@ -446,6 +461,7 @@ int do_round(msa_ctx* x) {
   a.round = x->rounds_done;
   a.images = x->g.nb;
   a.iters = x->iters_done;
+  a.lin = P.scheme == MSA_SCHEME_LINEARISED_ADMM ? 1 : 0;
   CUDA_TRY(msa_launch_record(x->sums, a, x->d_rec + x->rec_pending, x->stream));
   x->launches += 1;
   if (x->timing) {
@@ -480,6 +496,13 @@ int k1_variant() {
 // the variant cascade sweep (opt-in) -> tiled C = 3 -> C = 16 -> generic.
 int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int o) {
   const msa_params& P = x->prm;
+  if (P.scheme == MSA_SCHEME_LINEARISED_ADMM) {  // mu lives in the p ping-pong buffers
+    cudaError_t e = msa_launch_iter_lin_generic(g, KC, x->d_off, x->d_om, x->c[s], x->p[s], x->I, x->c[o], x->p[o],
+                                                x->stream);
+    if (e != cudaSuccess) return set_err(MSA_ECUDA, "linearised iteration kernel: %s", cudaGetErrorString(e));
+    ++x->launches;
+    return MSA_OK;
+  }
   int launched = 0;
   cudaError_t e = cudaErrorNotSupported;
   if (k1_variant() == K1_SWEEP)

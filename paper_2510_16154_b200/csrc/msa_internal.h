@@ -17,6 +17,12 @@ cudaError_t msa_launch_iter_generic(const MsaGeom& g, const MsaIterConsts& K, co
                                     const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                     float* c_out, float* cb_out, float* p_out, cudaStream_t s);
 
+// Single-loop linearised ADMM iteration (msa.h MSA_SCHEME_LINEARISED_ADMM), any C: reads c, mu, I,
+// writes c_out, mu_out.
+cudaError_t msa_launch_iter_lin_generic(const MsaGeom& g, const MsaIterConsts& K, const int2* d_off,
+                                        const float* d_om, const float* c, const float* mu, const float* I,
+                                        float* c_out, float* mu_out, cudaStream_t s);
+
 // Specialised fused iteration (msa_iter_fast.cu). Returns cudaErrorNotSupported (without
 // launching) when no specialisation covers (C, R, kernel, offset set).
 cudaError_t msa_launch_iter_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
@@ -47,6 +53,7 @@ cudaError_t msa_launch_reduce(const double* partials, int nb, int nblk, double* 
 struct MsaRecordArgs {
   double w, beta, alpha, rho, npx;
   int C, round, images;
+  int lin;  // single-loop scheme record (ROF primal / dual of p = -mu)
   long long iters;
 };
 // sums[MSA_NSUM] -> one msa_round_stats record (device).

@@ -101,6 +101,101 @@ cudaError_t launch_iter_generic_c(const MsaGeom& g, const MsaIterConsts& K, cons
   return cudaGetLastError();
 }
 
+
+// ------------------------------------------------------------------ K1 generic, single-loop scheme
+// (msa.h MSA_SCHEME_LINEARISED_ADMM): c_half as in k_iter_generic; mu+ =
+// Pi_beta(mu - rho grad c) at (i,j), (i-1,j), (i,j-1) (the last two only feed the divergence);
+// c+ = c_half + (-tau div(2 mu+ - mu) + tau alpha (I - c_half)) / (1 + tau alpha). mu ping-pongs
+// between mu (in) and mu_out.
+template <int C, int KER>
+__global__ void __launch_bounds__(256) k_iter_lin_generic(MsaGeom g, MsaIterConsts K, const int2* __restrict__ off,
+                                                          const float* __restrict__ om, const float* __restrict__ c,
+                                                          const float* __restrict__ mu, const float* __restrict__ I,
+                                                          float* __restrict__ c_out, float* __restrict__ mu_out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = g.k1_lo + blockIdx.y * blockDim.y + threadIdx.y;
+  const int b = blockIdx.z;
+  if (i >= g.W || jl >= msa_k1_hi(g)) return;
+  const int j = g.row0 + jl;
+  const int W = g.W, H = g.H;
+  float ci[C], acc[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    ci[k] = c[msa_idx(g, b, k, C, j, i)];
+    acc[k] = 0.0f;
+  }
+  for (int o = 0; o < K.n_off; ++o) {
+    const int2 d = off[o];
+    const int ii = i + d.x, jj = j + d.y;
+    if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;  // excluded, not padded (R20)
+    float cj[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) cj[k] = c[msa_idx(g, b, k, C, jj, ii)];
+    msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
+  }
+  float chalf[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+  float mbx[3][C], mby[3][C], qx0[C], qy0[C];
+  const int pi[3] = {i, i - 1, i};
+  const int pj[3] = {j, j, j - 1};
+#pragma unroll
+  for (int s = 0; s < 3; ++s) {
+    const int a = pi[s], bj = pj[s];
+    if (a < 0 || bj < 0) {
+#pragma unroll
+      for (int k = 0; k < C; ++k) mbx[s][k] = mby[s][k] = 0.0f;
+      continue;
+    }
+    float gx[C], gy[C], mx[C], my[C], qx[C], qy[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const float c0 = c[msa_idx(g, b, k, C, bj, a)];
+      gx[k] = a < W - 1 ? __fmul_rn(__fsub_rn(c[msa_idx(g, b, k, C, bj, a + 1)], c0), K.inv_hx) : 0.0f;
+      gy[k] = bj < H - 1 ? __fmul_rn(__fsub_rn(c[msa_idx(g, b, k, C, bj + 1, a)], c0), K.inv_hy) : 0.0f;
+      mx[k] = mu[msa_idx(g, b, k, 2 * C, bj, a)];
+      my[k] = mu[msa_idx(g, b, C + k, 2 * C, bj, a)];
+    }
+    msa_lin_dual<C>(K, gx, gy, mx, my, qx, qy);
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      mbx[s][k] = __fmaf_rn(2.0f, qx[k], -mx[k]);  // 2 mu+ - mu (2 mu+ is exact: one rounding)
+      mby[s][k] = __fmaf_rn(2.0f, qy[k], -my[k]);
+      if (s == 0) {
+        qx0[k] = qx[k];
+        qy0[k] = qy[k];
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    float ax = i < W - 1 ? mbx[0][k] : 0.0f;
+    if (i > 0) ax = __fsub_rn(ax, mbx[1][k]);
+    float ay = j < H - 1 ? mby[0][k] : 0.0f;
+    if (j > 0) ay = __fsub_rn(ay, mby[2][k]);
+    const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
+    float cp, cbp;
+    msa_prox_extrap(K, chalf[k], -d, I[msa_idx(g, b, k, C, j, i)], cp, cbp);  // -tau div(2 mu+ - mu)
+    c_out[msa_idx(g, b, k, C, j, i)] = cp;
+    mu_out[msa_idx(g, b, k, 2 * C, j, i)] = qx0[k];
+    mu_out[msa_idx(g, b, C + k, 2 * C, j, i)] = qy0[k];
+  }
+}
+
+template <int C>
+cudaError_t launch_iter_lin_generic_c(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
+                                      const float* c, const float* mu, const float* I, float* co, float* muo,
+                                      cudaStream_t s) {
+  const int nr = msa_k1_hi(g) - g.k1_lo;
+  if (nr <= 0) return cudaSuccess;
+  dim3 blk(32, 8), grd((g.W + 31) / 32, (nr + 7) / 8, g.nb);
+  if (K.kernel == 0)
+    k_iter_lin_generic<C, 0><<<grd, blk, 0, s>>>(g, K, off, om, c, mu, I, co, muo);
+  else
+    k_iter_lin_generic<C, 1><<<grd, blk, 0, s>>>(g, K, off, om, c, mu, I, co, muo);
+  return cudaGetLastError();
+}
+
 // ------------------------------------------------------------------ K2 round
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
@@ -162,7 +257,7 @@ __global__ void __launch_bounds__(256) k_round(MsaGeom g, MsaRoundConsts R, cons
       const float v = __fmul_rn(f, a[m]);
       const float vg = __fsub_rn(v, gv[m]);
       res += (double)vg * (double)vg;
-      mu_out[msa_idx(g, b, m, 2 * C, j, i)] = __fmaf_rn(R.gamma, vg, mv[m]);
+      if (mu_out) mu_out[msa_idx(g, b, m, 2 * C, j, i)] = __fmaf_rn(R.gamma, vg, mv[m]);  // null: stats only
     }
     acc[MSA_S_RES] += res;
     acc[MSA_S_TV] += sqrt((double)g2);
@@ -213,10 +308,16 @@ __global__ void k_record(const double* __restrict__ S, MsaRecordArgs a, msa_roun
   r.iters = a.iters;
   r.e_tv = a.w * a.beta * S[MSA_S_TV];
   r.e_fid = 0.5 * a.alpha * a.w * S[MSA_S_FID];
-  r.primal = a.w * S[MSA_S_HUB] + r.e_fid;
-  r.dual = a.alpha > 0 ? -a.w * S[MSA_S_IDP] - a.w * S[MSA_S_DP2] / (2.0 * a.alpha) - a.w * S[MSA_S_MUP] / a.rho -
-                             a.w * S[MSA_S_PP] / (2.0 * a.rho)
-                       : __longlong_as_double(0x7ff8000000000000ULL);
+  if (a.lin) {  // single-loop scheme: ROF primal K, ROF dual of p = -mu (the sums were taken with p := mu)
+    r.primal = r.e_tv + r.e_fid;
+    r.dual = a.alpha > 0 ? a.w * S[MSA_S_IDP] - a.w * S[MSA_S_DP2] / (2.0 * a.alpha)
+                         : __longlong_as_double(0x7ff8000000000000ULL);
+  } else {
+    r.primal = a.w * S[MSA_S_HUB] + r.e_fid;
+    r.dual = a.alpha > 0 ? -a.w * S[MSA_S_IDP] - a.w * S[MSA_S_DP2] / (2.0 * a.alpha) - a.w * S[MSA_S_MUP] / a.rho -
+                               a.w * S[MSA_S_PP] / (2.0 * a.rho)
+                         : __longlong_as_double(0x7ff8000000000000ULL);
+  }
   r.gap = r.primal - r.dual;
   r.al_residual = sqrt(a.w * S[MSA_S_RES]);
   r.rho = a.rho;
@@ -250,6 +351,21 @@ __global__ void k_unpack(MsaGeom g, int nm, const float* __restrict__ inter, flo
 }
 
 }  // namespace
+
+cudaError_t msa_launch_iter_lin_generic(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
+                                        const float* c, const float* mu, const float* I, float* co, float* muo,
+                                        cudaStream_t s) {
+  switch (g.C) {
+#define MSA_CASE_L(CC) \
+  case CC:             \
+    return launch_iter_lin_generic_c<CC>(g, K, off, om, c, mu, I, co, muo, s);
+    MSA_CASE_L(1) MSA_CASE_L(2) MSA_CASE_L(3) MSA_CASE_L(4) MSA_CASE_L(5) MSA_CASE_L(6) MSA_CASE_L(7) MSA_CASE_L(8)
+    MSA_CASE_L(9) MSA_CASE_L(10) MSA_CASE_L(11) MSA_CASE_L(12) MSA_CASE_L(13) MSA_CASE_L(14) MSA_CASE_L(15)
+    MSA_CASE_L(16)
+#undef MSA_CASE_L
+    default: return cudaErrorInvalidValue;
+  }
+}
 
 cudaError_t msa_launch_iter_generic(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
                                     const float* c, const float* cb, const float* p, const float* mu, const float* I,

@@ -38,7 +38,7 @@ def test_library_is_sm100a():
 
 
 def test_abi_version(lib):
-    assert lib.msa_abi_version() == 1
+    assert lib.msa_abi_version() == 2
 
 
 def _params(**kw):
