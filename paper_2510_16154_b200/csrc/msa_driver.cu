@@ -497,8 +497,15 @@ int k1_variant() {
 int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int o) {
   const msa_params& P = x->prm;
   if (P.scheme == MSA_SCHEME_LINEARISED_ADMM) {  // mu lives in the p ping-pong buffers
-    cudaError_t e = msa_launch_iter_lin_generic(g, KC, x->d_off, x->d_om, x->c[s], x->p[s], x->I, x->c[o], x->p[o],
-                                                x->stream);
+    int ok = 0;
+    cudaError_t e = cudaErrorNotSupported;
+    if (k1_variant() != K1_GENERIC)
+      e = msa_launch_iter_fast_lin(g, KC, x->T, P.radius, x->c[s], x->p[s], x->I, x->c[o], x->p[o], x->stream, &ok);
+    if (!ok && e != cudaErrorNotSupported && e != cudaSuccess)
+      return set_err(MSA_ECUDA, "linearised tiled kernel: %s", cudaGetErrorString(e));
+    if (!ok)
+      e = msa_launch_iter_lin_generic(g, KC, x->d_off, x->d_om, x->c[s], x->p[s], x->I, x->c[o], x->p[o],
+                                      x->stream);
     if (e != cudaSuccess) return set_err(MSA_ECUDA, "linearised iteration kernel: %s", cudaGetErrorString(e));
     ++x->launches;
     return MSA_OK;

@@ -23,6 +23,11 @@ cudaError_t msa_launch_iter_lin_generic(const MsaGeom& g, const MsaIterConsts& K
                                         const float* d_om, const float* c, const float* mu, const float* I,
                                         float* c_out, float* mu_out, cudaStream_t s);
 
+// Tiled C = 3 form of the single-loop scheme (msa_iter_fast.cu, LIN); bitwise equal to the generic one.
+cudaError_t msa_launch_iter_fast_lin(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                                     const float* c, const float* mu, const float* I, float* c_out, float* mu_out,
+                                     cudaStream_t s, int* launched);
+
 // Specialised fused iteration (msa_iter_fast.cu). Returns cudaErrorNotSupported (without
 // launching) when no specialisation covers (C, R, kernel, offset set).
 cudaError_t msa_launch_iter_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,

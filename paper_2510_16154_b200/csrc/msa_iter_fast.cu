@@ -188,7 +188,9 @@ struct Occ {
 #endif
 };
 
-template <int R, int P>
+// LIN = the single-loop linearised ADMM scheme (msa.h MSA_SCHEME_LINEARISED_ADMM): tm.p is mu
+// (in), tm.po mu+ (out); no cbar / mu / cbar+ traffic; the dual step takes grad c from the c tile.
+template <int R, int P, bool LIN>
 __global__ void __launch_bounds__(NT, Occ<P>::blocks)
     k_iter_fast_c3(MsaGeom g, MsaIterConsts K, FastOm om, const __grid_constant__ TmaSet tm) {
   using S = Smem<R, P>;
@@ -219,10 +221,15 @@ __global__ void __launch_bounds__(NT, Occ<P>::blocks)
     const int ys = y0 - g.row0 + g.G;  // stored-row index of global row y0
     mbar_expect_tx(&bars[0], (unsigned)(sizeof(float) * C * SH * SW));
     tma_load3(sc, &tm.c, x0 - SX, ys - R, b * C, &bars[0]);
-    mbar_expect_tx(&bars[1], (unsigned)(sizeof(float) * (C * BH * BW + 4 * C * QH * QW + C * TH * TW)));
-    tma_load3(scb, &tm.cb, x0 - BX, ys - 1, b * C, &bars[1]);
-    tma_load3(spp, &tm.p, x0 - BX, ys - 1, b * 2 * C, &bars[1]);
-    tma_load3(smu, &tm.mu, x0 - BX, ys - 1, b * 2 * C, &bars[1]);
+    if constexpr (LIN) {
+      mbar_expect_tx(&bars[1], (unsigned)(sizeof(float) * (2 * C * QH * QW + C * TH * TW)));
+      tma_load3(spp, &tm.p, x0 - BX, ys - 1, b * 2 * C, &bars[1]);  // mu
+    } else {
+      mbar_expect_tx(&bars[1], (unsigned)(sizeof(float) * (C * BH * BW + 4 * C * QH * QW + C * TH * TW)));
+      tma_load3(scb, &tm.cb, x0 - BX, ys - 1, b * C, &bars[1]);
+      tma_load3(spp, &tm.p, x0 - BX, ys - 1, b * 2 * C, &bars[1]);
+      tma_load3(smu, &tm.mu, x0 - BX, ys - 1, b * 2 * C, &bars[1]);
+    }
     tma_load3(sI, &tm.I, x0, ys, b * C, &bars[1]);
   }
   mbar_wait(&bars[0], 0);
@@ -251,6 +258,73 @@ __global__ void __launch_bounds__(NT, Occ<P>::blocks)
     for (int k = 0; k < C; ++k) upk(fma2(DT, acc[j][k], ci[j][k]), chalf[2 * j][k], chalf[2 * j + 1][k]);
 
   mbar_wait(&bars[1], 0);
+  if constexpr (LIN) {
+    // ---- mu+ = Pi_beta(mu - rho grad c) at (tx, ty) in [-1, 31] x [-1, TH-1]; grad c from the c
+    // tile (read-only here), mu from the mu tile; mb = 2 mu+ - mu -> smu region ([2C][SPH][SPW])
+    float* sb = smu;
+    float qo[P][2 * C];  // mu+ of this thread's own pixels
+    auto lin_at = [&](int tx, int ty, float* own) {
+      const int xx = x0 + tx, yy = y0 + ty;
+      if (xx < 0 || yy < 0 || xx >= W || yy >= H) return;
+      float gx[C], gy[C], mx[C], my[C], qx[C], qy[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const float* ck = sc + (k * SH + ty + R) * SW + SX + tx;
+        const float c0 = ck[0];
+        gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(ck[1], c0), K.inv_hx) : 0.0f;
+        gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(ck[SW], c0), K.inv_hy) : 0.0f;
+        mx[k] = spp[(k * QH + ty + 1) * QW + BX + tx];
+        my[k] = spp[((C + k) * QH + ty + 1) * QW + BX + tx];
+      }
+      msa_lin_dual<C>(K, gx, gy, mx, my, qx, qy);
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        sb[(k * SPH + ty + 1) * SPW + tx + 1] = __fmaf_rn(2.0f, qx[k], -mx[k]);
+        sb[((C + k) * SPH + ty + 1) * SPW + tx + 1] = __fmaf_rn(2.0f, qy[k], -my[k]);
+        if (own) {
+          own[k] = qx[k];
+          own[C + k] = qy[k];
+        }
+      }
+    };
+#pragma unroll
+    for (int r = 0; r < P; ++r) lin_at(lx, strip * P + r, qo[r]);
+    if (strip == 0) lin_at(lx, -1, nullptr);
+    if (strip == 1 && lx < TH) lin_at(-1, lx, nullptr);
+    __syncthreads();  // mb complete; the c and mu tiles are dead
+    float* oc = spp;  // [C][TH][TW] c+
+    float* op = sc;   // [2C][TH][TW] mu+
+    if (x < W) {
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        const int ty = strip * P + r, yy = ybase + r;
+        const int sy = ty + 1, sx = lx + 1;
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          float ax = x < W - 1 ? sb[(k * SPH + sy) * SPW + sx] : 0.0f;
+          if (x > 0) ax = __fsub_rn(ax, sb[(k * SPH + sy) * SPW + sx - 1]);
+          float ay = yy < H - 1 ? sb[((C + k) * SPH + sy) * SPW + sx] : 0.0f;
+          if (yy > 0) ay = __fsub_rn(ay, sb[((C + k) * SPH + sy - 1) * SPW + sx]);
+          const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
+          float cp, cbp;
+          msa_prox_extrap(K, chalf[r][k], -d, sI[(k * TH + ty) * TW + lx], cp, cbp);  // -tau div(2 mu+ - mu)
+          oc[(k * TH + ty) * TW + lx] = cp;
+          op[(k * TH + ty) * TW + lx] = qo[r][k];
+          op[((C + k) * TH + ty) * TW + lx] = qo[r][C + k];
+        }
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const int ys = y0 - g.row0 + g.G;
+      tma_store3(&tm.co, x0, ys, b * C, oc);
+      tma_store3(&tm.po, x0, ys, b * 2 * C, op);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    }
+    return;
+  }
   __syncthreads();  // every warp is done with the c tile (sp reuses it)
 
   // ---- step 2: p+ at tile pixel (tx, ty) (tx in [-1, 31], ty in [-1, TH-1]) -> sp[.][ty+1][tx+1]
@@ -372,7 +446,7 @@ bool get_maps(const MapKey& k, const MsaGeom& g, int SH, int BH, int QH, int TH,
   return true;
 }
 
-template <int R, int P>
+template <int R, int P, bool LIN>
 cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om, const float* c, const float* cb,
                       const float* p, const float* mu, const float* I, float* co, float* cbo, float* po,
                       cudaStream_t s) {
@@ -386,18 +460,18 @@ cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om
   if (!get_maps(key, g, S::SH, S::BH, S::QH, S::TH, &tm)) return cudaErrorNotSupported;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_iter_fast_c3<R, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_iter_fast_c3<R, P, LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   dim3 grd((g.W + TW - 1) / TW, (nr + S::TH - 1) / S::TH, g.nb);
-  k_iter_fast_c3<R, P><<<grd, NT, S::bytes, s>>>(g, K, om, tm);
+  k_iter_fast_c3<R, P, LIN><<<grd, NT, S::bytes, s>>>(g, K, om, tm);
   return cudaGetLastError();
 }
 
-template <int R>
+template <int R, bool LIN>
 cudaError_t launch_c3(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, const float* c,
                       const float* cb, const float* p, const float* mu, const float* I, float* co, float* cbo,
                       float* po, cudaStream_t s) {
@@ -414,15 +488,17 @@ cudaError_t launch_c3(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
     prev = idx;
   }
   static const int rows_per_thread = getenv("MSA_K1_P") ? atoi(getenv("MSA_K1_P")) : 4;  // A/B hook
-  if (rows_per_thread == 4) return launch_rp<R, 4>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
-  return launch_rp<R, 2>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
+  if (rows_per_thread == 4) return launch_rp<R, 4, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
+  return launch_rp<R, 2, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
 }
 
 }  // namespace
 
-cudaError_t msa_launch_iter_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
-                                 const float* c, const float* cb, const float* p, const float* mu, const float* I,
-                                 float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
+namespace {
+template <bool LIN>
+cudaError_t launch_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R, const float* c,
+                        const float* cb, const float* p, const float* mu, const float* I, float* c_out,
+                        float* cb_out, float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
   // test hook: MSA_FORCE_GENERIC=1 selects the generic kernel (bitwise-identical results)
   static const bool force_generic = getenv("MSA_FORCE_GENERIC") != nullptr;
@@ -432,12 +508,26 @@ cudaError_t msa_launch_iter_fast(const MsaGeom& g, const MsaIterConsts& K, const
     if (T.dx[o] * T.dx[o] + T.dy[o] * T.dy[o] >= R * R) return cudaErrorNotSupported;
   cudaError_t e;
   switch (R) {
-    case 2: e = launch_c3<2>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
-    case 3: e = launch_c3<3>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
-    case 4: e = launch_c3<4>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
-    case 5: e = launch_c3<5>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
+    case 2: e = launch_c3<2, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
+    case 3: e = launch_c3<3, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
+    case 4: e = launch_c3<4, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
+    case 5: e = launch_c3<5, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
     default: return cudaErrorNotSupported;
   }
   if (e == cudaSuccess) *launched = 1;
   return e;
+}
+}  // namespace
+
+cudaError_t msa_launch_iter_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                                 const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                                 float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
+  return launch_fast<false>(g, K, T, R, c, cb, p, mu, I, c_out, cb_out, p_out, s, launched);
+}
+
+cudaError_t msa_launch_iter_fast_lin(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                                     const float* c, const float* mu, const float* I, float* c_out, float* mu_out,
+                                     cudaStream_t s, int* launched) {
+  // the map set wants eight fields: the unused cbar / mu / cbar+ maps alias c, mu and c+
+  return launch_fast<true>(g, K, T, R, c, c, mu, mu, I, c_out, c_out, mu_out, s, launched);
 }

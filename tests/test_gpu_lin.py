@@ -105,3 +105,25 @@ def test_lin_split_bitwise(tmp_path):
         outs.append(np.load(out))
     for k in ("c", "mu"):
         assert np.array_equal(outs[0][k], outs[1][k]), k
+
+
+@pytest.mark.parametrize("shape,R", [((1, 64, 32, 3), 5), ((1, 130, 97, 3), 5), ((2, 70, 66, 3), 2),
+                                     ((1, 37, 29, 3), 3), ((1, 5, 7, 3), 4)])
+def test_lin_tile_equals_generic_bitwise(shape, R, tmp_path):
+    """The tiled C = 3 kernel of the single-loop scheme (msa_iter_fast.cu, LIN) has the generic
+    kernel's per-pixel arithmetic: bitwise-identical fields, across a round."""
+    B, H, W, C = shape
+    h = 1.0 / (W - 1) if W > 1 else 1.0
+    spec = dict(seed=H * 100 + W + R, shape=list(shape), iters=3,
+                params=dict(alpha=8.0 / h, beta=1.0, radius=R, kernel=0, eps_c=20.0, dt=0.25, rho=2.5 * h,
+                            gamma=2.5 * h, iters_per_round=2, rounds=1, scheme=LIN))
+    outs = []
+    for variant in ("generic", "tile"):
+        env = dict(os.environ, MSA_K1=variant)
+        env.pop("MSA_FORCE_GENERIC", None)
+        out = str(tmp_path / f"{variant}.npz")
+        subprocess.run([sys.executable, os.path.join(HERE, "_run_case.py"), json.dumps(spec), out], check=True,
+                       env=env)
+        outs.append(np.load(out))
+    for k in ("c", "mu"):
+        assert np.array_equal(outs[0][k], outs[1][k]), (k, float(np.max(np.abs(outs[0][k] - outs[1][k]))))
