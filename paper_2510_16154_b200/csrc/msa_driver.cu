@@ -112,6 +112,7 @@ struct msa_ctx {
   bool timing = false, in_iter_batch = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> iter_ev, round_ev;
   int64_t iter_launches_t = 0, round_launches_t = 0;
+  float* d_omtab = nullptr;  // 1 - a_delta for every (dx, dy) of the window, large supports (R > 8)
   // nccl
   ncclComm_t comm = nullptr;
   // rows mode: halo exchange on its own stream, overlapped with the interior K1 launch (§8(e))
@@ -143,7 +144,7 @@ int validate(const msa_params* p) {
   if (!finite_all(p)) return set_err(MSA_EINVAL, "non-finite parameter");
   if (p->alpha < 0) return set_err(MSA_EINVAL, "alpha must be >= 0");
   if (p->beta < 0) return set_err(MSA_EINVAL, "beta must be >= 0");
-  if (p->radius < 0 || p->radius > MSA_MAXR) return set_err(MSA_EINVAL, "radius must be in [0,8]");
+  if (p->radius < 0 || p->radius > MSA_MAXR) return set_err(MSA_EINVAL, "radius must be in [0,64]");
   if (p->kernel != MSA_KERNEL_WENDLAND && p->kernel != MSA_KERNEL_PRINTED) return set_err(MSA_EINVAL, "bad kernel");
   if (p->eps_c < 0) return set_err(MSA_EINVAL, "eps_c must be >= 0");
   if (p->dt < 0) return set_err(MSA_EINVAL, "dt must be >= 0");
@@ -238,7 +239,7 @@ size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
 struct Layout {
   size_t plane_floats, f1, f2;  // floats per plane, per C-field, per 2C-field
-  size_t off_I, off_mu, off_set[2], off_partials, off_sums, off_off, off_om, off_rec, total;
+  size_t off_I, off_mu, off_set[2], off_partials, off_sums, off_off, off_om, off_omtab, off_rec, total;
   int pitch, nblk;
 };
 Layout layout(const msa_params* p, const Part& pt) {
@@ -262,6 +263,7 @@ Layout layout(const msa_params* p, const Part& pt) {
   L.off_sums = o;     o += align_up(MSA_NSUM * 8, 256);
   L.off_off = o;      o += align_up(MSA_MAXOFF * sizeof(int2), 256);
   L.off_om = o;       o += align_up(MSA_MAXOFF * sizeof(float), 256);
+  L.off_omtab = o;    o += align_up(MSA_MAXOFF * sizeof(float), 256);  // [2R+1]^2 table (R > 8)
   L.off_rec = o;      o += align_up(REC_CAP * sizeof(msa_round_stats), 256);
   L.total = o;
   return L;
@@ -496,6 +498,20 @@ int k1_variant() {
 // the variant cascade sweep (opt-in) -> tiled C = 3 -> C = 16 -> generic.
 int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int o) {
   const msa_params& P = x->prm;
+  // large supports (NEXT-3): step 1 by the chunked n-body kernel into c[o], steps 2-3 generic
+  if (P.radius > 8 && P.channels <= 4 && k1_variant() != K1_GENERIC) {
+    cudaError_t e = msa_launch_agent_large(g, KC, P.radius, x->d_omtab, x->c[s], x->c[o], x->stream);
+    if (e != cudaSuccess) return set_err(MSA_ECUDA, "large-support agent kernel: %s", cudaGetErrorString(e));
+    if (P.scheme == MSA_SCHEME_LINEARISED_ADMM)
+      e = msa_launch_iter_lin_generic(g, KC, x->d_off, x->d_om, x->c[s], x->p[s], x->I, x->c[o], x->p[o], x->stream,
+                                      x->c[o]);
+    else
+      e = msa_launch_iter_generic(g, KC, x->d_off, x->d_om, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
+                                  x->cb[o], x->p[o], x->stream, x->c[o]);
+    if (e != cudaSuccess) return set_err(MSA_ECUDA, "iteration kernel launch: %s", cudaGetErrorString(e));
+    x->launches += 2;
+    return MSA_OK;
+  }
   if (P.scheme == MSA_SCHEME_LINEARISED_ADMM) {  // mu lives in the p ping-pong buffers
     int ok = 0;
     cudaError_t e = cudaErrorNotSupported;
@@ -754,6 +770,7 @@ int msa_init(const msa_params* params, const float* image, int image_on_device, 
   x->sums = (double*)(x->ws + L.off_sums);
   x->d_off = (int2*)(x->ws + L.off_off);
   x->d_om = (float*)(x->ws + L.off_om);
+  x->d_omtab = (float*)(x->ws + L.off_omtab);
   x->d_rec = (msa_round_stats*)(x->ws + L.off_rec);
   // zero the workspace (ghost rows of the outer slabs stay defined), then the offset table
   std::vector<int2> offs(std::max(x->T.n, 1));
@@ -764,6 +781,17 @@ int msa_init(const msa_params* params, const float* image, int image_on_device, 
       e = cudaMemcpyAsync(x->d_off, offs.data(), sizeof(int2) * x->T.n, cudaMemcpyHostToDevice, x->stream);
     if (e == cudaSuccess && x->T.n > 0)
       e = cudaMemcpyAsync(x->d_om, x->T.om, sizeof(float) * x->T.n, cudaMemcpyHostToDevice, x->stream);
+    std::vector<float> omtab;
+    if (e == cudaSuccess && params->radius > 8) {  // same formula and rounding as the offset table
+      const int R = params->radius, OW = 2 * R + 1;
+      omtab.resize((size_t)OW * OW);
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx) {
+          const double a = 0.5 * x->eps_x * ((dx * x->hx) * (dx * x->hx) + (dy * x->hy) * (dy * x->hy));
+          omtab[(size_t)(dy + R) * OW + dx + R] = (float)(1.0 - a);
+        }
+      e = cudaMemcpyAsync(x->d_omtab, omtab.data(), sizeof(float) * omtab.size(), cudaMemcpyHostToDevice, x->stream);
+    }
     if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);  // offs is a host temporary
     if (e != cudaSuccess) return fail(set_err(MSA_ECUDA, "init copies: %s", cudaGetErrorString(e)));
   }

@@ -13,15 +13,22 @@ struct MsaOffsetTable {
 };
 
 // Generic kernels (msa_kernels.cu): any C in [1,16], any R in [0,8].
+// chalf_in (may be null, may alias c_out): c_half computed by msa_launch_agent_large; step 1 is skipped.
 cudaError_t msa_launch_iter_generic(const MsaGeom& g, const MsaIterConsts& K, const int2* d_off, const float* d_om,
                                     const float* c, const float* cb, const float* p, const float* mu, const float* I,
-                                    float* c_out, float* cb_out, float* p_out, cudaStream_t s);
+                                    float* c_out, float* cb_out, float* p_out, cudaStream_t s,
+                                    const float* chalf_in = nullptr);
+
+// Step 1 alone for large supports (msa_agent_large.cu): 8 < R <= 64, C <= 4; omtab = 1 - a_delta for
+// every (dx, dy) in [-R, R]^2 ([dy + R][dx + R]); writes c_half.
+cudaError_t msa_launch_agent_large(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab,
+                                   const float* c, float* chalf, cudaStream_t s);
 
 // Single-loop linearised ADMM iteration (msa.h MSA_SCHEME_LINEARISED_ADMM), any C: reads c, mu, I,
 // writes c_out, mu_out.
 cudaError_t msa_launch_iter_lin_generic(const MsaGeom& g, const MsaIterConsts& K, const int2* d_off,
                                         const float* d_om, const float* c, const float* mu, const float* I,
-                                        float* c_out, float* mu_out, cudaStream_t s);
+                                        float* c_out, float* mu_out, cudaStream_t s, const float* chalf_in = nullptr);
 
 // Tiled C = 3 form of the single-loop scheme (msa_iter_fast.cu, LIN); bitwise equal to the generic one.
 cudaError_t msa_launch_iter_fast_lin(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,

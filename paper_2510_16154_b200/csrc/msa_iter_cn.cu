@@ -42,10 +42,11 @@ constexpr int CW = TW + 2 * CX; // 40
 constexpr int QW = TW + 1;      // p+ tile: columns x0-1 .. x0+31
 constexpr int QH = TH + 1;      // rows y0-1 .. y0+7
 
+constexpr int CN_MAXOFF = 81;  // R <= 4
 struct CnOffsets {
   int n;
-  signed char dx[MSA_MAXOFF], dy[MSA_MAXOFF];
-  float om[MSA_MAXOFF];
+  signed char dx[CN_MAXOFF], dy[CN_MAXOFF];
+  float om[CN_MAXOFF];
 };
 struct CnMaps {
   CUtensorMap c, cb;
@@ -241,7 +242,7 @@ cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const M
                                const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
-  if (g.C != 16 || R < 1 || R > 4) return cudaErrorNotSupported;
+  if (g.C != 16 || R < 1 || R > 4 || T.n > CN_MAXOFF) return cudaErrorNotSupported;
   CnOffsets off;
   off.n = T.n;
   for (int o = 0; o < T.n; ++o) {

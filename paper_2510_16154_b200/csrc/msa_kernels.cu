@@ -18,33 +18,39 @@ __global__ void __launch_bounds__(256) k_iter_generic(MsaGeom g, MsaIterConsts K
                                                       const float* __restrict__ om, const float* __restrict__ c,
                                                       const float* __restrict__ cb, const float* __restrict__ p,
                                                       const float* __restrict__ mu, const float* __restrict__ I,
-                                                      float* __restrict__ c_out, float* __restrict__ cb_out,
-                                                      float* __restrict__ p_out) {
+                                                      float* c_out, float* __restrict__ cb_out,
+                                                      float* __restrict__ p_out, const float* chalf_in) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int jl = g.k1_lo + blockIdx.y * blockDim.y + threadIdx.y;
   const int b = blockIdx.z;
   if (i >= g.W || jl >= msa_k1_hi(g)) return;
   const int j = g.row0 + jl;
   const int W = g.W, H = g.H;
-  // step 1: agent Euler step (eq:MAsystem windowed, R2)
-  float ci[C], acc[C];
-#pragma unroll
-  for (int k = 0; k < C; ++k) {
-    ci[k] = c[msa_idx(g, b, k, C, j, i)];
-    acc[k] = 0.0f;
-  }
-  for (int o = 0; o < K.n_off; ++o) {
-    const int2 d = off[o];
-    const int ii = i + d.x, jj = j + d.y;
-    if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue; // excluded, not padded (R20)
-    float cj[C];
-#pragma unroll
-    for (int k = 0; k < C; ++k) cj[k] = c[msa_idx(g, b, k, C, jj, ii)];
-    msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
-  }
+  // step 1: agent Euler step (eq:MAsystem windowed, R2), or c_half from the large-support kernel
+  // (chalf_in, which may alias c_out: only this thread reads / writes its pixel there)
   float chalf[C];
+  if (chalf_in) {
 #pragma unroll
-  for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+    for (int k = 0; k < C; ++k) chalf[k] = chalf_in[msa_idx(g, b, k, C, j, i)];
+  } else {
+    float ci[C], acc[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      ci[k] = c[msa_idx(g, b, k, C, j, i)];
+      acc[k] = 0.0f;
+    }
+    for (int o = 0; o < K.n_off; ++o) {
+      const int2 d = off[o];
+      const int ii = i + d.x, jj = j + d.y;
+      if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue; // excluded, not padded (R20)
+      float cj[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) cj[k] = c[msa_idx(g, b, k, C, jj, ii)];
+      msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+  }
   // step 2: p+ at (i,j), (i-1,j), (i,j-1); the last two only feed the divergence
   float qx[3][C], qy[3][C];
   const int pi[3] = {i, i - 1, i};
@@ -90,14 +96,14 @@ __global__ void __launch_bounds__(256) k_iter_generic(MsaGeom g, MsaIterConsts K
 template <int C>
 cudaError_t launch_iter_generic_c(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
                                   const float* c, const float* cb, const float* p, const float* mu, const float* I,
-                                  float* co, float* cbo, float* po, cudaStream_t s) {
+                                  float* co, float* cbo, float* po, cudaStream_t s, const float* chalf_in) {
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   dim3 blk(32, 8), grd((g.W + 31) / 32, (nr + 7) / 8, g.nb);
   if (K.kernel == 0)
-    k_iter_generic<C, 0><<<grd, blk, 0, s>>>(g, K, off, om, c, cb, p, mu, I, co, cbo, po);
+    k_iter_generic<C, 0><<<grd, blk, 0, s>>>(g, K, off, om, c, cb, p, mu, I, co, cbo, po, chalf_in);
   else
-    k_iter_generic<C, 1><<<grd, blk, 0, s>>>(g, K, off, om, c, cb, p, mu, I, co, cbo, po);
+    k_iter_generic<C, 1><<<grd, blk, 0, s>>>(g, K, off, om, c, cb, p, mu, I, co, cbo, po, chalf_in);
   return cudaGetLastError();
 }
 
@@ -111,31 +117,37 @@ template <int C, int KER>
 __global__ void __launch_bounds__(256) k_iter_lin_generic(MsaGeom g, MsaIterConsts K, const int2* __restrict__ off,
                                                           const float* __restrict__ om, const float* __restrict__ c,
                                                           const float* __restrict__ mu, const float* __restrict__ I,
-                                                          float* __restrict__ c_out, float* __restrict__ mu_out) {
+                                                          float* c_out, float* __restrict__ mu_out,
+                                                          const float* chalf_in) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int jl = g.k1_lo + blockIdx.y * blockDim.y + threadIdx.y;
   const int b = blockIdx.z;
   if (i >= g.W || jl >= msa_k1_hi(g)) return;
   const int j = g.row0 + jl;
   const int W = g.W, H = g.H;
-  float ci[C], acc[C];
-#pragma unroll
-  for (int k = 0; k < C; ++k) {
-    ci[k] = c[msa_idx(g, b, k, C, j, i)];
-    acc[k] = 0.0f;
-  }
-  for (int o = 0; o < K.n_off; ++o) {
-    const int2 d = off[o];
-    const int ii = i + d.x, jj = j + d.y;
-    if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;  // excluded, not padded (R20)
-    float cj[C];
-#pragma unroll
-    for (int k = 0; k < C; ++k) cj[k] = c[msa_idx(g, b, k, C, jj, ii)];
-    msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
-  }
   float chalf[C];
+  if (chalf_in) {  // from the large-support kernel (may alias c_out: own pixel only)
 #pragma unroll
-  for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+    for (int k = 0; k < C; ++k) chalf[k] = chalf_in[msa_idx(g, b, k, C, j, i)];
+  } else {
+    float ci[C], acc[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      ci[k] = c[msa_idx(g, b, k, C, j, i)];
+      acc[k] = 0.0f;
+    }
+    for (int o = 0; o < K.n_off; ++o) {
+      const int2 d = off[o];
+      const int ii = i + d.x, jj = j + d.y;
+      if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;  // excluded, not padded (R20)
+      float cj[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) cj[k] = c[msa_idx(g, b, k, C, jj, ii)];
+      msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+  }
   float mbx[3][C], mby[3][C], qx0[C], qy0[C];
   const int pi[3] = {i, i - 1, i};
   const int pj[3] = {j, j, j - 1};
@@ -185,14 +197,14 @@ __global__ void __launch_bounds__(256) k_iter_lin_generic(MsaGeom g, MsaIterCons
 template <int C>
 cudaError_t launch_iter_lin_generic_c(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
                                       const float* c, const float* mu, const float* I, float* co, float* muo,
-                                      cudaStream_t s) {
+                                      cudaStream_t s, const float* chalf_in) {
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   dim3 blk(32, 8), grd((g.W + 31) / 32, (nr + 7) / 8, g.nb);
   if (K.kernel == 0)
-    k_iter_lin_generic<C, 0><<<grd, blk, 0, s>>>(g, K, off, om, c, mu, I, co, muo);
+    k_iter_lin_generic<C, 0><<<grd, blk, 0, s>>>(g, K, off, om, c, mu, I, co, muo, chalf_in);
   else
-    k_iter_lin_generic<C, 1><<<grd, blk, 0, s>>>(g, K, off, om, c, mu, I, co, muo);
+    k_iter_lin_generic<C, 1><<<grd, blk, 0, s>>>(g, K, off, om, c, mu, I, co, muo, chalf_in);
   return cudaGetLastError();
 }
 
@@ -354,11 +366,11 @@ __global__ void k_unpack(MsaGeom g, int nm, const float* __restrict__ inter, flo
 
 cudaError_t msa_launch_iter_lin_generic(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
                                         const float* c, const float* mu, const float* I, float* co, float* muo,
-                                        cudaStream_t s) {
+                                        cudaStream_t s, const float* chalf_in) {
   switch (g.C) {
 #define MSA_CASE_L(CC) \
   case CC:             \
-    return launch_iter_lin_generic_c<CC>(g, K, off, om, c, mu, I, co, muo, s);
+    return launch_iter_lin_generic_c<CC>(g, K, off, om, c, mu, I, co, muo, s, chalf_in);
     MSA_CASE_L(1) MSA_CASE_L(2) MSA_CASE_L(3) MSA_CASE_L(4) MSA_CASE_L(5) MSA_CASE_L(6) MSA_CASE_L(7) MSA_CASE_L(8)
     MSA_CASE_L(9) MSA_CASE_L(10) MSA_CASE_L(11) MSA_CASE_L(12) MSA_CASE_L(13) MSA_CASE_L(14) MSA_CASE_L(15)
     MSA_CASE_L(16)
@@ -369,11 +381,11 @@ cudaError_t msa_launch_iter_lin_generic(const MsaGeom& g, const MsaIterConsts& K
 
 cudaError_t msa_launch_iter_generic(const MsaGeom& g, const MsaIterConsts& K, const int2* off, const float* om,
                                     const float* c, const float* cb, const float* p, const float* mu, const float* I,
-                                    float* co, float* cbo, float* po, cudaStream_t s) {
+                                    float* co, float* cbo, float* po, cudaStream_t s, const float* chalf_in) {
   switch (g.C) {
 #define MSA_CASE(CC) \
   case CC:           \
-    return launch_iter_generic_c<CC>(g, K, off, om, c, cb, p, mu, I, co, cbo, po, s);
+    return launch_iter_generic_c<CC>(g, K, off, om, c, cb, p, mu, I, co, cbo, po, s, chalf_in);
     MSA_CASE(1) MSA_CASE(2) MSA_CASE(3) MSA_CASE(4) MSA_CASE(5) MSA_CASE(6) MSA_CASE(7) MSA_CASE(8)
     MSA_CASE(9) MSA_CASE(10) MSA_CASE(11) MSA_CASE(12) MSA_CASE(13) MSA_CASE(14) MSA_CASE(15) MSA_CASE(16)
 #undef MSA_CASE
