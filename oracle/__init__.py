@@ -87,6 +87,33 @@ class Params:
 _D = ctypes.c_void_p
 
 
+class _DalParams(ctypes.Structure):
+    _fields_ = [("M", ctypes.c_int32), ("cost", ctypes.c_int32), ("iters", ctypes.c_int32),
+                ("max_ls", ctypes.c_int32), ("sigma0", ctypes.c_double), ("b", ctypes.c_double),
+                ("c", ctypes.c_double), ("ex_lo", ctypes.c_double), ("ex_hi", ctypes.c_double),
+                ("ec_lo", ctypes.c_double), ("ec_hi", ctypes.c_double), ("rho", ctypes.c_double)]
+
+
+@dataclass
+class DalParams:
+    """NEXT-1 DAL settings (oracle/msa_oracle.h mo_dal_params)."""
+    M: int
+    cost: int = 0           # 0: J of eq:cost_functional, 1: L~ with fixed v, mu
+    iters: int = 10
+    max_ls: int = 30
+    sigma0: float = 1.0
+    b: float = 0.5
+    c: float = 1e-4
+    ex_lo: float = 2.0      # E = [2, 1100]^2 (PAPER.md:270)
+    ex_hi: float = 1100.0
+    ec_lo: float = 2.0
+    ec_hi: float = 1100.0
+    rho: float = 1.0
+
+    def c_struct(self) -> _DalParams:
+        return _DalParams(**asdict(self))
+
+
 def _load():
     global _lib
     if _lib is None:
@@ -113,6 +140,13 @@ def _load():
             "mo_energy_L": ([P, ctypes.c_double, _D, _D, _D, _D], ctypes.c_double),
             "mo_energy_Ltilde": ([P, ctypes.c_double, _D, _D, _D, _D], ctypes.c_double),
             "mo_shrink_field": ([P, ctypes.c_double, _D, _D, _D], None),
+            "mo_phi_prime": ([ctypes.c_double, ctypes.c_int], ctypes.c_double),
+            "mo_agent_rhs_eps": ([P, ctypes.c_double, ctypes.c_double, _D, _D], None),
+            "mo_agent_jtvp": ([P, ctypes.c_double, ctypes.c_double, _D, _D, _D], None),
+            "mo_agent_deps": ([P, ctypes.c_double, ctypes.c_double, _D, _D, _D], None),
+            "mo_dal_cost": ([P, ctypes.POINTER(_DalParams), _D, _D, _D, _D, _D], ctypes.c_double),
+            "mo_dal_gradient": ([P, ctypes.POINTER(_DalParams), _D, _D, _D, _D, _D], ctypes.c_double),
+            "mo_dal": ([P, ctypes.POINTER(_DalParams), _D, _D, _D, _D, _D, _D], ctypes.c_int),
             "mo_labels": ([_D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_float, _D,
                            ctypes.POINTER(ctypes.c_int32), _D, ctypes.c_int32], ctypes.c_int),
         }
@@ -265,3 +299,66 @@ def labels(c: np.ndarray, delta: float = 0.1, max_k: int = 0):
     if rc != 0:
         raise ValueError("labels: non-finite or out-of-range field")
     return lab, n.value, pal[:min(max_k, n.value)] if max_k > 0 else None
+
+
+# ---------------------------------------------------------------- NEXT-1: DAL (Algorithm 1)
+def phi_prime(r: float, kernel: int = 0) -> float:
+    return _load().mo_phi_prime(r, kernel)
+
+
+def agent_rhs_eps(p: Params, eps_x: float, eps_c: float, c) -> np.ndarray:
+    c = _f64(c)
+    F = np.empty_like(c)
+    _load().mo_agent_rhs_eps(ctypes.byref(derive(p).c()), eps_x, eps_c, _ptr(c), _ptr(F))
+    return F
+
+
+def agent_jtvp(p: Params, eps_x: float, eps_c: float, c, lam) -> np.ndarray:
+    c, lam = _f64(c), _f64(lam)
+    g = np.empty_like(c)
+    _load().mo_agent_jtvp(ctypes.byref(derive(p).c()), eps_x, eps_c, _ptr(c), _ptr(lam), _ptr(g))
+    return g
+
+
+def agent_deps(p: Params, eps_x: float, eps_c: float, c, lam) -> np.ndarray:
+    c, lam = _f64(c), _f64(lam)
+    out = np.zeros(2)
+    _load().mo_agent_deps(ctypes.byref(derive(p).c()), eps_x, eps_c, _ptr(c), _ptr(lam), _ptr(out))
+    return out
+
+
+def _vmu(p: Params, v, mu):
+    shape = (p.height, p.width, 2 * p.channels)
+    v = _f64(np.zeros(shape) if v is None else v)
+    mu = _f64(np.zeros(shape) if mu is None else mu)
+    return v, mu
+
+
+def dal_cost(p: Params, d: DalParams, eps, I, v=None, mu=None, return_state: bool = False):
+    eps, I = _f64(eps), _f64(I)
+    v, mu = _vmu(p, v, mu)
+    cT = np.empty_like(I)
+    J = _load().mo_dal_cost(ctypes.byref(p.c()), ctypes.byref(d.c_struct()), _ptr(eps), _ptr(I), _ptr(v), _ptr(mu),
+                            _ptr(cT))
+    return (J, cT) if return_state else J
+
+
+def dal_gradient(p: Params, d: DalParams, eps, I, v=None, mu=None):
+    eps, I = _f64(eps), _f64(I)
+    v, mu = _vmu(p, v, mu)
+    g = np.empty_like(eps)
+    J = _load().mo_dal_gradient(ctypes.byref(p.c()), ctypes.byref(d.c_struct()), _ptr(eps), _ptr(I), _ptr(v),
+                                _ptr(mu), _ptr(g))
+    return J, g
+
+
+def dal(p: Params, d: DalParams, eps, I, v=None, mu=None):
+    """Algorithm 1 from eps ([M][2], updated copy returned) -> (eps, J_hist[iters+1], sigma_hist[iters])."""
+    eps = _f64(eps).copy()
+    I = _f64(I)
+    v, mu = _vmu(p, v, mu)
+    Jh = np.zeros(d.iters + 1)
+    sh = np.zeros(max(d.iters, 1))
+    _load().mo_dal(ctypes.byref(p.c()), ctypes.byref(d.c_struct()), _ptr(eps), _ptr(I), _ptr(v), _ptr(mu), _ptr(Jh),
+                   _ptr(sh))
+    return eps, Jh, sh[:d.iters]

@@ -591,3 +591,242 @@ int mo_labels(const float* c, int H, int W, int C, float delta, int32_t* labels,
   free(parent); free(seg_of_root); free(sum); free(cnt); free(seg_root); free(mean); free(keys);
   return 0;
 }
+
+/* ============================================================ NEXT-1: DAL (Algorithm 1) */
+
+/* phi'(r) on [0,1): standard (4r+1)(1-r)^4 -> -20 r (1-r)^3; printed (4r-1)(1-r)^4 ->
+ * (1-r)^3 (8 - 20 r); 0 for r >= 1 (the C^2 Wendland kernel, eq:kernel PAPER.md:259-267). */
+double mo_phi_prime(double r, int kernel) {
+  if (r < 0.0) r = 0.0;
+  if (r >= 1.0) return 0.0;
+  const double s = 1.0 - r;
+  return kernel == 0 ? -20.0 * r * s * s * s : s * s * s * (8.0 - 20.0 * r);
+}
+
+static void with_eps(const mo_params* prm, double eps_x, double eps_c, mo_params* q) {
+  *q = *prm;
+  q->eps_x = eps_x;
+  q->eps_c = eps_c;
+}
+
+/* F(c; eps) of eq:MAsystem with the given control (prm derived; eps_x > 0). */
+void mo_agent_rhs_eps(const mo_params* prm, double eps_x, double eps_c, const double* c, double* F) {
+  mo_params q;
+  with_eps(prm, eps_x, eps_c, &q);
+  mo_agent_rhs(&q, c, F);
+}
+
+/* g = (dF/dc)^T lam. For a window pair (k, j = k + delta), d = c_j - c_k, r = eps_x/2 |delta|_h^2
+ * + eps_c/2 |d|^2: dF_i/dc_j = (1/N_R)[phi'(r) eps_c d d^T + phi(r) Id] for j != i and
+ * dF_i/dc_i = -sum_j dF_i/dc_j (eq:dF_dc, without the j = i term: reading R26). Using the window's
+ * symmetry (k in W(j) iff j in W(k), same r) the transpose product collapses to a stencil:
+ *   g_k = (1/N_R) sum_{j in W(k)} [ phi(r) (lam_j - lam_k) + eps_c phi'(r) (d . (lam_j - lam_k)) d ]. */
+void mo_agent_jtvp(const mo_params* prm, double eps_x, double eps_c, const double* c, const double* lam, double* g) {
+  const int H = prm->height, W = prm->width, C = prm->channels, R = prm->radius;
+  const double NR = (double)mo_window_size(R);
+#pragma omp parallel for schedule(static)
+  for (int j = 0; j < H; ++j)
+    for (int i = 0; i < W; ++i) {
+      double acc[64];
+      for (int k = 0; k < C; ++k) acc[k] = 0.0;
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx) {
+          if (dx * dx + dy * dy > R * R) continue;
+          const int ii = i + dx, jj = j + dy;
+          if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;
+          double d[64], dl[64], s = 0.0, ddl = 0.0;
+          for (int k = 0; k < C; ++k) {
+            d[k] = c[IDX(jj, ii) * C + k] - c[IDX(j, i) * C + k];
+            dl[k] = lam[IDX(jj, ii) * C + k] - lam[IDX(j, i) * C + k];
+            s += d[k] * d[k];
+            ddl += d[k] * dl[k];
+          }
+          const double r = mo_pair_r(dx * prm->hx, dy * prm->hy, s, eps_x, eps_c);
+          const double ph = mo_phi(r, prm->kernel), dph = mo_phi_prime(r, prm->kernel);
+          for (int k = 0; k < C; ++k) acc[k] += ph * dl[k] + eps_c * dph * ddl * d[k];
+        }
+      for (int k = 0; k < C; ++k) g[IDX(j, i) * C + k] = acc[k] / NR;
+    }
+}
+
+/* out2 = ( <lam, dF/deps_x>, <lam, dF/deps_c> ) (Euclidean over pixels and channels):
+ * dF_i/deps_x = (1/N_R) sum_j phi'(r) |delta|_h^2/2 d,  dF_i/deps_c = (1/N_R) sum_j phi'(r) |d|^2/2 d
+ * (eq:dF_depsx, eq:dF_depsc with the window of R2). */
+void mo_agent_deps(const mo_params* prm, double eps_x, double eps_c, const double* c, const double* lam,
+                   double* out2) {
+  const int H = prm->height, W = prm->width, C = prm->channels, R = prm->radius;
+  const double NR = (double)mo_window_size(R);
+  double sx = 0.0, sc = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : sx, sc)
+  for (int j = 0; j < H; ++j)
+    for (int i = 0; i < W; ++i)
+      for (int dy = -R; dy <= R; ++dy)
+        for (int dx = -R; dx <= R; ++dx) {
+          if (dx * dx + dy * dy > R * R) continue;
+          const int ii = i + dx, jj = j + dy;
+          if (ii < 0 || ii >= W || jj < 0 || jj >= H) continue;
+          double s = 0.0, dlam = 0.0;
+          for (int k = 0; k < C; ++k) {
+            const double d = c[IDX(jj, ii) * C + k] - c[IDX(j, i) * C + k];
+            s += d * d;
+            dlam += d * lam[IDX(j, i) * C + k];
+          }
+          const double dxo = dx * prm->hx, dyo = dy * prm->hy;
+          const double dph = mo_phi_prime(mo_pair_r(dxo, dyo, s, eps_x, eps_c), prm->kernel);
+          sx += dph * 0.5 * (dxo * dxo + dyo * dyo) * dlam / NR;
+          sc += dph * 0.5 * s * dlam / NR;
+        }
+  out2[0] = sx;
+  out2[1] = sc;
+}
+
+/* terminal cost Phi(c) and its gradient dPhi/dc (hx hy quadrature; grad, div of R6) */
+static double terminal(const mo_params* prm, const mo_dal_params* d, const double* c, const double* I,
+                       const double* v, const double* mu, double* grad) {
+  const int H = prm->height, W = prm->width, C = prm->channels;
+  const size_t n1 = (size_t)H * W * C, n2 = 2 * n1;
+  const double w = prm->hx * prm->hy, alpha = prm->alpha;
+  double* g = (double*)malloc(n2 * sizeof(double));
+  double* q = (double*)malloc(n2 * sizeof(double));
+  mo_grad(c, g, H, W, C, prm->hx, prm->hy);
+  double e = 0.0;
+  for (size_t k = 0; k < n2; ++k) {
+    if (d->cost == 0) {          /* 1/2 |grad c|^2: dPhi/dc = -w div(grad c) */
+      q[k] = g[k];
+      e += 0.5 * g[k] * g[k];
+    } else {                     /* rho/2 |v - grad c + mu/rho|^2: dPhi/dc = w div(mu + rho v - rho grad c) */
+      const double a = v[k] - g[k] + mu[k] / d->rho;
+      q[k] = -d->rho * a;
+      e += 0.5 * d->rho * a * a;
+    }
+  }
+  for (size_t k = 0; k < n1; ++k) e += 0.5 * alpha * (c[k] - I[k]) * (c[k] - I[k]);
+  if (grad) {
+    double* dv = (double*)malloc(n1 * sizeof(double));
+    mo_div(q, dv, H, W, C, prm->hx, prm->hy);  /* <q, grad dc> = -<div q, dc> */
+    for (size_t k = 0; k < n1; ++k) grad[k] = w * (-dv[k] + alpha * (c[k] - I[k]));
+    free(dv);
+  }
+  free(g); free(q);
+  return w * e;
+}
+
+/* J(eps) = Phi(c^M); cT (may be NULL) receives c^M. */
+double mo_dal_cost(const mo_params* prm_in, const mo_dal_params* d, const double* eps, const double* I,
+                   const double* v, const double* mu, double* cT) {
+  mo_params prm;
+  mo_derive(prm_in, &prm);
+  const size_t n1 = (size_t)prm.height * prm.width * prm.channels;
+  double* c = (double*)malloc(n1 * sizeof(double));
+  double* F = (double*)malloc(n1 * sizeof(double));
+  memcpy(c, I, n1 * sizeof(double));
+  for (int m = 0; m < d->M; ++m) {
+    mo_agent_rhs_eps(&prm, eps[2 * m], eps[2 * m + 1], c, F);
+    for (size_t k = 0; k < n1; ++k) c[k] += prm.dt * F[k];
+  }
+  const double J = terminal(&prm, d, c, I, v, mu, NULL);
+  if (cT) memcpy(cT, c, n1 * sizeof(double));
+  free(c); free(F);
+  return J;
+}
+
+/* Exact gradient of the discrete J: forward sweep storing c^0..c^{M-1}, lam^M = dPhi/dc(c^M),
+ * dJ/deps[m] = dt <lam^{m+1}, dF/deps(c^m)>, lam^m = lam^{m+1} + dt (dF/dc(c^m))^T lam^{m+1}
+ * (eq:opt_system-b in discrete-adjoint form; eq:dF_depsx, eq:dF_depsc). Returns J. */
+double mo_dal_gradient(const mo_params* prm_in, const mo_dal_params* d, const double* eps, const double* I,
+                       const double* v, const double* mu, double* grad) {
+  mo_params prm;
+  mo_derive(prm_in, &prm);
+  const size_t n1 = (size_t)prm.height * prm.width * prm.channels;
+  const int M = d->M;
+  double* traj = (double*)malloc((size_t)(M + 1) * n1 * sizeof(double));
+  double* F = (double*)malloc(n1 * sizeof(double));
+  double* lam = (double*)malloc(n1 * sizeof(double));
+  double* g = (double*)malloc(n1 * sizeof(double));
+  memcpy(traj, I, n1 * sizeof(double));
+  for (int m = 0; m < M; ++m) {
+    mo_agent_rhs_eps(&prm, eps[2 * m], eps[2 * m + 1], traj + (size_t)m * n1, F);
+    for (size_t k = 0; k < n1; ++k) traj[(size_t)(m + 1) * n1 + k] = traj[(size_t)m * n1 + k] + prm.dt * F[k];
+  }
+  const double J = terminal(&prm, d, traj + (size_t)M * n1, I, v, mu, lam);
+  for (int m = M - 1; m >= 0; --m) {
+    const double* cm = traj + (size_t)m * n1;
+    double de[2];
+    mo_agent_deps(&prm, eps[2 * m], eps[2 * m + 1], cm, lam, de);
+    grad[2 * m] = prm.dt * de[0];
+    grad[2 * m + 1] = prm.dt * de[1];
+    mo_agent_jtvp(&prm, eps[2 * m], eps[2 * m + 1], cm, lam, g);
+    for (size_t k = 0; k < n1; ++k) lam[k] += prm.dt * g[k];
+  }
+  free(traj); free(F); free(lam); free(g);
+  return J;
+}
+
+static void project_E(const mo_dal_params* d, double* e, int M) {
+  for (int m = 0; m < M; ++m) {
+    e[2 * m] = e[2 * m] < d->ex_lo ? d->ex_lo : (e[2 * m] > d->ex_hi ? d->ex_hi : e[2 * m]);
+    e[2 * m + 1] = e[2 * m + 1] < d->ec_lo ? d->ec_lo : (e[2 * m + 1] > d->ec_hi ? d->ec_hi : e[2 * m + 1]);
+  }
+}
+
+/* Algorithm 1 with the readings of DESIGN.md R25/R31: descent along -D,
+ * candidates Pi_E(eps - tau D), Armijo test J(cand) <= J(eps) - c tau |D|^2. Two-way search: if
+ * sigma passes, grow it (tau / b) while the test passes and keep the last passing tau; otherwise
+ * shrink (b tau) until it passes (at most max_ls evaluations; a step that never passes is not
+ * taken). sigma^(j+1) = the accepted tau. J_hist[0..iters], sigma_hist[0..iters) may be NULL.
+ * Returns the number of iterations that took a step. */
+/* one Armijo test: cand = Pi_E(eps - t D); J(cand) <= J0 - c t |D|^2 */
+static int armijo_ok(const mo_params* prm, const mo_dal_params* d, const double* eps, const double* D, double D2,
+                     double J0, double t, const double* I, const double* v, const double* mu, double* cand) {
+  for (int m = 0; m < 2 * d->M; ++m) cand[m] = eps[m] - t * D[m];
+  project_E(d, cand, d->M);
+  return mo_dal_cost(prm, d, cand, I, v, mu, NULL) <= J0 - d->c * t * D2;
+}
+
+int mo_dal(const mo_params* prm_in, const mo_dal_params* d, double* eps, const double* I, const double* v,
+           const double* mu, double* J_hist, double* sigma_hist) {
+  const int M = d->M;
+  double* D = (double*)malloc(2 * (size_t)M * sizeof(double));
+  double* cand = (double*)malloc(2 * (size_t)M * sizeof(double));
+  double sigma = d->sigma0;
+  int taken = 0;
+  project_E(d, eps, M);
+  for (int it = 0; it < d->iters; ++it) {
+    const double J0 = mo_dal_gradient(prm_in, d, eps, I, v, mu, D);
+    if (J_hist) J_hist[it] = J0;
+    double D2 = 0.0;
+    for (int m = 0; m < 2 * M; ++m) D2 += D[m] * D[m];
+    double tau = sigma, acc_tau = -1.0;
+    int evals = 1;
+    if (armijo_ok(prm_in, d, eps, D, D2, J0, tau, I, v, mu, cand)) {
+      acc_tau = tau;
+      while (evals < d->max_ls) {
+        ++evals;
+        if (!armijo_ok(prm_in, d, eps, D, D2, J0, tau / d->b, I, v, mu, cand)) break;
+        tau /= d->b;
+        acc_tau = tau;
+      }
+    } else {
+      while (evals < d->max_ls) {
+        ++evals;
+        tau *= d->b;
+        if (armijo_ok(prm_in, d, eps, D, D2, J0, tau, I, v, mu, cand)) {
+          acc_tau = tau;
+          break;
+        }
+      }
+    }
+    if (sigma_hist) sigma_hist[it] = acc_tau;
+    if (acc_tau > 0) {
+      sigma = acc_tau;
+      for (int m = 0; m < 2 * M; ++m) eps[m] -= sigma * D[m];
+      project_E(d, eps, M);
+      ++taken;
+    } else {
+      sigma = tau;  /* no admissible step within the cap: start the next search from the smallest tried */
+    }
+  }
+  if (J_hist) J_hist[d->iters] = mo_dal_cost(prm_in, d, eps, I, v, mu, NULL);
+  free(D); free(cand);
+  return taken;
+}

@@ -72,6 +72,35 @@ void mo_shrink_field(const mo_params* prm, double rho, const double* c, const do
 int mo_labels(const float* c, int H, int W, int C, float delta, int32_t* labels, int32_t* n_clusters,
               float* palette, int32_t max_k);
 
+/* ---- NEXT-1: DAL control optimisation (Algorithm 1), discrete adjoint form.
+ * Control eps[m] = (eps_x, eps_c) per Euler step m < M (constant on the step); state
+ * c^{m+1} = c^m + dt F(c^m; eps[m]) (eq:MAsystem with the window of reading R2), c^0 = I.
+ * Terminal cost Phi (hx hy quadrature): cost 0 = J of eq:cost_functional,
+ *   Phi = <1/2 |grad c|^2 + alpha/2 (c - I)^2>;  cost 1 = L~ of eq:complete_square with fixed
+ *   v, mu:  Phi = <rho/2 |v - grad c + mu/rho|^2 + alpha/2 (c - I)^2>  (beta |v| is constant in c). */
+typedef struct {
+  int32_t M;          /* Euler steps (T = M dt) */
+  int32_t cost;       /* 0 quadratic J, 1 L~ (ADMM u-step, Alg. 2 line 5) */
+  int32_t iters;      /* DAL iterations */
+  int32_t max_ls;     /* line-search evaluations cap per iteration */
+  double sigma0;      /* initial step sigma^(0) */
+  double b, c;        /* Armijo factors b, c in (0,1) */
+  double ex_lo, ex_hi, ec_lo, ec_hi; /* box E ([2,1100]^2) */
+  double rho;         /* L~ penalty (cost 1) */
+} mo_dal_params;
+
+double mo_phi_prime(double r, int kernel);
+void mo_agent_rhs_eps(const mo_params* prm, double eps_x, double eps_c, const double* c, double* F);
+void mo_agent_jtvp(const mo_params* prm, double eps_x, double eps_c, const double* c, const double* lam, double* g);
+void mo_agent_deps(const mo_params* prm, double eps_x, double eps_c, const double* c, const double* lam,
+                   double* out2);
+double mo_dal_cost(const mo_params* prm, const mo_dal_params* d, const double* eps, const double* I, const double* v,
+                   const double* mu, double* cT);
+double mo_dal_gradient(const mo_params* prm, const mo_dal_params* d, const double* eps, const double* I,
+                       const double* v, const double* mu, double* grad);
+int mo_dal(const mo_params* prm, const mo_dal_params* d, double* eps, const double* I, const double* v,
+           const double* mu, double* J_hist, double* sigma_hist);
+
 #ifdef __cplusplus
 }
 #endif

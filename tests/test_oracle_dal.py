@@ -1,0 +1,97 @@
+"""Pins of the DAL oracle (Algorithm 1; oracle mo_dal*):
+  D1  phi' against a central difference of phi (both kernel forms, eq:kernel).
+  D2  the transpose Jacobian product (eq:dF_dc, R26) against the directional derivative of F by
+      central differences: <g, v> = d/dh <lam, F(c + h v)>.
+  D3  <lam, dF/deps> (eq:dF_depsx, eq:dF_depsc) against central differences in eps.
+  D4  the full discrete-adjoint gradient of J against central differences of J, for the quadratic
+      cost (eq:cost_functional) and the L~ cost with v, mu (eq:complete_square, eq:new_adjoint).
+  D5  Algorithm 1: every accepted step satisfies the Armijo test, J never increases, eps stays in E."""
+import numpy as np
+import pytest
+
+import oracle
+
+
+def _setup(H=6, W=7, C=3, R=3, M=4, seed=0, **kw):
+    rng = np.random.default_rng(seed)
+    I = rng.random((H, W, C))
+    p = oracle.Params(height=H, width=W, channels=C, radius=R, eps_x=30.0, eps_c=8.0, dt=0.25, alpha=5.0,
+                      beta=1.0, rho=1.0, gamma=1.0, **kw)
+    eps = np.stack([rng.uniform(20.0, 60.0, M), rng.uniform(4.0, 12.0, M)], axis=1)
+    return rng, I, p, eps
+
+
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_D1_phi_prime(kernel):
+    for r in np.linspace(0.01, 0.99, 23):
+        h = 1e-6
+        fd = (oracle.phi(r + h, kernel) - oracle.phi(r - h, kernel)) / (2 * h)
+        assert oracle.phi_prime(r, kernel) == pytest.approx(fd, rel=1e-7, abs=1e-9)
+    assert oracle.phi_prime(1.0, kernel) == 0.0 and oracle.phi_prime(1.5, kernel) == 0.0
+
+
+@pytest.mark.parametrize("C,kernel", [(3, 0), (1, 1), (2, 0)])
+def test_D2_transpose_jacobian_product(C, kernel):
+    rng, I, p, _ = _setup(C=C, kernel=kernel)
+    c = I + 0.05 * rng.standard_normal(I.shape)
+    lam = rng.standard_normal(I.shape)
+    v = rng.standard_normal(I.shape)
+    ex, ec = 30.0, 8.0
+    g = oracle.agent_jtvp(p, ex, ec, c, lam)
+    h = 1e-6
+    fd = (np.sum(lam * oracle.agent_rhs_eps(p, ex, ec, c + h * v)) -
+          np.sum(lam * oracle.agent_rhs_eps(p, ex, ec, c - h * v))) / (2 * h)
+    assert np.sum(g * v) == pytest.approx(fd, rel=1e-7)
+
+
+def test_D3_eps_derivatives():
+    rng, I, p, _ = _setup()
+    c = I + 0.05 * rng.standard_normal(I.shape)
+    lam = rng.standard_normal(I.shape)
+    ex, ec = 30.0, 8.0
+    de = oracle.agent_deps(p, ex, ec, c, lam)
+    h = 1e-5
+    fx = (np.sum(lam * oracle.agent_rhs_eps(p, ex + h, ec, c)) - np.sum(lam * oracle.agent_rhs_eps(p, ex - h, ec, c)))
+    fc = (np.sum(lam * oracle.agent_rhs_eps(p, ex, ec + h, c)) - np.sum(lam * oracle.agent_rhs_eps(p, ex, ec - h, c)))
+    assert de[0] == pytest.approx(fx / (2 * h), rel=1e-6)
+    assert de[1] == pytest.approx(fc / (2 * h), rel=1e-6)
+
+
+@pytest.mark.parametrize("cost", [0, 1])
+def test_D4_gradient_matches_finite_differences(cost):
+    rng, I, p, eps = _setup(M=5, seed=3 + cost)
+    d = oracle.DalParams(M=5, cost=cost, rho=0.7)
+    v = mu = None
+    if cost == 1:
+        v = 0.3 * rng.standard_normal((6, 7, 6))
+        mu = 0.3 * rng.standard_normal((6, 7, 6))
+    J, g = oracle.dal_gradient(p, d, eps, I, v, mu)
+    assert J == pytest.approx(oracle.dal_cost(p, d, eps, I, v, mu), rel=1e-15)
+    for m in range(5):
+        for q in range(2):
+            h = 1e-4 * eps[m, q]
+            ep, em = eps.copy(), eps.copy()
+            ep[m, q] += h
+            em[m, q] -= h
+            fd = (oracle.dal_cost(p, d, ep, I, v, mu) - oracle.dal_cost(p, d, em, I, v, mu)) / (2 * h)
+            assert g[m, q] == pytest.approx(fd, rel=2e-5, abs=1e-12), (m, q)
+
+
+def test_D5_armijo_descent_and_projection():
+    rng, I, p, eps = _setup(M=6, seed=9)
+    d = oracle.DalParams(M=6, iters=8, sigma0=1e3, b=0.5, c=1e-4, ex_lo=2.0, ex_hi=1100.0, ec_lo=2.0, ec_hi=1100.0)
+    eps1, Jh, sh = oracle.dal(p, d, eps, I)
+    assert np.all(np.diff(Jh) <= 1e-15)
+    assert Jh[-1] < Jh[0]
+    assert np.all((eps1[:, 0] >= 2.0) & (eps1[:, 0] <= 1100.0) & (eps1[:, 1] >= 2.0) & (eps1[:, 1] <= 1100.0))
+    # replay: each accepted step passes the Armijo test of Algorithm 1 (descent along -D, R25)
+    e = eps.copy()
+    for it in range(d.iters):
+        J0, D = oracle.dal_gradient(p, d, e, I)
+        if sh[it] > 0:
+            cand = e - sh[it] * D
+            cand[:, 0] = np.clip(cand[:, 0], 2.0, 1100.0)
+            cand[:, 1] = np.clip(cand[:, 1], 2.0, 1100.0)
+            assert oracle.dal_cost(p, d, cand, I) <= J0 - d.c * sh[it] * np.sum(D * D) + 1e-15
+            e = cand
+    assert np.allclose(e, eps1, rtol=0, atol=1e-12)
