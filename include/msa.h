@@ -220,6 +220,39 @@ int msa_set_timing(msa_ctx* ctx, int enable);
 int msa_get_timing(msa_ctx* ctx, double* iter_ms, int64_t* iter_launches, double* round_ms,
                    int64_t* round_launches);
 
+/* ---- NEXT-1: DAL control optimisation (Algorithm 1).
+ * Optimises the control eps(t) = (eps_x, eps_c), constant on each of `steps` Euler steps of
+ * length params->dt (T = steps dt; the paper: T = 125, dt = 0.25), of the agent
+ * dynamics c' = F(c; eps) (eq:MAsystem on the window D_R of reading R2, c(0) = I) for the terminal
+ * cost Phi(c(T)) with the hx hy quadrature:
+ *   cost 0: J = <1/2 |grad c|^2 + alpha/2 (c - I)^2>        (eq:cost_functional, Section 3 DAL)
+ *   cost 1: L~ = <rho/2 |v - grad c + mu/rho|^2 + alpha/2 (c - I)^2> with fixed v, mu
+ *           (eq:complete_square; the u-step of Alg. 2, line 5, terminal condition eq:new_adjoint).
+ * Gradient: exact discrete adjoint of the Euler scheme (backward transpose-Jacobian sweep,
+ * eq:opt_system-b with eq:dF_dc minus its j = i term, reading R26; eq:dF_depsx, eq:dF_depsc).
+ * Step: two-way Armijo backtracking with the projection Pi_E onto the box E, descent along -D
+ * (reading R25), keeping the last step that passes the test (reading R31).
+ * Context: one image (nimages = 1), world = 1, C <= 4; radius R bounds the support (R >= the
+ * support radius 1/(h sqrt(eps_x,min/2)) makes the window sum the paper's all-pairs sum).
+ * eps: host float64 [steps][2] (initial guess in, optimised control out, projected onto E).
+ * v, mu: host float32 [H][W][2C] for cost 1 (NULL = 0). J_hist[iters + 1], sigma_hist[iters]:
+ * host or NULL (sigma <= 0: no admissible step that iteration). On return c = cbar = c(T; eps).
+ * The trajectory (steps + 1 fields) is kept on the device. Synchronises. */
+typedef struct {
+  int32_t steps;      /* M >= 1 */
+  int32_t cost;       /* 0 or 1, see above */
+  int32_t iters;      /* DAL iterations >= 0 */
+  int32_t max_ls;     /* cost evaluations per line search >= 1 */
+  double sigma0;      /* initial step sigma^(0) > 0 */
+  double b, c;        /* Armijo factors in (0, 1) */
+  double ex_lo, ex_hi, ec_lo, ec_hi; /* the box E = [ex_lo, ex_hi] x [ec_lo, ec_hi], ex_lo > 0 */
+} msa_dal_params;
+int msa_dal(msa_ctx* ctx, const msa_dal_params* d, double* eps, const float* v, const float* mu, double* J_hist,
+            double* sigma_hist);
+/* J(eps) and its gradient dJ/deps ([steps][2], host) without optimising (may be NULL). */
+int msa_dal_gradient(msa_ctx* ctx, const msa_dal_params* d, const double* eps, const float* v, const float* mu,
+                     double* J, double* grad);
+
 int msa_sync(msa_ctx* ctx);
 int msa_free(msa_ctx* ctx);
 

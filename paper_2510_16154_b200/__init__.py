@@ -28,13 +28,40 @@ SCHEME_CP_ROUNDS, SCHEME_LINEARISED_ADMM = 0, 1
 ABI_SYMBOLS = ["msa_abi_version", "msa_last_error", "msa_workspace_bytes", "msa_partition_rows",
                "msa_nccl_unique_id", "msa_halo_plan", "msa_init", "msa_reset", "msa_step", "msa_solve", "msa_labels",
                "msa_get_field", "msa_set_field", "msa_get_stats", "msa_state_bytes", "msa_get_state",
-               "msa_set_state", "msa_query", "msa_set_timing", "msa_get_timing", "msa_sync", "msa_free"]
+               "msa_set_state", "msa_query", "msa_set_timing", "msa_get_timing", "msa_dal", "msa_dal_gradient",
+               "msa_sync", "msa_free"]
 
 
 class MsaError(RuntimeError):
     def __init__(self, code: int, msg: str):
         super().__init__(f"msa error {code}: {msg}")
         self.code = code
+
+
+class _DalParams(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_int32), ("cost", ctypes.c_int32), ("iters", ctypes.c_int32),
+                ("max_ls", ctypes.c_int32), ("sigma0", ctypes.c_double), ("b", ctypes.c_double),
+                ("c", ctypes.c_double), ("ex_lo", ctypes.c_double), ("ex_hi", ctypes.c_double),
+                ("ec_lo", ctypes.c_double), ("ec_hi", ctypes.c_double)]
+
+
+@dataclass
+class DalParams:
+    """msa_dal_params (include/msa.h): NEXT-1, Algorithm 1 of the paper."""
+    steps: int
+    cost: int = 0
+    iters: int = 10
+    max_ls: int = 30
+    sigma0: float = 1.0
+    b: float = 0.5
+    c: float = 1e-4
+    ex_lo: float = 2.0
+    ex_hi: float = 1100.0
+    ec_lo: float = 2.0
+    ec_hi: float = 1100.0
+
+    def c_struct(self) -> "_DalParams":
+        return _DalParams(**asdict(self))
 
 
 class _CParams(ctypes.Structure):
@@ -159,6 +186,8 @@ def lib():
             "msa_set_timing": ([P, ctypes.c_int], ctypes.c_int),
             "msa_get_timing": ([P, PD, PI64, PD, PI64], ctypes.c_int),
             "msa_sync": ([P], ctypes.c_int),
+            "msa_dal": ([P, ctypes.POINTER(_DalParams), P, P, P, P, P], ctypes.c_int),
+            "msa_dal_gradient": ([P, ctypes.POINTER(_DalParams), P, P, P, P, P], ctypes.c_int),
             "msa_free": ([P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
@@ -359,3 +388,37 @@ class Solver:
 
     def sync(self) -> None:
         _check(lib().msa_sync(self._ctx))
+
+    # -- NEXT-1: DAL control optimisation (Algorithm 1)
+    @staticmethod
+    def _vmu(v, mu):
+        keep = []
+        out = []
+        for a in (v, mu):
+            if a is None:
+                out.append(None)
+            else:
+                a = np.ascontiguousarray(a, dtype=np.float32)
+                keep.append(a)
+                out.append(a.ctypes.data)
+        return out, keep
+
+    def dal(self, d: "DalParams", eps, v=None, mu=None):
+        """Optimises eps ([steps][2]) from the given guess; returns (eps, J_hist, sigma_hist)."""
+        e = np.ascontiguousarray(eps, dtype=np.float64).copy()
+        assert e.shape == (d.steps, 2)
+        Jh = np.zeros(d.iters + 1)
+        sh = np.zeros(max(d.iters, 1))
+        (vp, mp), keep = self._vmu(v, mu)
+        _check(lib().msa_dal(self._ctx, ctypes.byref(d.c_struct()), e.ctypes.data, vp, mp, Jh.ctypes.data,
+                             sh.ctypes.data))
+        return e, Jh, sh[:d.iters]
+
+    def dal_gradient(self, d: "DalParams", eps, v=None, mu=None):
+        e = np.ascontiguousarray(eps, dtype=np.float64)
+        g = np.zeros_like(e)
+        J = ctypes.c_double()
+        (vp, mp), keep = self._vmu(v, mu)
+        _check(lib().msa_dal_gradient(self._ctx, ctypes.byref(d.c_struct()), e.ctypes.data, vp, mp, ctypes.byref(J),
+                                      g.ctypes.data))
+        return J.value, g

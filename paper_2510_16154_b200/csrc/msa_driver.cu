@@ -1184,6 +1184,205 @@ int msa_get_timing(msa_ctx* x, double* iter_ms, int64_t* iter_launches, double* 
   return MSA_OK;
 }
 
+
+// ------------------------------------------------------------------ NEXT-1: DAL (Algorithm 1)
+namespace {
+struct DalBuffers {
+  float* traj = nullptr;   // [M+1][C planes] (or 2 ping-pong slots for cost-only sweeps)
+  float *lam0 = nullptr, *lam1 = nullptr, *q = nullptr, *v = nullptr, *mu = nullptr;
+  double *partials = nullptr, *dev = nullptr;  // dev: [0] J, [2 + 2m] deps of step m
+  ~DalBuffers() {
+    void* ps[] = {traj, lam0, lam1, q, v, mu, partials, dev};
+    for (void* p : ps)
+      if (p) cudaFree(p);
+  }
+};
+
+int dal_check(msa_ctx* x, const msa_dal_params* d) {
+  if (!x || !d) return set_err(MSA_EINVAL, "NULL argument");
+  const msa_params& P = x->prm;
+  if (x->g.nb != 1 || P.world != 1) return set_err(MSA_EINVAL, "msa_dal needs one image on one rank");
+  if (P.channels > 4) return set_err(MSA_EINVAL, "msa_dal supports C <= 4");
+  if (d->steps < 1 || d->iters < 0 || d->max_ls < 1 || (d->cost != 0 && d->cost != 1))
+    return set_err(MSA_EINVAL, "bad DAL steps / iters / max_ls / cost");
+  if (!(d->sigma0 > 0) || !(d->b > 0 && d->b < 1) || !(d->c > 0 && d->c < 1))
+    return set_err(MSA_EINVAL, "DAL needs sigma0 > 0 and b, c in (0, 1)");
+  if (!(d->ex_lo > 0) || d->ex_hi < d->ex_lo || d->ec_lo < 0 || d->ec_hi < d->ec_lo)
+    return set_err(MSA_EINVAL, "bad box E (need 0 < ex_lo <= ex_hi, 0 <= ec_lo <= ec_hi)");
+  return MSA_OK;
+}
+
+size_t plane_floats(const msa_ctx* x) { return (size_t)x->g.C * x->g.plane; }
+
+int dal_alloc(msa_ctx* x, const msa_dal_params* d, const float* v, const float* mu, DalBuffers& B, bool full) {
+  const size_t pf = plane_floats(x), pf2 = 2 * pf;
+  const size_t slots = full ? (size_t)d->steps + 1 : 2;
+  CUDA_TRY(cudaMalloc((void**)&B.traj, sizeof(float) * pf * slots));
+  CUDA_TRY(cudaMalloc((void**)&B.lam0, sizeof(float) * pf));
+  CUDA_TRY(cudaMalloc((void**)&B.lam1, sizeof(float) * pf));
+  CUDA_TRY(cudaMalloc((void**)&B.q, sizeof(float) * pf2));
+  CUDA_TRY(cudaMalloc((void**)&B.v, sizeof(float) * pf2));
+  CUDA_TRY(cudaMalloc((void**)&B.mu, sizeof(float) * pf2));
+  CUDA_TRY(cudaMalloc((void**)&B.partials, sizeof(double) * 2 * (size_t)msa_dal_blocks(x->g)));
+  CUDA_TRY(cudaMalloc((void**)&B.dev, sizeof(double) * (2 + 2 * (size_t)d->steps)));
+  CUDA_TRY(cudaMemsetAsync(B.v, 0, sizeof(float) * pf2, x->stream));
+  CUDA_TRY(cudaMemsetAsync(B.mu, 0, sizeof(float) * pf2, x->stream));
+  CUDA_TRY(cudaMemsetAsync(B.traj, 0, sizeof(float) * pf * slots, x->stream));  // pad columns stay 0
+  const float* src[2] = {v, mu};
+  float* dst[2] = {B.v, B.mu};
+  for (int f = 0; f < 2; ++f) {
+    if (!src[f] || d->cost != 1) continue;
+    const size_t n = (size_t)x->g.H * x->g.W * 2 * x->g.C;
+    float* stage = x->c[1 - x->cur];
+    CUDA_TRY(cudaMemcpyAsync(stage, src[f], n * sizeof(float), cudaMemcpyHostToDevice, x->stream));
+    CUDA_TRY(msa_launch_unpack(x->g, 2 * x->g.C, stage, dst[f], x->stream));
+  }
+  return MSA_OK;
+}
+
+// forward sweep; full: keep every state in traj[m]; returns J (host) and leaves c(T) in the last slot
+int dal_forward(msa_ctx* x, const msa_dal_params* d, const double* eps, DalBuffers& B, bool full, double* J,
+                float** cT) {
+  const msa_params& P = x->prm;
+  const size_t pf = plane_floats(x);
+  CUDA_TRY(cudaMemcpyAsync(B.traj, x->I, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
+  for (int m = 0; m < d->steps; ++m) {
+    const float* cm = B.traj + (full ? (size_t)m : (size_t)(m & 1)) * pf;
+    float* cn = B.traj + (full ? (size_t)(m + 1) : (size_t)((m + 1) & 1)) * pf;
+    CUDA_TRY(msa_dal_step(x->g, x->hx, x->hy, P.dt, P.radius, P.kernel, x->NR, eps[2 * m], eps[2 * m + 1], cm, cn,
+                          x->stream));
+    ++x->launches;
+  }
+  float* last = B.traj + (full ? (size_t)d->steps : (size_t)(d->steps & 1)) * pf;
+  CUDA_TRY(msa_dal_terminal(x->g, d->cost, P.rho, x->hx, x->hy, P.alpha, last, x->I, B.v, B.mu, B.q,
+                            full ? B.lam0 : nullptr, B.partials, B.dev, x->stream));
+  x->launches += full ? 3 : 2;
+  double Jr = 0.0;
+  CUDA_TRY(cudaMemcpyAsync(&Jr, B.dev, sizeof(double), cudaMemcpyDeviceToHost, x->stream));
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  *J = Jr * x->hx * x->hy;
+  if (cT) *cT = last;
+  return MSA_OK;
+}
+
+// J and dJ/deps (grad [M][2]) by the discrete adjoint
+int dal_grad(msa_ctx* x, const msa_dal_params* d, const double* eps, DalBuffers& B, double* J, double* grad) {
+  const msa_params& P = x->prm;
+  const size_t pf = plane_floats(x);
+  int rc = dal_forward(x, d, eps, B, true, J, nullptr);
+  if (rc != MSA_OK) return rc;
+  float *lam = B.lam0, *lam2 = B.lam1;
+  for (int m = d->steps - 1; m >= 0; --m) {
+    CUDA_TRY(msa_dal_back(x->g, x->hx, x->hy, P.dt, P.radius, P.kernel, x->NR, eps[2 * m], eps[2 * m + 1],
+                          B.traj + (size_t)m * pf, lam, lam2, B.partials, B.dev + 2 + 2 * m, x->stream));
+    x->launches += 2;
+    std::swap(lam, lam2);
+  }
+  std::vector<double> de(2 * (size_t)d->steps);
+  CUDA_TRY(cudaMemcpyAsync(de.data(), B.dev + 2, sizeof(double) * de.size(), cudaMemcpyDeviceToHost, x->stream));
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  for (int m = 0; m < d->steps; ++m) {
+    grad[2 * m] = P.dt * de[2 * m] / eps[2 * m];  // the kernel sums dphi * eps_x/2 |delta|^2 (d . lam)
+    grad[2 * m + 1] = P.dt * de[2 * m + 1];
+  }
+  return MSA_OK;
+}
+
+void dal_project(const msa_dal_params* d, double* e) {
+  for (int m = 0; m < d->steps; ++m) {
+    e[2 * m] = std::min(std::max(e[2 * m], d->ex_lo), d->ex_hi);
+    e[2 * m + 1] = std::min(std::max(e[2 * m + 1], d->ec_lo), d->ec_hi);
+  }
+}
+}  // namespace
+
+int msa_dal_gradient(msa_ctx* x, const msa_dal_params* d, const double* eps, const float* v, const float* mu,
+                     double* J, double* grad) {
+  int rc = dal_check(x, d);
+  if (rc != MSA_OK) return rc;
+  if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
+  DalBuffers B;
+  if ((rc = dal_alloc(x, d, v, mu, B, true)) != MSA_OK) return rc;
+  std::vector<double> g(2 * (size_t)d->steps);
+  double Jv = 0.0;
+  if ((rc = dal_grad(x, d, eps, B, &Jv, g.data())) != MSA_OK) return rc;
+  if (J) *J = Jv;
+  if (grad) std::copy(g.begin(), g.end(), grad);
+  return MSA_OK;
+}
+
+int msa_dal(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, const float* mu, double* J_hist,
+            double* sigma_hist) {
+  int rc = dal_check(x, d);
+  if (rc != MSA_OK) return rc;
+  if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
+  DalBuffers B, Bc;
+  if ((rc = dal_alloc(x, d, v, mu, B, true)) != MSA_OK) return rc;
+  if ((rc = dal_alloc(x, d, v, mu, Bc, false)) != MSA_OK) return rc;
+  const int M2 = 2 * d->steps;
+  std::vector<double> D(M2), cand(M2);
+  dal_project(d, eps);
+  double sigma = d->sigma0;
+  auto cost = [&](const double* e, double* J) { return dal_forward(x, d, e, Bc, false, J, nullptr); };
+  for (int it = 0; it < d->iters; ++it) {
+    double J0 = 0.0;
+    if ((rc = dal_grad(x, d, eps, B, &J0, D.data())) != MSA_OK) return rc;
+    if (J_hist) J_hist[it] = J0;
+    double D2 = 0.0;
+    for (double g : D) D2 += g * g;
+    auto ok = [&](double t, bool* pass) {
+      for (int m = 0; m < M2; ++m) cand[m] = eps[m] - t * D[m];
+      dal_project(d, cand.data());
+      double J = 0.0;
+      int r = cost(cand.data(), &J);
+      *pass = J <= J0 - d->c * t * D2;
+      return r;
+    };
+    double tau = sigma, acc = -1.0;
+    int evals = 1;
+    bool pass = false;
+    if ((rc = ok(tau, &pass)) != MSA_OK) return rc;
+    if (pass) {
+      acc = tau;
+      while (evals < d->max_ls) {
+        ++evals;
+        if ((rc = ok(tau / d->b, &pass)) != MSA_OK) return rc;
+        if (!pass) break;
+        tau /= d->b;
+        acc = tau;
+      }
+    } else {
+      while (evals < d->max_ls) {
+        ++evals;
+        tau *= d->b;
+        if ((rc = ok(tau, &pass)) != MSA_OK) return rc;
+        if (pass) {
+          acc = tau;
+          break;
+        }
+      }
+    }
+    if (sigma_hist) sigma_hist[it] = acc;
+    if (acc > 0) {
+      sigma = acc;
+      for (int m = 0; m < M2; ++m) eps[m] -= sigma * D[m];
+      dal_project(d, eps);
+    } else {
+      sigma = tau;
+    }
+  }
+  // final state c(T; eps) -> c, cbar (Alg. 2 continues from it)
+  double Jf = 0.0;
+  float* cT = nullptr;
+  if ((rc = dal_forward(x, d, eps, Bc, false, &Jf, &cT)) != MSA_OK) return rc;
+  if (J_hist) J_hist[d->iters] = Jf;
+  const size_t pf = plane_floats(x);
+  CUDA_TRY(cudaMemcpyAsync(x->c[x->cur], cT, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
+  CUDA_TRY(cudaMemcpyAsync(x->cb[x->cur], cT, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  return MSA_OK;
+}
+
 int msa_sync(msa_ctx* x) {
   if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
   CUDA_TRY(cudaStreamSynchronize(x->stream));

@@ -104,3 +104,14 @@ cudaError_t msa_labels_merge(int nparts, int S_total, int W, int C, const int32_
                              cudaStream_t st, long long* launches);
 cudaError_t msa_labels_relabel(int npix, const int32_t* seg_of_pix, int seg_off, const int32_t* cl_of_seg,
                                int32_t* labels, cudaStream_t st);
+
+// NEXT-1 DAL building blocks (msa_dal.cu); one image, world 1, C <= 4.
+cudaError_t msa_dal_step(const MsaGeom& g, double hx, double hy, double dt, int R, int kernel, int NR, double eps_x,
+                         double eps_c, const float* c, float* c_out, cudaStream_t s);
+int msa_dal_blocks(const MsaGeom& g);
+cudaError_t msa_dal_back(const MsaGeom& g, double hx, double hy, double dt, int R, int kernel, int NR, double eps_x,
+                         double eps_c, const float* c, const float* lam, float* lam_out, double* partials,
+                         double* deps_dev, cudaStream_t s);
+cudaError_t msa_dal_terminal(const MsaGeom& g, int cost, double rho, double hx, double hy, double alpha,
+                             const float* c, const float* I, const float* v, const float* mu, float* q, float* lam,
+                             double* partials, double* J_dev, cudaStream_t s);

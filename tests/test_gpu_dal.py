@@ -1,0 +1,73 @@
+"""GPU DAL (msa.h msa_dal / msa_dal_gradient; msa_dal.cu) against the DAL
+oracle (pinned by finite differences in tests/test_oracle_dal.py): terminal state, cost and the
+discrete-adjoint gradient for both terminal costs, and Algorithm 1's iterates (Armijo descent,
+projection onto E, the same accepted steps as the oracle)."""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+msa = pytest.importorskip("paper_2510_16154_b200")
+
+
+def _case(H=16, W=16, C=3, R=15, M=12, seed=0, kernel=0):
+    rng = np.random.default_rng(seed)
+    blocks = np.repeat(np.repeat(rng.random((4, 4, C)), H // 4, 0), W // 4, 1)
+    I = np.clip(blocks + 0.05 * rng.standard_normal((H, W, C)), 0, 1).astype(np.float32)
+    h = 1.0 / (W - 1)
+    sp = dict(alpha=8.0 / h * 0.1, beta=1.0, radius=R, kernel=kernel, eps_x=0.0, eps_c=57.0, dt=0.25, rho=0.5,
+              gamma=0.5, kappa=1.0, tau=0.0, sigma=0.0, theta=1.0, iters_per_round=1, rounds=1)
+    eps = np.stack([rng.uniform(30.0, 300.0, M), rng.uniform(20.0, 120.0, M)], axis=1)
+    return rng, I, sp, eps
+
+
+def _oracle_params(I, sp):
+    H, W, C = I.shape
+    return oracle.Params.from_solver(H, W, C, sp)
+
+
+@pytest.mark.parametrize("cost,kernel", [(0, 0), (1, 0), (0, 1)])
+def test_dal_gradient_parity(cost, kernel):
+    rng, I, sp, eps = _case(seed=cost + 2 * kernel, kernel=kernel)
+    H, W, C = I.shape
+    M = eps.shape[0]
+    v = mu = None
+    if cost == 1:
+        v = (0.3 * rng.standard_normal((H, W, 2 * C))).astype(np.float32)
+        mu = (0.3 * rng.standard_normal((H, W, 2 * C))).astype(np.float32)
+    with msa.Solver(msa.Params.from_solver(1, H, W, C, sp), I[None]) as s:
+        J, g = s.dal_gradient(msa.DalParams(steps=M, cost=cost), eps, v, mu)
+    od = oracle.DalParams(M=M, cost=cost, rho=sp["rho"])
+    Jo, go = oracle.dal_gradient(_oracle_params(I, sp), od, eps, I.astype(np.float64), v, mu)
+    assert J == pytest.approx(Jo, rel=1e-5)
+    scale = np.max(np.abs(go), axis=0)
+    assert np.all(np.abs(g - go) <= 2e-3 * scale + 1e-9), (np.max(np.abs(g - go) / scale))
+
+
+def test_dal_terminal_state_and_cost():
+    rng, I, sp, eps = _case(seed=5, M=20)
+    H, W, C = I.shape
+    d = msa.DalParams(steps=20, iters=0)
+    with msa.Solver(msa.Params.from_solver(1, H, W, C, sp), I[None]) as s:
+        e, Jh, _ = s.dal(d, eps)
+        cT = s.get_field(msa.FIELD_C)[0]
+    Jo, cTo = oracle.dal_cost(_oracle_params(I, sp), oracle.DalParams(M=20), e, I.astype(np.float64),
+                              return_state=True)
+    assert Jh[0] == pytest.approx(Jo, rel=1e-5)
+    assert np.max(np.abs(cT - cTo)) <= 1e-5
+
+
+def test_dal_algorithm1_matches_oracle():
+    rng, I, sp, eps = _case(seed=7, M=10)
+    H, W, C = I.shape
+    kw = dict(iters=6, max_ls=25, sigma0=1e4, b=0.5, c=1e-4, ex_lo=2.0, ex_hi=1100.0, ec_lo=2.0, ec_hi=1100.0)
+    with msa.Solver(msa.Params.from_solver(1, H, W, C, sp), I[None]) as s:
+        e, Jh, sh = s.dal(msa.DalParams(steps=10, **kw), eps)
+    eo, Jho, sho = oracle.dal(_oracle_params(I, sp), oracle.DalParams(M=10, **kw), eps, I.astype(np.float64))
+    assert np.all(np.diff(Jh) <= 1e-9 * abs(Jh[0]))      # Armijo: J never increases
+    assert Jh[-1] < Jh[0]
+    assert np.all((e[:, 0] >= 2.0) & (e[:, 0] <= 1100.0) & (e[:, 1] >= 2.0) & (e[:, 1] <= 1100.0))
+    np.testing.assert_allclose(sh, sho, rtol=1e-12)       # same accepted steps
+    np.testing.assert_allclose(Jh, Jho, rtol=1e-4)
+    np.testing.assert_allclose(e, eo, rtol=2e-3, atol=1e-6)
