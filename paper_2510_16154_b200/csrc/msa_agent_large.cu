@@ -19,9 +19,12 @@ namespace {
 constexpr int TW = 32, TH = 8, NT = TW * TH;
 constexpr int CR = 16;  // neighbour rows per chunk
 
+// omtab == null (DAL, a control per step): 1 - a_delta = 1 - (exh_x dx^2 + exh_y dy^2) formed here,
+// exh = eps_x/2 h^2, exactly as the generic DAL step forms it (so the two agree bitwise).
 template <int C, int KER>
 __global__ void __launch_bounds__(NT) k_agent_large(MsaGeom g, MsaIterConsts K, int R, const float* __restrict__ omtab,
-                                                    const float* __restrict__ c, float* __restrict__ chalf) {
+                                                    float exh_x, float exh_y, const float* __restrict__ c,
+                                                    float* __restrict__ chalf) {
   extern __shared__ __align__(16) float smem[];
   const int SWL = TW + 2 * R;                  // staged columns x0-R .. x0+31+R
   float4* snb = reinterpret_cast<float4*>(smem);  // [CR][SWL]
@@ -59,7 +62,10 @@ __global__ void __launch_bounds__(NT) k_agent_large(MsaGeom g, MsaIterConsts K, 
     for (int e = threadIdx.x; e < ndy * OW; e += NT) {
       const int q = e / OW, dxi = e - q * OW;
       const int dy = dyl + q;
-      som[e] = (dy >= -R && dy <= R) ? omtab[(dy + R) * OW + dxi] : -1.0f;
+      const int dx = dxi - R;
+      som[e] = (dy < -R || dy > R) ? -1.0f
+               : omtab ? omtab[(dy + R) * OW + dxi]
+                       : 1.0f - __fmaf_rn(exh_x, (float)(dx * dx), exh_y * (float)(dy * dy));
     }
     __syncthreads();
     if (!own) continue;
@@ -89,8 +95,8 @@ __global__ void __launch_bounds__(NT) k_agent_large(MsaGeom g, MsaIterConsts K, 
 }
 
 template <int C>
-cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab, const float* c, float* ch,
-                     cudaStream_t s) {
+cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab, float exh_x, float exh_y,
+                     const float* c, float* ch, cudaStream_t s) {
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   const size_t smem = sizeof(float) * (4 * CR * (TW + 2 * R) + (CR + TH - 1) * (2 * R + 1));
@@ -102,14 +108,14 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const floa
       if (e != cudaSuccess) return e;
       attr[0] = true;
     }
-    k_agent_large<C, 0><<<grd, NT, smem, s>>>(g, K, R, omtab, c, ch);
+    k_agent_large<C, 0><<<grd, NT, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch);
   } else {
     if (!attr[1]) {
       cudaError_t e = cudaFuncSetAttribute(k_agent_large<C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
       if (e != cudaSuccess) return e;
       attr[1] = true;
     }
-    k_agent_large<C, 1><<<grd, NT, smem, s>>>(g, K, R, omtab, c, ch);
+    k_agent_large<C, 1><<<grd, NT, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch);
   }
   return cudaGetLastError();
 }
@@ -117,13 +123,160 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const floa
 }  // namespace
 
 cudaError_t msa_launch_agent_large(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab,
-                                   const float* c, float* chalf, cudaStream_t s) {
+                                   const float* c, float* chalf, cudaStream_t s, float exh_x, float exh_y) {
   if (R <= 8 || R > MSA_MAXR) return cudaErrorNotSupported;
   switch (g.C) {
-    case 1: return launch_c<1>(g, K, R, omtab, c, chalf, s);
-    case 2: return launch_c<2>(g, K, R, omtab, c, chalf, s);
-    case 3: return launch_c<3>(g, K, R, omtab, c, chalf, s);
-    case 4: return launch_c<4>(g, K, R, omtab, c, chalf, s);
+    case 1: return launch_c<1>(g, K, R, omtab, exh_x, exh_y, c, chalf, s);
+    case 2: return launch_c<2>(g, K, R, omtab, exh_x, exh_y, c, chalf, s);
+    case 3: return launch_c<3>(g, K, R, omtab, exh_x, exh_y, c, chalf, s);
+    case 4: return launch_c<4>(g, K, R, omtab, exh_x, exh_y, c, chalf, s);
     default: return cudaErrorNotSupported;
   }
+}
+
+// ------------------------------------------------------------------ DAL backward step, large supports
+// lam_out = lam + dt (dF/dc)^T lam and the per-block partials of <lam, dF/deps> (see msa_dal.cu's
+// k_dal_back: same per-term arithmetic in the same order - dy ascending, dx ascending - with the
+// colours and adjoints staged through shared memory as float4 in chunks of CR rows).
+namespace {
+template <int C>
+__global__ void __launch_bounds__(NT) k_dal_back_large(MsaGeom g, int R, int ker, float exh_x, float exh_y, float e_c,
+                                                       float eps_c, float inv_NR, float dt,
+                                                       const float* __restrict__ c, const float* __restrict__ lam,
+                                                       float* __restrict__ lam_out, double* __restrict__ partials) {
+  extern __shared__ __align__(16) float smem[];
+  const int SWL = TW + 2 * R, OW = 2 * R + 1;
+  float4* sc = reinterpret_cast<float4*>(smem);  // [CR][SWL]
+  float4* sl = sc + CR * SWL;                    // [CR][SWL]
+  float* sa = reinterpret_cast<float*>(sl + CR * SWL);  // [CR + TH - 1][OW]: eps_x/2 |delta|_h^2
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * TW, y0 = blockIdx.y * TH;
+  const int W = g.W, H = g.H;
+  const int x = x0 + tx, y = y0 + ty;
+  const bool own = x < W && y < H;
+  const int ylo = max(0, y0 - R), yhi = min(H, y0 + TH + R);
+  float ci[C], li[C], acc[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    ci[k] = own ? c[msa_idx(g, 0, k, C, y, x)] : 0.0f;
+    li[k] = own ? lam[msa_idx(g, 0, k, C, y, x)] : 0.0f;
+    acc[k] = 0.0f;
+  }
+  float sx = 0.0f, scc = 0.0f;
+  for (int yc = ylo; yc < yhi; yc += CR) {
+    const int nrow = min(CR, yhi - yc);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nrow * SWL; e += NT) {
+      const int r = e / SWL, col = e - r * SWL;
+      const int xx = x0 - R + col, yy = yc + r;
+      float v[4] = {0.0f, 0.0f, 0.0f, 0.0f}, l[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      if (xx >= 0 && xx < W) {
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          v[k] = c[msa_idx(g, 0, k, C, yy, xx)];
+          l[k] = lam[msa_idx(g, 0, k, C, yy, xx)];
+        }
+      }
+      sc[e] = make_float4(v[0], v[1], v[2], v[3]);
+      sl[e] = make_float4(l[0], l[1], l[2], l[3]);
+    }
+    const int dyl = yc - (y0 + TH - 1), ndy = nrow + TH - 1;
+    for (int e = threadIdx.x; e < ndy * OW; e += NT) {
+      const int q = e / OW, dx = e - q * OW - R, dy = dyl + q;
+      sa[e] = __fmaf_rn(exh_x, (float)(dx * dx), exh_y * (float)(dy * dy));
+    }
+    __syncthreads();
+    if (!own) continue;
+    for (int r = 0; r < nrow; ++r) {
+      const int dy = yc + r - y;
+      if (dy < -R || dy > R) continue;
+      int m = (int)sqrtf((float)(R * R - dy * dy));
+      while (m * m > R * R - dy * dy) --m;
+      while ((m + 1) * (m + 1) <= R * R - dy * dy) ++m;
+      const float4* crow = sc + r * SWL + tx + R;
+      const float4* lrow = sl + r * SWL + tx + R;
+      const float* arow = sa + (dy - dyl) * OW + R;
+      const int dxl = max(-m, -x), dxh = min(m, W - 1 - x);
+      for (int dx = dxl; dx <= dxh; ++dx) {
+        if (dx == 0 && dy == 0) continue;
+        const float4 cv = crow[dx], lv = lrow[dx];
+        const float cn[4] = {cv.x, cv.y, cv.z, cv.w}, ln[4] = {lv.x, lv.y, lv.z, lv.w};
+        const float a2 = arow[dx];
+        float d[C], dl[C], s2 = 0.0f, ddl = 0.0f, dli = 0.0f;
+#pragma unroll
+        for (int k = 0; k < C; ++k) {
+          d[k] = __fsub_rn(cn[k], ci[k]);
+          dl[k] = __fsub_rn(ln[k], li[k]);
+          s2 = __fmaf_rn(d[k], d[k], s2);
+          ddl = __fmaf_rn(d[k], dl[k], ddl);
+          dli = __fmaf_rn(d[k], li[k], dli);
+        }
+        const float t = fmaxf(1.0f - __fmaf_rn(e_c, s2, a2), 0.0f);
+        if (t <= 0.0f) continue;
+        const float t2 = __fmul_rn(t, t), t4 = __fmul_rn(t2, t2), t3 = __fmul_rn(t2, t);
+        const float ph = __fmul_rn(t4, __fmaf_rn(-4.0f, t, ker == 0 ? 5.0f : 3.0f));
+        const float rr = 1.0f - t;
+        const float dph = ker == 0 ? __fmul_rn(-20.0f * rr, t3) : __fmul_rn(t3, __fmaf_rn(-20.0f, rr, 8.0f));
+        const float f = __fmul_rn(eps_c, __fmul_rn(dph, ddl));
+#pragma unroll
+        for (int k = 0; k < C; ++k) acc[k] = __fmaf_rn(ph, dl[k], __fmaf_rn(f, d[k], acc[k]));
+        sx = __fmaf_rn(__fmul_rn(dph, a2), dli, sx);
+        scc = __fmaf_rn(__fmul_rn(dph, 0.5f * s2), dli, scc);
+      }
+    }
+  }
+  double sums[2] = {0.0, 0.0};
+  if (own) {
+#pragma unroll
+    for (int k = 0; k < C; ++k) lam_out[msa_idx(g, 0, k, C, y, x)] = __fmaf_rn(dt * inv_NR, acc[k], li[k]);
+    sums[0] = (double)sx * inv_NR;
+    sums[1] = (double)scc * inv_NR;
+  }
+  // block reduction (fixed order) -> partials[block][2]
+  __shared__ double red[8][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    double v = sums[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[warp][q] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+    partials[((long long)blockIdx.y * gridDim.x + blockIdx.x) * 2 + threadIdx.x] = t;
+  }
+}
+}  // namespace
+
+int msa_dal_back_large_blocks(const MsaGeom& g) { return ((g.W + TW - 1) / TW) * ((g.H + TH - 1) / TH); }
+
+cudaError_t msa_dal_back_large(const MsaGeom& g, int R, int kernel, float exh_x, float exh_y, float eps_c,
+                               float inv_NR, float dt, const float* c, const float* lam, float* lam_out,
+                               double* partials, cudaStream_t s) {
+  if (R <= 8 || R > MSA_MAXR) return cudaErrorNotSupported;
+  const size_t smem = sizeof(float) * (8 * CR * (TW + 2 * R) + (CR + TH - 1) * (2 * R + 1));
+  dim3 grd((g.W + TW - 1) / TW, (g.H + TH - 1) / TH);
+  const float e_c = 0.5f * eps_c;
+#define DAL_BL(CC)                                                                                                  \
+  case CC: {                                                                                                        \
+    static bool attr = false;                                                                                       \
+    if (!attr) {                                                                                                    \
+      cudaError_t e = cudaFuncSetAttribute(k_dal_back_large<CC>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
+                                           160 * 1024);                                                             \
+      if (e != cudaSuccess) return e;                                                                               \
+      attr = true;                                                                                                  \
+    }                                                                                                               \
+    k_dal_back_large<CC><<<grd, NT, smem, s>>>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR, dt, c, lam, lam_out, \
+                                               partials);                                                           \
+    break;                                                                                                          \
+  }
+  switch (g.C) {
+    DAL_BL(1) DAL_BL(2) DAL_BL(3) DAL_BL(4)
+    default: return cudaErrorNotSupported;
+  }
+#undef DAL_BL
+  return cudaGetLastError();
 }

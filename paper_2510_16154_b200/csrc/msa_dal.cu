@@ -12,6 +12,9 @@
 // while the supports of the control box E reach the whole image (R up to 64).
 // The host loop (msa_driver.cu, msa_dal) runs the forward sweep (storing the trajectory), the
 // backward sweep, and the two-way Armijo search on J, with deterministic fp64 reductions.
+#include <cstdlib>
+#include <cstring>
+
 #include "msa_internal.h"
 
 namespace {
@@ -264,9 +267,25 @@ static DalConsts make_consts(const MsaDalConstsHost& h, double eps_x, double eps
     default: return cudaErrorNotSupported;                         \
   }
 
+static bool dal_large(int R, int C) {
+  static const bool force_generic = getenv("MSA_DAL_GENERIC") != nullptr;  // A/B and test hook
+  return R > 8 && C <= 4 && !force_generic;
+}
+
 cudaError_t msa_dal_step(const MsaGeom& g, double hx, double hy, double dt, int R, int kernel, int NR, double eps_x,
                          double eps_c, const float* c, float* c_out, cudaStream_t s) {
   const DalConsts Q = make_consts(MsaDalConstsHost{hx, hy, dt, R, kernel, NR}, eps_x, eps_c);
+  if (dal_large(R, g.C)) {  // chunked shared-memory n-body kernel, same arithmetic and order
+    MsaIterConsts K;
+    memset(&K, 0, sizeof(K));
+    K.dt_NR = Q.dt_NR;
+    K.e_c = Q.e_c;
+    K.kernel = kernel;
+    MsaGeom gg = g;
+    gg.k1_lo = 0;
+    gg.k1_hi = 0;
+    return msa_launch_agent_large(gg, K, R, nullptr, c, c_out, s, Q.ex_half_hx2, Q.ex_half_hy2);
+  }
   dim3 blk(32, 8), grd((g.W + 31) / 32, (g.H + 7) / 8);
   if (kernel == 0) {
     DAL_DISPATCH(k_dal_step, g, Q, c, c_out)
@@ -283,6 +302,13 @@ cudaError_t msa_dal_back(const MsaGeom& g, double hx, double hy, double dt, int 
                          double eps_c, const float* c, const float* lam, float* lam_out, double* partials,
                          double* deps_dev, cudaStream_t s) {
   const DalConsts Q = make_consts(MsaDalConstsHost{hx, hy, dt, R, kernel, NR}, eps_x, eps_c);
+  if (dal_large(R, g.C)) {
+    cudaError_t e = msa_dal_back_large(g, R, kernel, Q.ex_half_hx2, Q.ex_half_hy2, Q.eps_c, Q.inv_NR, (float)dt, c,
+                                       lam, lam_out, partials, s);
+    if (e != cudaSuccess) return e;
+    k_sum_partials<<<1, 32, 0, s>>>(partials, msa_dal_back_large_blocks(g), 2, deps_dev);
+    return cudaGetLastError();
+  }
   dim3 blk(32, 8), grd((g.W + 31) / 32, (g.H + 7) / 8);
   DAL_DISPATCH(k_dal_back, g, Q, c, lam, lam_out, partials, (float)dt)
   k_sum_partials<<<1, 32, 0, s>>>(partials, msa_dal_blocks(g), 2, deps_dev);

@@ -22,7 +22,13 @@ cudaError_t msa_launch_iter_generic(const MsaGeom& g, const MsaIterConsts& K, co
 // Step 1 alone for large supports (msa_agent_large.cu): 8 < R <= 64, C <= 4; omtab = 1 - a_delta for
 // every (dx, dy) in [-R, R]^2 ([dy + R][dx + R]); writes c_half.
 cudaError_t msa_launch_agent_large(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab,
-                                   const float* c, float* chalf, cudaStream_t s);
+                                   const float* c, float* chalf, cudaStream_t s, float exh_x = 0.0f,
+                                   float exh_y = 0.0f);
+// DAL backward step for large supports (msa_agent_large.cu): one image, partials [blocks][2]
+int msa_dal_back_large_blocks(const MsaGeom& g);
+cudaError_t msa_dal_back_large(const MsaGeom& g, int R, int kernel, float exh_x, float exh_y, float eps_c,
+                               float inv_NR, float dt, const float* c, const float* lam, float* lam_out,
+                               double* partials, cudaStream_t s);
 
 // Single-loop linearised ADMM iteration (msa.h MSA_SCHEME_LINEARISED_ADMM), any C: reads c, mu, I,
 // writes c_out, mu_out.

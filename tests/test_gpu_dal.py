@@ -9,6 +9,8 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 msa = pytest.importorskip("paper_2510_16154_b200")
+import os as _os
+HERE_DIR = _os.path.dirname(_os.path.abspath(__file__))
 
 
 def _case(H=16, W=16, C=3, R=15, M=12, seed=0, kernel=0):
@@ -71,3 +73,41 @@ def test_dal_algorithm1_matches_oracle():
     np.testing.assert_allclose(sh, sho, rtol=1e-12)       # same accepted steps
     np.testing.assert_allclose(Jh, Jho, rtol=1e-4)
     np.testing.assert_allclose(e, eo, rtol=2e-3, atol=1e-6)
+
+
+@pytest.mark.parametrize("R,C,kernel", [(15, 3, 0), (12, 1, 1), (20, 4, 0)])
+def test_dal_large_support_kernels_bitwise(R, C, kernel, tmp_path):
+    """R > 8 runs the forward and backward steps on the chunked shared-memory kernels; they have the
+    generic DAL kernels' arithmetic and summation order: bitwise-equal cost and gradient."""
+    import json
+    import os
+    import subprocess
+    import sys
+    script = r"""
+import json, sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2510_16154_b200 as msa
+spec = json.loads(sys.argv[1])
+rng = np.random.default_rng(spec["seed"])
+H, W, C, R, M = spec["H"], spec["W"], spec["C"], spec["R"], spec["M"]
+I = rng.random((1, H, W, C), dtype=np.float32)
+h = 1.0 / (W - 1)
+sp = dict(alpha=0.8 / h, beta=1.0, radius=R, kernel=spec["kernel"], eps_x=0.0, eps_c=57.0, dt=0.25, rho=0.5,
+          gamma=0.5, kappa=1.0, tau=0.0, sigma=0.0, theta=1.0, iters_per_round=1, rounds=1)
+eps = np.stack([rng.uniform(8.0, 200.0, M), rng.uniform(20.0, 120.0, M)], axis=1)
+with msa.Solver(msa.Params.from_solver(1, H, W, C, sp), I) as s:
+    J, g = s.dal_gradient(msa.DalParams(steps=M), eps)
+np.savez(sys.argv[2], J=np.array([J]), g=g)
+""" % os.path.dirname(HERE_DIR)
+    spec = dict(seed=R + C, H=29, W=37, C=C, R=R, M=6, kernel=kernel)
+    outs = []
+    for generic in (False, True):
+        env = dict(os.environ)
+        env.pop("MSA_DAL_GENERIC", None)
+        if generic:
+            env["MSA_DAL_GENERIC"] = "1"
+        out = str(tmp_path / f"g{int(generic)}.npz")
+        subprocess.run([sys.executable, "-c", script, json.dumps(spec), out], check=True, env=env)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0]["J"], outs[1]["J"])
+    assert np.array_equal(outs[0]["g"], outs[1]["g"])
