@@ -21,7 +21,8 @@ constexpr int CR = 16;  // neighbour rows per chunk
 
 // omtab == null (DAL, a control per step): 1 - a_delta = 1 - (exh_x dx^2 + exh_y dy^2) formed here,
 // exh = eps_x/2 h^2, exactly as the generic DAL step forms it (so the two agree bitwise).
-template <int C, int KER>
+// SC: the scaled form (MsaIterConsts::scaled; omtab then holds -om/e_c); the DAL uses the direct one.
+template <int C, int KER, bool SC>
 __global__ void __launch_bounds__(NT) k_agent_large(MsaGeom g, MsaIterConsts K, int R, const float* __restrict__ omtab,
                                                     float exh_x, float exh_y, const float* __restrict__ c,
                                                     float* __restrict__ chalf) {
@@ -85,13 +86,25 @@ __global__ void __launch_bounds__(NT) k_agent_large(MsaGeom g, MsaIterConsts K, 
         float cj[C];
 #pragma unroll
         for (int k = 0; k < C; ++k) cj[k] = nv[k];
-        msa_agent_term<C, KER>(ci, cj, omr[dx], K.e_c, acc);
+        if constexpr (SC)
+          msa_agent_term_s<C, KER>(ci, cj, omr[dx], K.m4, acc);
+        else
+          msa_agent_term<C, KER>(ci, cj, omr[dx], K.e_c, acc);
       }
     }
   }
   if (!own) return;
 #pragma unroll
-  for (int k = 0; k < C; ++k) chalf[msa_idx(g, b, k, C, y, x)] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+  for (int k = 0; k < C; ++k) chalf[msa_idx(g, b, k, C, y, x)] = __fmaf_rn(SC ? K.dt_s : K.dt_NR, acc[k], ci[k]);
+}
+
+template <typename F>
+cudaError_t go(F* kern, dim3 grd, size_t smem, const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab,
+               float exh_x, float exh_y, const float* c, float* ch, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+  if (e != cudaSuccess) return e;
+  kern<<<grd, NT, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch);
+  return cudaGetLastError();
 }
 
 template <int C>
@@ -100,24 +113,12 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const floa
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   const size_t smem = sizeof(float) * (4 * CR * (TW + 2 * R) + (CR + TH - 1) * (2 * R + 1));
-  static bool attr[2] = {false, false};
   dim3 grd((g.W + TW - 1) / TW, (nr + TH - 1) / TH, g.nb);
-  if (K.kernel == 0) {
-    if (!attr[0]) {
-      cudaError_t e = cudaFuncSetAttribute(k_agent_large<C, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      if (e != cudaSuccess) return e;
-      attr[0] = true;
-    }
-    k_agent_large<C, 0><<<grd, NT, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch);
-  } else {
-    if (!attr[1]) {
-      cudaError_t e = cudaFuncSetAttribute(k_agent_large<C, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      if (e != cudaSuccess) return e;
-      attr[1] = true;
-    }
-    k_agent_large<C, 1><<<grd, NT, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch);
-  }
-  return cudaGetLastError();
+  const bool sc = K.scaled && omtab;
+  if (K.kernel == 0 && sc) return go(k_agent_large<C, 0, true>, grd, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
+  if (K.kernel == 0) return go(k_agent_large<C, 0, false>, grd, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
+  if (sc) return go(k_agent_large<C, 1, true>, grd, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
+  return go(k_agent_large<C, 1, false>, grd, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
 }
 
 }  // namespace

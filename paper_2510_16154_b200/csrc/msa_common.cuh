@@ -45,6 +45,14 @@ struct MsaIterConsts {
   float beta, beta2;
   float tau, tau_alpha, inv_1ta, theta;  // step 3 (R7, R21)
   float rho;        // single-loop scheme (NEXT-2): mu+ = Pi_beta(mu - rho grad c)
+  // Scaled step-1 form (scaled = 1, every K1 variant): t = e_c t' with t' = max(om/e_c - |d|^2, 0),
+  // so phi(t) = e_c^4 t'^4 (q0 - 4 e_c t') and e_c^4 moves into the Euler step size. The offset
+  // tables then hold nom = -om/e_c and |d|^2 + nom is one fma chain: one FP32 operation less per
+  // interaction term than t = max(om - e_c |d|^2, 0). Used for e_c in [1e-3, 1e3] (fp32 range of
+  // t'^4 and e_c^4); otherwise scaled = 0 and every variant uses the direct form.
+  int scaled;
+  float dt_s;       // dt / N_R * e_c^4                (fp64, rounded once)
+  float m4;         // -4 e_c (exact)
 };
 
 // phi as a function of t = max(1 - r, 0) (eq:kernel PAPER.md:259-267; R3, R21):
@@ -70,6 +78,26 @@ __device__ __forceinline__ void msa_agent_term(const float (&ci)[C], const float
   for (int k = 1; k < C; ++k) s = __fmaf_rn(d[k], d[k], s);
   float t = fmaxf(__fmaf_rn(-e_c, s, om), 0.0f);
   float w = msa_phi_t<KER>(t);
+#pragma unroll
+  for (int k = 0; k < C; ++k) acc[k] = __fmaf_rn(w, d[k], acc[k]);
+}
+
+// The same term in the scaled form (MsaIterConsts::scaled): nom = -om/e_c, m4 = -4 e_c;
+// acc accumulates phi / e_c^4 (d), the caller applies dt_s = dt/N_R e_c^4.
+template <int C, int KER>
+__device__ __forceinline__ void msa_agent_term_s(const float (&ci)[C], const float (&cj)[C], float nom, float m4,
+                                                 float (&acc)[C]) {
+  float d[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) d[k] = __fsub_rn(cj[k], ci[k]);
+  float s = __fmaf_rn(d[0], d[0], nom);
+#pragma unroll
+  for (int k = 1; k < C; ++k) s = __fmaf_rn(d[k], d[k], s);
+  const float t = fmaxf(-s, 0.0f);
+  const float t2 = __fmul_rn(t, t);
+  const float t4 = __fmul_rn(t2, t2);
+  const float q = __fmaf_rn(m4, t, KER == 0 ? 5.0f : 3.0f);
+  const float w = __fmul_rn(t4, q);
 #pragma unroll
   for (int k = 0; k < C; ++k) acc[k] = __fmaf_rn(w, d[k], acc[k]);
 }

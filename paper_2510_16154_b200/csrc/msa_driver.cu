@@ -86,6 +86,7 @@ struct msa_ctx {
   msa_params prm;
   double hx, hy, eps_x, tau, sigma, theta, rho_cur;
   int NR = 0;
+  int scaled = 0;  // MsaIterConsts::scaled
   MsaOffsetTable T;
   MsaGeom g;
   int image0 = 0;
@@ -124,6 +125,17 @@ struct msa_ctx {
   int32_t* lab_count = nullptr;
   float* lab_pal = nullptr;
   int lab_pal_cap = 0;
+  // msa_solve as a replayed CUDA graph (single-GPU / batch mode, timing off): one captured solve
+  // per starting state (ping-pong set, rho, position in the round), at most two live
+  struct SolveGraph {
+    cudaGraphExec_t exec = nullptr;
+    int cur0 = 0, cur1 = 0;
+    double rho0 = 0, rho1 = 0;
+    int64_t phase = 0, iters_base = 0, launches_delta = 0;
+    int32_t rounds_base = 0;
+  } graphs[2];
+  int n_graphs = 0;
+  bool graphs_off = false;
 };
 
 namespace {
@@ -172,8 +184,19 @@ int validate(const msa_params* p) {
 struct Derived {
   double hx, hy, eps_x, tau, sigma, theta;
   int NR;
+  int scaled;  // MsaIterConsts::scaled
   MsaOffsetTable T;
 };
+
+// Scaled step-1 form (msa_common.cuh MsaIterConsts::scaled) for e_c = eps_c/2 in [1e-3, 1e3];
+// MSA_NO_SCALED=1 (test hook) keeps the direct form (then only the generic kernels run).
+bool use_scaled(double eps_c) {
+  static const bool off = getenv("MSA_NO_SCALED") != nullptr;
+  const double e_c = 0.5 * eps_c;
+  return !off && e_c >= 1e-3 && e_c <= 1e3;
+}
+// the offset constant as the kernels consume it: om = 1 - a_delta, or -om/e_c in the scaled form
+float om_entry(double om, double eps_c, int scaled) { return scaled ? (float)(-om / (0.5 * eps_c)) : (float)om; }
 
 int derive(const msa_params* p, Derived* d) {
   d->hx = p->width > 1 ? 1.0 / (double)(p->width - 1) : 1.0;    // R5
@@ -196,6 +219,7 @@ int derive(const msa_params* p, Derived* d) {
   const int R = p->radius;
   d->NR = 0;
   d->T.n = 0;
+  d->scaled = use_scaled(p->eps_c) ? 1 : 0;
   // offset order: dx ascending; within a column the even dy ascending, then the odd dy
   // ascending (the order of K1's two parity passes over a cached column). Both kernels sum
   // the terms of a pixel in this order, so they agree bitwise.
@@ -212,6 +236,7 @@ int derive(const msa_params* p, Derived* d) {
       d->T.dx[d->T.n] = dx;
       d->T.dy[d->T.n] = dy;
       d->T.om[d->T.n] = (float)om;
+      d->T.oms[d->T.n] = om_entry(om, p->eps_c, d->scaled);
       ++d->T.n;
     }
   return MSA_OK;
@@ -289,6 +314,10 @@ MsaIterConsts iter_consts(const msa_ctx* x, double rho) {
   K.inv_1ta = (float)(1.0 / (1.0 + x->tau * p.alpha));
   K.theta = (float)x->theta;
   K.rho = (float)rho;
+  K.scaled = x->scaled;
+  const double e_c = 0.5 * p.eps_c;
+  K.dt_s = (float)(p.dt / (double)x->NR * (e_c * e_c) * (e_c * e_c));
+  K.m4 = (float)(-4.0 * e_c);
   return K;
 }
 
@@ -657,9 +686,99 @@ void free_ctx(msa_ctx* x) {
   if (x->lab_buf) cudaFree(x->lab_buf);
   if (x->lab_count) cudaFree(x->lab_count);
   if (x->lab_pal) cudaFree(x->lab_pal);
+  for (int i = 0; i < x->n_graphs; ++i) cudaGraphExecDestroy(x->graphs[i].exec);
   if (x->own_ws && x->ws) cudaFree(x->ws);
   if (x->own_stream && x->stream) cudaStreamDestroy(x->stream);
   delete x;
+}
+
+// --- msa_solve through a CUDA graph. The solve is rounds x K K1 launches plus three launches
+// per round; at small sizes (cfg 1, 64^2) each K1 is a few microseconds and the host launch
+// rate bounds the solve. The first solve from a given starting state (ping-pong set, rho, phase
+// in the round) is captured and instantiated, later ones replay it. Kernel arguments are
+// pointers into the context's fixed workspace and constants that depend only on that state,
+// except the round / iteration numbers baked into the record kernel, which msa_solve shifts
+// after the fetch. Not used in rows mode (NCCL calls and the comm stream), with timing on, or
+// with MSA_NO_GRAPH set; any capture failure falls back to direct launches for this context.
+bool graph_ok(const msa_ctx* x) {
+  static const bool off = getenv("MSA_NO_GRAPH") != nullptr;
+  const msa_params& P = x->prm;
+  return !off && !x->graphs_off && !x->timing && !(P.world > 1 && P.shard == MSA_SHARD_ROWS) &&
+         P.rounds <= REC_CAP && (int64_t)P.rounds * P.iters_per_round > 0;
+}
+
+// Runs one solve's steps through a (possibly new) graph. Returns MSA_OK with *done = false when
+// the caller should launch directly instead. *shift_round / *shift_iters: what to add to the
+// round / iters fields of the records this solve produces.
+int solve_graph(msa_ctx* x, int64_t n, bool* done, int32_t* shift_round, int64_t* shift_iters) {
+  *done = false;
+  *shift_round = 0;
+  *shift_iters = 0;
+  int rc;
+  if (x->rec_pending && (rc = fetch_records(x)) != MSA_OK) return rc;  // the graph writes records from 0
+  const int K = x->prm.iters_per_round;
+  msa_ctx::SolveGraph* G = nullptr;
+  for (int i = 0; i < x->n_graphs; ++i) {
+    msa_ctx::SolveGraph& c = x->graphs[i];
+    if (c.cur0 == x->cur && c.rho0 == x->rho_cur && c.phase == x->iters_done % K) G = &c;
+  }
+  if (!G) {
+    // capture: do_steps enqueues into the capturing stream and advances the host state
+    const int cur0 = x->cur;
+    const double rho0 = x->rho_cur;
+    const int64_t it0 = x->iters_done, l0 = x->launches;
+    const int32_t r0 = x->rounds_done;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(x->stream, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      rc = do_steps(x, n);
+      cudaError_t e2 = cudaStreamEndCapture(x->stream, &graph);
+      if (rc == MSA_OK && e2 == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+      else e = e2 != cudaSuccess ? e2 : cudaErrorUnknown;
+      if (graph) cudaGraphDestroy(graph);
+    }
+    const int cur1 = x->cur;
+    const double rho1 = x->rho_cur;
+    const int64_t dl = x->launches - l0;
+    // restore the host state either way; on success the replay below advances it again
+    x->cur = cur0; x->rho_cur = rho0; x->iters_done = it0; x->launches = l0; x->rounds_done = r0;
+    x->rec_pending = 0;
+    if (e != cudaSuccess || rc != MSA_OK) {
+      cudaGetLastError();
+      x->graphs_off = true;
+      return MSA_OK;
+    }
+    if (x->n_graphs == 2) {  // evict the older entry
+      cudaGraphExecDestroy(x->graphs[0].exec);
+      x->graphs[0] = x->graphs[1];
+      x->n_graphs = 1;
+    }
+    msa_ctx::SolveGraph& c = x->graphs[x->n_graphs++];
+    c.exec = exec;
+    c.cur0 = cur0;
+    c.cur1 = cur1;
+    c.rho0 = rho0;
+    c.rho1 = rho1;
+    c.phase = it0 % K;
+    c.iters_base = it0;
+    c.rounds_base = r0;
+    c.launches_delta = dl;
+    G = &c;
+  }
+  CUDA_TRY(cudaGraphLaunch(G->exec, x->stream));
+  const int64_t rounds = (x->iters_done + n) / K - x->iters_done / K;
+  *shift_round = x->rounds_done - G->rounds_base;
+  *shift_iters = x->iters_done - G->iters_base;
+  x->cur = G->cur1;
+  x->rho_cur = G->rho1;
+  x->iters_done += n;
+  x->rounds_done += (int32_t)rounds;
+  x->rec_pending += (int)rounds;
+  x->launches += G->launches_delta;
+  if (rounds) x->halo_mu_dirty = true;
+  *done = true;
+  return MSA_OK;
 }
 
 }  // namespace
@@ -734,6 +853,7 @@ int msa_init(const msa_params* params, const float* image, int image_on_device, 
   x->prm.nccl_id = nullptr;
   x->hx = d.hx; x->hy = d.hy; x->eps_x = d.eps_x; x->tau = d.tau; x->sigma = d.sigma; x->theta = d.theta;
   x->NR = d.NR;
+  x->scaled = d.scaled;
   x->T = d.T;
   Part pt = partition(params);
   Layout L = layout(params, pt);
@@ -780,7 +900,8 @@ int msa_init(const msa_params* params, const float* image, int image_on_device, 
     if (e == cudaSuccess && x->T.n > 0)
       e = cudaMemcpyAsync(x->d_off, offs.data(), sizeof(int2) * x->T.n, cudaMemcpyHostToDevice, x->stream);
     if (e == cudaSuccess && x->T.n > 0)
-      e = cudaMemcpyAsync(x->d_om, x->T.om, sizeof(float) * x->T.n, cudaMemcpyHostToDevice, x->stream);
+      e = cudaMemcpyAsync(x->d_om, x->scaled ? x->T.oms : x->T.om, sizeof(float) * x->T.n, cudaMemcpyHostToDevice,
+                          x->stream);
     std::vector<float> omtab;
     if (e == cudaSuccess && params->radius > 8) {  // same formula and rounding as the offset table
       const int R = params->radius, OW = 2 * R + 1;
@@ -788,7 +909,7 @@ int msa_init(const msa_params* params, const float* image, int image_on_device, 
       for (int dy = -R; dy <= R; ++dy)
         for (int dx = -R; dx <= R; ++dx) {
           const double a = 0.5 * x->eps_x * ((dx * x->hx) * (dx * x->hx) + (dy * x->hy) * (dy * x->hy));
-          omtab[(size_t)(dy + R) * OW + dx + R] = (float)(1.0 - a);
+          omtab[(size_t)(dy + R) * OW + dx + R] = om_entry(1.0 - a, params->eps_c, x->scaled);
         }
       e = cudaMemcpyAsync(x->d_omtab, omtab.data(), sizeof(float) * omtab.size(), cudaMemcpyHostToDevice, x->stream);
     }
@@ -829,10 +950,19 @@ int msa_step(msa_ctx* x, int32_t n_iters) {
 int msa_solve(msa_ctx* x, msa_round_stats* stats) {
   if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
   const size_t before = x->stats.size() + x->rec_pending;
-  int rc = do_steps(x, (int64_t)x->prm.rounds * x->prm.iters_per_round);
-  if (rc != MSA_OK) return rc;
+  const int64_t n = (int64_t)x->prm.rounds * x->prm.iters_per_round;
+  bool graphed = false;
+  int32_t shift_round = 0;
+  int64_t shift_iters = 0;
+  int rc;
+  if (graph_ok(x) && (rc = solve_graph(x, n, &graphed, &shift_round, &shift_iters)) != MSA_OK) return rc;
+  if (!graphed && (rc = do_steps(x, n)) != MSA_OK) return rc;
   if ((rc = fetch_records(x)) != MSA_OK) return rc;
   CUDA_TRY(cudaStreamSynchronize(x->stream));
+  for (size_t r = before; graphed && r < x->stats.size(); ++r) {
+    x->stats[r].round += shift_round;
+    x->stats[r].iters += shift_iters;
+  }
   int diverged = -1;
   for (size_t r = before; r < x->stats.size(); ++r) {
     if (stats) stats[r - before] = x->stats[r];

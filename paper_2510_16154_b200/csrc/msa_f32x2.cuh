@@ -33,4 +33,10 @@ __device__ __forceinline__ f2 relu2(f2 v) {
   return pk(fmaxf(a, 0.0f), fmaxf(b, 0.0f));
 }
 
+__device__ __forceinline__ f2 relu2n(f2 v) {  // max(-v, 0) per lane
+  float a, b;
+  upk(v, a, b);
+  return pk(fmaxf(-a, 0.0f), fmaxf(-b, 0.0f));
+}
+
 }  // namespace msa_f32x2

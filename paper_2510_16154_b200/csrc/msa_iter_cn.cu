@@ -10,7 +10,7 @@
 //     ([C][TH+2R][40]) and the cbar tile with one row below / above ([C][TH+2][40]); out-of-image
 //     boxes are zero-filled and masked by coordinates (R20).
 //   * Step 1 (eq:MAsystem, windowed, R2): neighbours from shared memory, the driver's offset order
-//     and msa_agent_term, so results equal the generic kernel bit for bit.
+//     and msa_agent_term_s, so results equal the generic kernel bit for bit.
 //   * Step 2 (dual ascent + projection, R7): p+ for the tile and its low-side halo (33 x TH+1), with
 //     p and mu read straight from global memory (coalesced: a warp reads consecutive columns of
 //     one component row), written to shared memory (reusing the c tile).
@@ -99,8 +99,8 @@ __global__ void __launch_bounds__(NT, CN_OCC)
   mbar_wait(&bar, 0);
 
   const int y = y0 + ty;
-  // ---- step 1: agent Euler step (the driver's offset order, msa_agent_term: bitwise equal to the
-  // generic kernel)
+  // ---- step 1: agent Euler step (the driver's offset order, msa_agent_term_s - the scaled form:
+  // bitwise equal to the generic kernel)
   float chalf[C];
   {
     float ci[C], acc[C];
@@ -117,10 +117,10 @@ __global__ void __launch_bounds__(NT, CN_OCC)
       const float* src = sc + (ty + R + dy) * CW + CX + tx + dx;
 #pragma unroll
       for (int k = 0; k < C; ++k) cj[k] = src[k * SH * CW];
-      msa_agent_term<C, KER>(ci, cj, T.om[o], K.e_c, acc);
+      msa_agent_term_s<C, KER>(ci, cj, T.om[o], K.m4, acc);
     }
 #pragma unroll
-    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_s, acc[k], ci[k]);
   }
   __syncthreads();  // the c tile is dead: sq reuses it
 
@@ -242,14 +242,14 @@ cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const M
                                const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
-  if (g.C != 16 || R < 1 || R > 4 || T.n > CN_MAXOFF) return cudaErrorNotSupported;
+  if (g.C != 16 || R < 1 || R > 4 || T.n > CN_MAXOFF || !K.scaled) return cudaErrorNotSupported;
   CnOffsets off;
   off.n = T.n;
   for (int o = 0; o < T.n; ++o) {
     if (T.dx[o] < -R || T.dx[o] > R || T.dy[o] < -R || T.dy[o] > R) return cudaErrorNotSupported;
     off.dx[o] = (signed char)T.dx[o];
     off.dy[o] = (signed char)T.dy[o];
-    off.om[o] = T.om[o];
+    off.om[o] = T.oms[o];
   }
   CnKey key;
   memset(&key, 0, sizeof(key));

@@ -6,7 +6,8 @@
 //             (group 0), then - landing while step 1 computes - cbar (+1 halo), p and mu
 //             (+1 low-side halo) and I (group 1);
 //   step 1    the agent interaction over the interior disc D°_R (ring offsets carry phi = 0
-//             for eps_x >= the default and are skipped exactly). Each thread caches one
+//             for eps_x >= the default and are skipped exactly), in the scaled form
+//             (msa_common.cuh MsaIterConsts::scaled: 13 FP32 operations per term). Each thread caches one
 //             neighbour column in registers and evaluates two vertically adjacent pixels per
 //             instruction with packed f32x2 arithmetic (FFMA2/FMUL2/FADD2: on B200 these do not
 //             raise the FP32 peak but halve the issue slots, so loads, FMNMX and address
@@ -113,7 +114,7 @@ __device__ __forceinline__ void prefetch(float* dst, const float* src_img, long 
 // out-of-image neighbours (column mask cm, row validity from the global row of cache row k).
 template <int R, int P, bool MASK, int PAR>
 __device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx, int m, const FastOm& om, int& o,
-                                            f2 NE, f2 M4, f2 QC, float cm, int yk0, int H,
+                                            f2 M4, f2 QC, float cm, int yk0, int H,
                                             const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
   constexpr int SH = NSTRIP * P + 2 * R;
   constexpr int NQ = (P + 2 * R) / 2;
@@ -141,10 +142,10 @@ __device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx,
       f2 d[C];
 #pragma unroll
       for (int k = 0; k < C; ++k) d[k] = sub2(Cp[q][k], ci[j][k]);
-      f2 sq = mul2(d[0], d[0]);
+      f2 sq = fma2(d[0], d[0], OM);  // |d|^2 - om/e_c (scaled form, msa_agent_term_s)
 #pragma unroll
       for (int k = 1; k < C; ++k) sq = fma2(d[k], d[k], sq);
-      const f2 t = relu2(fma2(NE, sq, OM));
+      const f2 t = relu2n(sq);
       const f2 t2 = mul2(t, t);
       const f2 t4 = mul2(t2, t2);
       const f2 qv = fma2(M4, t, QC);
@@ -157,10 +158,10 @@ __device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx,
 }
 
 template <int R, int P, bool MASK>
-__device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const FastOm& om, float e_c, float qc,
+__device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const FastOm& om, float m4, float qc,
                                             int lx, int strip, int x, int ybase, int W, int H,
                                             const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
-  const f2 NE = pk(-e_c, -e_c), M4 = pk(-4.0f, -4.0f), QC = pk(qc, qc);
+  const f2 M4 = pk(m4, m4), QC = pk(qc, qc);
   int o = 0;  // offset index in the kernel's order; compile-time constant after unrolling
 #pragma unroll
   for (int dx = -R; dx <= R; ++dx) {
@@ -170,11 +171,11 @@ __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const 
     const float cm = (!MASK || (x + dx >= 0 && x + dx < W)) ? 1.0f : 0.0f;
     const int yk0 = ybase - m;
     if ((m & 1) == 0) {
-      column_pass<R, P, MASK, 0>(s, dx, m, om, o, NE, M4, QC, cm, yk0, H, ci, acc);
-      column_pass<R, P, MASK, 1>(s, dx, m, om, o, NE, M4, QC, cm, yk0, H, ci, acc);
+      column_pass<R, P, MASK, 0>(s, dx, m, om, o, M4, QC, cm, yk0, H, ci, acc);
+      column_pass<R, P, MASK, 1>(s, dx, m, om, o, M4, QC, cm, yk0, H, ci, acc);
     } else {
-      column_pass<R, P, MASK, 1>(s, dx, m, om, o, NE, M4, QC, cm, yk0, H, ci, acc);
-      column_pass<R, P, MASK, 0>(s, dx, m, om, o, NE, M4, QC, cm, yk0, H, ci, acc);
+      column_pass<R, P, MASK, 1>(s, dx, m, om, o, M4, QC, cm, yk0, H, ci, acc);
+      column_pass<R, P, MASK, 0>(s, dx, m, om, o, M4, QC, cm, yk0, H, ci, acc);
     }
   }
 }
@@ -217,6 +218,10 @@ __global__ void __launch_bounds__(NT, Occ<P>::blocks)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  // programmatic dependent launch: everything above overlaps the previous kernel's tail; nothing
+  // below may touch global memory before that kernel has completed (its c+ is our c, and we
+  // overwrite the buffers it reads)
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (threadIdx.x == 0) {
     const int ys = y0 - g.row0 + g.G;  // stored-row index of global row y0
     mbar_expect_tx(&bars[0], (unsigned)(sizeof(float) * C * SH * SW));
@@ -233,6 +238,7 @@ __global__ void __launch_bounds__(NT, Occ<P>::blocks)
     tma_load3(sI, &tm.I, x0, ys, b * C, &bars[1]);
   }
   mbar_wait(&bars[0], 0);
+  asm volatile("griddepcontrol.launch_dependents;");  // the next iteration may start launching
 
   // ---- step 1: agent Euler step for P rows (P/2 packed pixel pairs) of column x
   f2 ci[P / 2][C], acc[P / 2][C];
@@ -247,10 +253,10 @@ __global__ void __launch_bounds__(NT, Occ<P>::blocks)
   const float qc = K.kernel == 0 ? 5.0f : 3.0f;
   const bool interior = x0 - R >= 0 && x0 + TW + R <= W && y0 - R >= 0 && y0 + TH + R <= H;
   if (interior)
-    agent_phase<R, P, false>(sc, om, K.e_c, qc, lx, strip, x, ybase, W, H, ci, acc);
+    agent_phase<R, P, false>(sc, om, K.m4, qc, lx, strip, x, ybase, W, H, ci, acc);
   else
-    agent_phase<R, P, true>(sc, om, K.e_c, qc, lx, strip, x, ybase, W, H, ci, acc);
-  const f2 DT = pk(K.dt_NR, K.dt_NR);
+    agent_phase<R, P, true>(sc, om, K.m4, qc, lx, strip, x, ybase, W, H, ci, acc);
+  const f2 DT = pk(K.dt_s, K.dt_s);
   float chalf[P][C];
 #pragma unroll
   for (int j = 0; j < P / 2; ++j)
@@ -467,8 +473,18 @@ cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   dim3 grd((g.W + TW - 1) / TW, (nr + S::TH - 1) / S::TH, g.nb);
-  k_iter_fast_c3<R, P, LIN><<<grd, NT, S::bytes, s>>>(g, K, om, tm);
-  return cudaGetLastError();
+  static const bool pdl = getenv("MSA_NO_PDL") == nullptr;  // A/B hook
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grd;
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = S::bytes;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k_iter_fast_c3<R, P, LIN>, g, K, om, tm);
 }
 
 template <int R, bool LIN>
@@ -484,7 +500,7 @@ cudaError_t launch_c3(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
   for (int o = 0; o < T.n; ++o) {
     const int idx = kernel_order_index<R>(T.dx[o], T.dy[o]);
     if (idx < 0 || idx <= prev) return cudaErrorNotSupported;  // the driver's order must match
-    om.v[idx] = T.om[o];
+    om.v[idx] = T.oms[o];
     prev = idx;
   }
   static const int rows_per_thread = getenv("MSA_K1_P") ? atoi(getenv("MSA_K1_P")) : 4;  // A/B hook
@@ -502,7 +518,7 @@ cudaError_t launch_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffse
   *launched = 0;
   // test hook: MSA_FORCE_GENERIC=1 selects the generic kernel (bitwise-identical results)
   static const bool force_generic = getenv("MSA_FORCE_GENERIC") != nullptr;
-  if (g.C != 3 || force_generic) return cudaErrorNotSupported;
+  if (g.C != 3 || force_generic || !K.scaled) return cudaErrorNotSupported;  // scaled form only
   // every active offset must lie in the interior disc (true for eps_x >= the default)
   for (int o = 0; o < T.n; ++o)
     if (T.dx[o] * T.dx[o] + T.dy[o] * T.dy[o] >= R * R) return cudaErrorNotSupported;

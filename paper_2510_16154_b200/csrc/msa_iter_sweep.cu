@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(NW * 32, OCC)
 #pragma unroll
     for (int k = 0; k < C; ++k) S[i][k] = pk(0.0f, 0.0f);
   float qyp[C] = {0.0f, 0.0f, 0.0f};  // p+_y of the row below the next row to finalise
-  const f2 NE = pk(-K.e_c, -K.e_c), M4 = pk(-4.0f, -4.0f);
+  const f2 M4 = pk(K.m4, K.m4);  // scaled form (msa_agent_term_s)
   const float qcs = K.kernel == 0 ? 5.0f : 3.0f;
   const f2 QC = pk(qcs, qcs);
 
@@ -296,10 +296,10 @@ __global__ void __launch_bounds__(NW * 32, OCC)
               f2 d[C];
 #pragma unroll
               for (int k = 0; k < C; ++k) d[k] = sub2(np[a + 4][k], ci[jj][k]);
-              f2 sq = mul2(d[0], d[0]);
+              f2 sq = fma2(d[0], d[0], OM);  // |d|^2 - om/e_c
 #pragma unroll
               for (int k = 1; k < C; ++k) sq = fma2(d[k], d[k], sq);
-              const f2 t = relu2(fma2(NE, sq, OM));
+              const f2 t = relu2n(sq);
               const f2 t2 = mul2(t, t);
               const f2 t4 = mul2(t2, t2);
               const f2 w = mul2(t4, fma2(M4, t, QC));
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(NW * 32, OCC)
           const float dv = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
           float s0, s1;
           upk(S[r >> 1][k], s0, s1);
-          const float chalf = __fmaf_rn(K.dt_NR, (r & 1) ? s1 : s0, cr[(k * P + r) * RW + cl]);
+          const float chalf = __fmaf_rn(K.dt_s, (r & 1) ? s1 : s0, cr[(k * P + r) * RW + cl]);
           float cp, cbp;
           msa_prox_extrap(K, chalf, dv, sm.I[(k * P + r) * LW + cl], cp, cbp);
           if (st) {
@@ -544,8 +544,8 @@ bool build_om(const MsaOffsetTable& T, SweepOm* om) {
       const int a = find(dx, dy), b = find(-dx, -dy);
       if ((a < 0) != (b < 0)) return false;  // the window must be symmetric
       if (a >= 0) {
-        if (T.om[a] != T.om[b]) return false;
-        om->v[n] = T.om[a];
+        if (T.oms[a] != T.oms[b]) return false;
+        om->v[n] = T.oms[a];
       }
       ++n;
     }
@@ -569,8 +569,8 @@ cudaError_t msa_launch_iter_sweep(const MsaGeom& g, const MsaIterConsts& K, cons
                                   float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
   if (g.C != 3 || g.k1_lo != 0 || msa_k1_hi(g) != g.nrows) return cudaErrorNotSupported;  // whole slab only
-  // the sentinel needs eps_c > 0: with e_c * (1e18)^2 >= 1e6 an out-of-image partner has t < 0
-  if (!(K.e_c >= 1e-30f)) return cudaErrorNotSupported;
+  // scaled form only; an out-of-image partner (sentinel colour 1e18) has |d|^2 >= 1e36 > om/e_c, so t = 0
+  if (!K.scaled) return cudaErrorNotSupported;
   for (int o = 0; o < T.n; ++o)
     if (T.dx[o] * T.dx[o] + T.dy[o] * T.dy[o] >= R * R) return cudaErrorNotSupported;
   cudaError_t e;

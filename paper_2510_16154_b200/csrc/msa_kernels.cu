@@ -46,10 +46,14 @@ __global__ void __launch_bounds__(256) k_iter_generic(MsaGeom g, MsaIterConsts K
       float cj[C];
 #pragma unroll
       for (int k = 0; k < C; ++k) cj[k] = c[msa_idx(g, b, k, C, jj, ii)];
-      msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
+      if (K.scaled)
+        msa_agent_term_s<C, KER>(ci, cj, om[o], K.m4, acc);
+      else
+        msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
     }
+    const float dts = K.scaled ? K.dt_s : K.dt_NR;
 #pragma unroll
-    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(dts, acc[k], ci[k]);
   }
   // step 2: p+ at (i,j), (i-1,j), (i,j-1); the last two only feed the divergence
   float qx[3][C], qy[3][C];
@@ -143,10 +147,14 @@ __global__ void __launch_bounds__(256) k_iter_lin_generic(MsaGeom g, MsaIterCons
       float cj[C];
 #pragma unroll
       for (int k = 0; k < C; ++k) cj[k] = c[msa_idx(g, b, k, C, jj, ii)];
-      msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
+      if (K.scaled)
+        msa_agent_term_s<C, KER>(ci, cj, om[o], K.m4, acc);
+      else
+        msa_agent_term<C, KER>(ci, cj, om[o], K.e_c, acc);
     }
+    const float dts = K.scaled ? K.dt_s : K.dt_NR;
 #pragma unroll
-    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_NR, acc[k], ci[k]);
+    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(dts, acc[k], ci[k]);
   }
   float mbx[3][C], mby[3][C], qx0[C], qy0[C];
   const int pi[3] = {i, i - 1, i};

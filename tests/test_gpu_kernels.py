@@ -1,5 +1,7 @@
 """K1 variants against the generic kernel (msa_kernels.cu), over tile-aligned, ragged and tiny
 shapes, every specialised radius, both kernel forms, and across a multiplier round:
+  * every variant evaluates step 1 in the scaled form (msa_common.cuh MsaIterConsts::scaled); the
+    direct form (MSA_NO_SCALED=1, generic kernel) agrees with it to fp32 rounding;
   * the tiled kernel (msa_iter_fast.cu) has the generic kernel's per-pixel arithmetic and term order:
     bitwise-identical fields;
   * the pair-symmetric sweep kernel (msa_iter_sweep.cu) evaluates each pair weight once and sums the
@@ -19,10 +21,13 @@ pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(spec, variant: str, tmp_path, seg: int = 0, split: bool = False):
-    out = str(tmp_path / f"{variant}_{seg}_{int(split)}.npz")
+def _run(spec, variant: str, tmp_path, seg: int = 0, split: bool = False, direct: bool = False):
+    out = str(tmp_path / f"{variant}_{seg}_{int(split)}_{int(direct)}.npz")
     env = dict(os.environ)
     env.pop("MSA_FORCE_GENERIC", None)
+    env.pop("MSA_NO_SCALED", None)
+    if direct:
+        env["MSA_NO_SCALED"] = "1"
     env["MSA_K1"] = variant
     if split:
         env["MSA_K1_SPLIT"] = "1"
@@ -109,3 +114,17 @@ def test_k1_interior_boundary_split_bitwise(shape, R, variant, tmp_path):
     b = _run(spec, variant, tmp_path, split=True)
     for k in ("c", "cbar", "p", "mu"):
         assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("shape,R,ker", [((1, 64, 32, 3), 5, 0), ((1, 37, 29, 3), 3, 1), ((2, 40, 36, 16), 3, 0),
+                                        ((1, 48, 40, 3), 12, 0), ((1, 30, 33, 1), 2, 0)])
+def test_scaled_form_matches_direct_form(shape, R, ker, tmp_path):
+    # t = e_c t', phi(t) = e_c^4 phi-part(t'): the same weights up to fp32 rounding of the
+    # rescaled offset constants and of e_c^4 dt / N_R
+    spec = _spec(shape, R, ker)
+    a = _run(spec, "tile", tmp_path)
+    b = _run(spec, "tile", tmp_path, direct=True)
+    for k in ("c", "cbar", "p", "mu"):
+        scale = max(1.0, float(np.max(np.abs(b[k]))))
+        err = float(np.max(np.abs(a[k] - b[k]))) / scale
+        assert err <= 2e-5, (k, err)
