@@ -283,9 +283,10 @@ def main():
 
     # roofline of the dominant kernel K1 (fused iteration), DESIGN.md §5:
     #  bytes: 44*C algorithmic bytes per pixel-iteration (11 C-float fields read or written)
-    #  ALU:   n_off*(3C+5) + 27C + 2 FP32 pipe operations per pixel-iteration (the interaction term
-    #         sub/square-sum/t/phi/accumulate per active offset, plus steps 2-3); peak = 148 SMs x
-    #         128 FP32 lanes x clocks.max.sm (B200_PROFILING.md unit counts).
+    #  ALU:   n_off*(3C+4) + 27C + 2 FP32 pipe operations per pixel-iteration (the interaction term
+    #         in the scaled form - C subs, C square-sum fmas starting from -om/e_c, t^2, t^4, the
+    #         kernel polynomial, w, C accumulate fmas - per active offset, plus steps 2-3); peak =
+    #         148 SMs x 128 FP32 lanes x clocks.max.sm (B200_PROFILING.md unit counts).
     k1_avg_ms = tim["iter_ms"] / max(tim["iter_launches"], 1)  # per iteration (rows mode: 3 launches)
     alg_bytes = 44.0 * C * own_px
     achieved = alg_bytes / (k1_avg_ms * 1e-3) / 1e9
@@ -293,7 +294,7 @@ def main():
     traffic, _tr = _k1_traffic()
     k1_share = tim["iter_ms"] / ms_local if ms_local > 0 else None
     n_off = info.active_offsets
-    alg_ops = (n_off * (3 * C + 5) + 27 * C + 2) * own_px
+    alg_ops = (n_off * (3 * C + 4) + 27 * C + 2) * own_px
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
     alu_peak = sm_count * 128 * 1965e6 / 1e12  # T FP32 lane-ops/s at clocks.max.sm
     alu_achieved = alg_ops / (k1_avg_ms * 1e-3) / 1e12
