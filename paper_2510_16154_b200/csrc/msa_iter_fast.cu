@@ -2,20 +2,22 @@
 //
 // One CTA = one 32 x (8P) tile of output pixels, 256 threads: lane = column, 8 strips of P
 // rows. Per pixel it does SURVEY §8(a) steps 1-3 in one pass:
-//   prefetch  16-byte cp.async (zero-filled outside the stored rows) of the c tile + R halo
-//             (group 0), then - landing while step 1 computes - cbar (+1 halo), p and mu
-//             (+1 low-side halo) and I (group 1);
+//   loads     one elected thread issues TMA bulk-tensor loads (zero-filled outside the tensor) of
+//             the c tile + R halo on mbarrier 0, then - landing while step 1 computes - cbar
+//             (+1 halo), p and mu (+1 low-side halo) and I on mbarrier 1;
 //   step 1    the agent interaction over the interior disc D°_R (ring offsets carry phi = 0
 //             for eps_x >= the default and are skipped exactly), in the scaled form
-//             (msa_common.cuh MsaIterConsts::scaled: 13 FP32 operations per term). Each thread caches one
-//             neighbour column in registers and evaluates two vertically adjacent pixels per
-//             instruction with packed f32x2 arithmetic (FFMA2/FMUL2/FADD2: on B200 these do not
-//             raise the FP32 peak but halve the issue slots, so loads, FMNMX and address
-//             arithmetic issue in the gaps). A column is processed in two parity passes
+//             (msa_common.cuh MsaIterConsts::scaled: 13 FP32 operations per term). Each thread
+//             caches one neighbour column in registers and evaluates two vertically adjacent
+//             pixels per instruction with packed f32x2 arithmetic (FFMA2/FMUL2/FADD2: on B200
+//             these do not raise the FP32 peak but halve the issue slots, so loads, FMNMX and
+//             address arithmetic issue in the gaps). A column is processed in two parity passes
 //             (neighbour pairs starting on even / odd cache rows) so only one set of packed
 //             pairs is live. Border tiles run a masked variant (w x in-image mask);
 //   step 2    p+ for the tile and its low-side halo (row y0-1, column x0-1) from smem;
-//   step 3    div p+, prox fidelity, extrapolation; coalesced stores of c+, cbar+, p+.
+//   step 3    div p+, prox fidelity, extrapolation; c+, cbar+, p+ staged in smem and written by
+//             three TMA tensor stores (clipped at the image and slab edges).
+// Launched with programmatic dependent launch (the prologue overlaps the previous iteration).
 // Term order per pixel: dx ascending; within a column the even dy ascending, then the odd dy
 // ascending - the order of the driver's offset table, so the generic kernel gives
 // bitwise-identical results and no result depends on tile position (P19).
@@ -82,32 +84,6 @@ struct Smem {
   static constexpr int total = I_off + al(C * TH * TW);
   static constexpr size_t bytes = sizeof(float) * total;
 };
-
-// 16-byte cp.async of a [NM][ROWS][4*N4] window of a planar field (zero fill outside the
-// stored rows or the pitch). Thread t copies float4 column t % N4 of rows t / N4 + k NT / N4.
-template <int NM, int ROWS, int N4>
-__device__ __forceinline__ void prefetch(float* dst, const float* src_img, long long plane, const MsaGeom& g, int gy0,
-                                         int gx0) {
-  constexpr int RSTEP = NT / N4;
-  const int q = threadIdx.x % N4, r0 = threadIdx.x / N4;
-  if (r0 >= RSTEP) return;
-  const int gx = gx0 + 4 * q;
-  const bool okx = gx >= 0 && gx + 4 <= g.pitch;
-  const int nstored = g.nrows + 2 * g.G;
-  const int lr0 = gy0 - g.row0 + g.G;  // stored-row index of global row gy0
-  const unsigned dbase = (unsigned)__cvta_generic_to_shared(dst) + 16u * q;
-#pragma unroll
-  for (int m = 0; m < NM; ++m) {
-#pragma unroll
-    for (int r = r0; r < ROWS; r += RSTEP) {
-      const int lr = lr0 + r;
-      const bool ok = okx && lr >= 0 && lr < nstored;
-      const float* src = ok ? src_img + (long long)m * plane + (long long)lr * g.pitch + gx : src_img;
-      const unsigned d = dbase + 16u * (unsigned)((m * ROWS + r) * N4);
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(ok ? 16 : 0));
-    }
-  }
-}
 
 // One parity pass over the neighbour pairs of column dx: cache Cp[q] = rows (2q + PAR,
 // 2q + PAR + 1) of the column (cache row k = strip row k - m). MASK: zero the weight of
