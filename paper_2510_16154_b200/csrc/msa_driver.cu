@@ -32,25 +32,19 @@ static int set_err(int code, const char* fmt, ...) {
 
 // ------------------------------------------------------------------ NCCL (loaded on demand)
 namespace {
-struct NcclApi {
+struct NcclApi : MsaNcclFns {
   bool tried = false, ok = false;
-  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
-  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
-  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*GroupStart)() = nullptr;
-  ncclResult_t (*GroupEnd)() = nullptr;
-  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-  const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 NcclApi g_nccl;
 
 bool nccl_load() {
   if (g_nccl.tried) return g_nccl.ok;
   g_nccl.tried = true;
+  if (getenv("MSA_NCCL_LOOPBACK")) {  // test hook: in-process ranks (msa_nccl_loopback.cu)
+    static_cast<MsaNcclFns&>(g_nccl) = msa_nccl_loopback();
+    g_nccl.ok = true;
+    return true;
+  }
   // prefer the NCCL already mapped into the process (torch's), else the system one
   void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
   if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);

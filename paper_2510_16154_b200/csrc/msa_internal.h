@@ -2,6 +2,7 @@
 // (msa_driver.cu) and the kernel translation units. Not part of the ABI.
 #pragma once
 #include <cuda_runtime.h>
+#include <nccl.h>
 #include <stdint.h>
 
 #include "msa_common.cuh"
@@ -122,3 +123,20 @@ cudaError_t msa_dal_back(const MsaGeom& g, double hx, double hy, double dt, int 
 cudaError_t msa_dal_terminal(const MsaGeom& g, int cost, double rho, double hx, double hy, double alpha,
                              const float* c, const float* I, const float* v, const float* mu, float* q, float* lam,
                              double* partials, double* J_dev, cudaStream_t s);
+
+// The NCCL entry points the driver uses (loaded from libnccl.so.2 on demand), and an in-process
+// loopback implementation of them (msa_nccl_loopback.cu; test hook MSA_NCCL_LOOPBACK=1).
+struct MsaNcclFns {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+MsaNcclFns msa_nccl_loopback();
