@@ -184,7 +184,8 @@ int msa_solve(msa_ctx* ctx, msa_round_stats* stats);
  *       64-bit fixed-point sums, m = (double)sum llrint(c 2^32) / count * 2^-32);
  *  (iii) label = rank of the cluster's smallest member index j*W + i; palette = cluster mean.
  * labels: int32 [nimages][rows][W] of this rank's images, rows = H, or this rank's slab rows in
- * rows mode; n_clusters: int32 [nimages]; palette: float32 [nimages][max_k][C] or NULL.
+ * rows mode; n_clusters: int32 [nimages]; palette: float32 [nimages][max_k][C] or NULL (rows
+ * k < min(n_clusters, max_k) hold the means of clusters k, the remaining rows are zero).
  * Rows mode with world > 1: every rank runs stage (i) on its slab (the row above
  * is refreshed by a halo exchange first), the slabs' segment tables and boundary rows meet by
  * ncclAllGather, every rank runs the same merge (cross-slab edges, exact integer sums, stages

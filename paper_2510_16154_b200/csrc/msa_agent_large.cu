@@ -22,8 +22,10 @@ constexpr int CR = 16;  // neighbour rows per chunk
 // omtab == null (DAL, a control per step): 1 - a_delta = 1 - (exh_x dx^2 + exh_y dy^2) formed here,
 // exh = eps_x/2 h^2, exactly as the generic DAL step forms it (so the two agree bitwise).
 // SC: the scaled form (MsaIterConsts::scaled; omtab then holds -om/e_c); the DAL uses the direct one.
-template <int C, int KER, bool SC>
-__global__ void __launch_bounds__(NT) k_agent_large(MsaGeom g, MsaIterConsts K, int R, const float* __restrict__ omtab,
+// TH2: tile rows (8, or 2 when the image has too few 32 x 8 tiles to fill the GPU - DAL images are
+// small); every pixel's terms are summed in the same order either way.
+template <int C, int KER, bool SC, int TH2>
+__global__ void __launch_bounds__(32 * TH2) k_agent_large(MsaGeom g, MsaIterConsts K, int R, const float* __restrict__ omtab,
                                                     float exh_x, float exh_y, const float* __restrict__ c,
                                                     float* __restrict__ chalf) {
   extern __shared__ __align__(16) float smem[];
@@ -32,6 +34,7 @@ __global__ void __launch_bounds__(NT) k_agent_large(MsaGeom g, MsaIterConsts K, 
   float* som = smem + 4 * CR * SWL;            // [CR + TH - 1][2R+1]: 1 - a_delta for dy = yr - y
   const int OW = 2 * R + 1;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  constexpr int TH = TH2, NT = 32 * TH2;
   const int x0 = blockIdx.x * TW, y0 = g.row0 + g.k1_lo + blockIdx.y * TH, b = blockIdx.z;
   const int W = g.W, H = g.H;
   const int x = x0 + tx, y = y0 + ty;
@@ -99,12 +102,24 @@ __global__ void __launch_bounds__(NT) k_agent_large(MsaGeom g, MsaIterConsts K, 
 }
 
 template <typename F>
-cudaError_t go(F* kern, dim3 grd, size_t smem, const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab,
-               float exh_x, float exh_y, const float* c, float* ch, cudaStream_t s) {
+cudaError_t go(F* kern, int th, int nr, size_t smem, const MsaGeom& g, const MsaIterConsts& K, int R,
+               const float* omtab, float exh_x, float exh_y, const float* c, float* ch, cudaStream_t s) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   if (e != cudaSuccess) return e;
-  kern<<<grd, NT, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch);
+  dim3 grd((g.W + TW - 1) / TW, (nr + th - 1) / th, g.nb);
+  kern<<<grd, 32 * th, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch);
   return cudaGetLastError();
+}
+
+template <int C, int TH2>
+cudaError_t launch_th(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab, float exh_x, float exh_y,
+                      const float* c, float* ch, cudaStream_t s, int nr) {
+  const size_t smem = sizeof(float) * (4 * CR * (TW + 2 * R) + (CR + TH2 - 1) * (2 * R + 1));
+  const bool sc = K.scaled && omtab;
+  if (K.kernel == 0 && sc) return go(k_agent_large<C, 0, true, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
+  if (K.kernel == 0) return go(k_agent_large<C, 0, false, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
+  if (sc) return go(k_agent_large<C, 1, true, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
+  return go(k_agent_large<C, 1, false, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
 }
 
 template <int C>
@@ -112,13 +127,16 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const floa
                      const float* c, float* ch, cudaStream_t s) {
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
-  const size_t smem = sizeof(float) * (4 * CR * (TW + 2 * R) + (CR + TH - 1) * (2 * R + 1));
-  dim3 grd((g.W + TW - 1) / TW, (nr + TH - 1) / TH, g.nb);
-  const bool sc = K.scaled && omtab;
-  if (K.kernel == 0 && sc) return go(k_agent_large<C, 0, true>, grd, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
-  if (K.kernel == 0) return go(k_agent_large<C, 0, false>, grd, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
-  if (sc) return go(k_agent_large<C, 1, true>, grd, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
-  return go(k_agent_large<C, 1, false>, grd, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
+  // 32 x 8 tiles unless that leaves SMs idle (fewer than two tiles per SM): then 32 x 2
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const long long tiles8 = (long long)((g.W + TW - 1) / TW) * ((nr + TH - 1) / TH) * g.nb;
+  if (tiles8 < 2LL * sms) return launch_th<C, 2>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr);
+  return launch_th<C, TH>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr);
 }
 
 }  // namespace

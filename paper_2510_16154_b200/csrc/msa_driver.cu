@@ -1125,6 +1125,8 @@ int msa_labels(msa_ctx* x, float delta, int32_t* labels, int32_t* n_clusters, fl
     int32_t* ldev = out_on_device ? labels + N * b : x->lab_buf;
     int32_t* cdev = out_on_device ? n_clusters + b : x->lab_count;
     float* pdev = max_k > 0 ? (out_on_device ? palette + (size_t)b * max_k * C : x->lab_pal) : nullptr;
+    if (pdev)  // rows past the cluster count are zero (not the previous image's)
+      CUDA_TRY(cudaMemsetAsync(pdev, 0, sizeof(float) * (size_t)max_k * C, x->stream));
     long long launches = 0;
     if (nparts >= 2) {
       int rc = labels_parts(x, b, delta, nparts, ldev, cdev, pdev, max_k);

@@ -33,8 +33,22 @@ def run_one(p, I, delta, max_k):
         info = s.query()
         f = {k: s.get_field(w) for k, w in FIELDS}
         lab, cnt, pal = s.labels(delta, max_k)
-        return dict(row0=info.row0, nrows=info.nrows, stats=st, fields=f, lab=lab, cnt=cnt, pal=pal,
-                    launches=info.launches)
+        return dict(row0=info.row0, nrows=info.nrows, image0=info.image0, nimages=info.nimages, stats=st, fields=f,
+                    lab=lab, cnt=cnt, pal=pal, launches=info.launches)
+
+
+def check_batch(spec, base, I, ref, delta, max_k, world):
+    # images split across ranks, no collective: each rank's images equal the one-context run's
+    out = [run_one(msa.Params(**base, shard=msa.SHARD_BATCH, world=world, rank=r), I, delta, max_k)
+           for r in range(world)]
+    assert sum(o["nimages"] for o in out) == I.shape[0]
+    for o in out:
+        sl = slice(o["image0"], o["image0"] + o["nimages"])
+        for k, _ in FIELDS:
+            assert np.array_equal(o["fields"][k], ref["fields"][k][sl]), ("batch", world, k)
+        assert np.array_equal(o["lab"], ref["lab"][sl]) and np.array_equal(o["cnt"], ref["cnt"][sl])
+        assert np.array_equal(o["pal"], ref["pal"][sl])
+    return {"fields": "bitwise", "labels": "identical", "images": [o["nimages"] for o in out]}
 
 
 def main():
@@ -46,6 +60,11 @@ def main():
     delta, max_k = spec.get("delta", 0.1), 64
     ref = run_one(msa.Params(**base), I, delta, max_k)
     report = {"shape": spec["shape"], "worlds": {}}
+    if spec.get("shard") == "batch":
+        for world in spec["worlds"]:
+            report["worlds"][str(world)] = check_batch(spec, base, I, ref, delta, max_k, world)
+        print(json.dumps(report), flush=True)
+        return
     for world in spec["worlds"]:
         nid = msa.nccl_unique_id()
         out = [None] * world

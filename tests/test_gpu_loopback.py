@@ -57,3 +57,12 @@ def test_row_slabs_serial_exchange_and_generic_kernel():
     spec = dict(seed=5, shape=list(shape), worlds=[2], params=_params(shape[2], R))
     assert _run(spec, MSA_NO_OVERLAP="1")["worlds"]["2"]["fields"] == "bitwise"
     assert _run(spec, MSA_K1="generic")["worlds"]["2"]["fields"] == "bitwise"
+
+
+def test_batch_shards_match_one_context():
+    # shard = batch (cfg 5's mode): no data-path collective; every rank's images equal the
+    # one-context run bit for bit, uneven splits included (5 images over 2 and 3 ranks)
+    shape, R = (5, 40, 36, 16), 3
+    spec = dict(seed=11, shape=list(shape), worlds=[2, 3], shard="batch", params=_params(shape[2], R))
+    rep = _run(spec)
+    assert rep["worlds"]["3"]["images"] in ([2, 2, 1], [2, 1, 2], [1, 2, 2])
