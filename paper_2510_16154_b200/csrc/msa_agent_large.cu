@@ -12,6 +12,9 @@
 // The sum runs over dy ascending, then dx ascending (not the generic kernel's order), so results
 // agree with it to fp32 rounding. Output: c_half = c + dt/N_R F, consumed by the generic kernel's
 // steps 2-3 (msa_launch_iter_generic with chalf_in).
+#include <algorithm>
+#include <cstdlib>
+
 #include "msa_internal.h"
 
 namespace {
@@ -24,10 +27,13 @@ constexpr int CR = 16;  // neighbour rows per chunk
 // SC: the scaled form (MsaIterConsts::scaled; omtab then holds -om/e_c); the DAL uses the direct one.
 // TH2: tile rows (8, or 2 when the image has too few 32 x 8 tiles to fill the GPU - DAL images are
 // small); every pixel's terms are summed in the same order either way.
+// NS > 1: the window's row chunks are dealt round-robin to NS CTAs per tile (blockIdx.z = part *
+// nb + image), each writing its partial sum to part_out[part]; k_large_combine adds the parts in
+// part order (small images: more warps in flight; a different summation order than NS = 1).
 template <int C, int KER, bool SC, int TH2>
 __global__ void __launch_bounds__(32 * TH2) k_agent_large(MsaGeom g, MsaIterConsts K, int R, const float* __restrict__ omtab,
                                                     float exh_x, float exh_y, const float* __restrict__ c,
-                                                    float* __restrict__ chalf) {
+                                                    float* __restrict__ chalf, int NS, float* __restrict__ part_out) {
   extern __shared__ __align__(16) float smem[];
   const int SWL = TW + 2 * R;                  // staged columns x0-R .. x0+31+R
   float4* snb = reinterpret_cast<float4*>(smem);  // [CR][SWL]
@@ -35,7 +41,8 @@ __global__ void __launch_bounds__(32 * TH2) k_agent_large(MsaGeom g, MsaIterCons
   const int OW = 2 * R + 1;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   constexpr int TH = TH2, NT = 32 * TH2;
-  const int x0 = blockIdx.x * TW, y0 = g.row0 + g.k1_lo + blockIdx.y * TH, b = blockIdx.z;
+  const int part = blockIdx.z / g.nb, b = blockIdx.z - part * g.nb;
+  const int x0 = blockIdx.x * TW, y0 = g.row0 + g.k1_lo + blockIdx.y * TH;
   const int W = g.W, H = g.H;
   const int x = x0 + tx, y = y0 + ty;
   const bool own = x < W && y < g.row0 + msa_k1_hi(g);
@@ -46,7 +53,7 @@ __global__ void __launch_bounds__(32 * TH2) k_agent_large(MsaGeom g, MsaIterCons
     ci[k] = own ? c[msa_idx(g, b, k, C, y, x)] : 0.0f;
     acc[k] = 0.0f;
   }
-  for (int yc = ylo; yc < yhi; yc += CR) {
+  for (int yc = ylo + part * CR; yc < yhi; yc += NS * CR) {
     const int nrow = min(CR, yhi - yc);
     __syncthreads();  // the previous chunk is consumed
     // stage the chunk: colours interleaved (pad lane 0), out-of-image columns zero (never used)
@@ -97,34 +104,63 @@ __global__ void __launch_bounds__(32 * TH2) k_agent_large(MsaGeom g, MsaIterCons
     }
   }
   if (!own) return;
+  if (NS > 1) {
+#pragma unroll
+    for (int k = 0; k < C; ++k) part_out[msa_idx(g, part * g.nb + b, k, C, y, x)] = acc[k];
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < C; ++k) chalf[msa_idx(g, b, k, C, y, x)] = __fmaf_rn(SC ? K.dt_s : K.dt_NR, acc[k], ci[k]);
 }
 
+template <int C>
+__global__ void k_large_combine(MsaGeom g, float dts, int NS, const float* __restrict__ part, const float* __restrict__ c,
+                                float* __restrict__ chalf) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  const int y = g.row0 + g.k1_lo + blockIdx.y;
+  const int b = blockIdx.z;
+  if (x >= g.W) return;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    float s = part[msa_idx(g, b, k, C, y, x)];
+    for (int q = 1; q < NS; ++q) s = __fadd_rn(s, part[msa_idx(g, q * g.nb + b, k, C, y, x)]);
+    chalf[msa_idx(g, b, k, C, y, x)] = __fmaf_rn(dts, s, c[msa_idx(g, b, k, C, y, x)]);
+  }
+}
+
+struct Split {
+  int NS;
+  float* part;
+};
+
 template <typename F>
 cudaError_t go(F* kern, int th, int nr, size_t smem, const MsaGeom& g, const MsaIterConsts& K, int R,
-               const float* omtab, float exh_x, float exh_y, const float* c, float* ch, cudaStream_t s) {
+               const float* omtab, float exh_x, float exh_y, const float* c, float* ch, cudaStream_t s, Split sp) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   if (e != cudaSuccess) return e;
-  dim3 grd((g.W + TW - 1) / TW, (nr + th - 1) / th, g.nb);
-  kern<<<grd, 32 * th, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch);
+  dim3 grd((g.W + TW - 1) / TW, (nr + th - 1) / th, g.nb * sp.NS);
+  kern<<<grd, 32 * th, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch, sp.NS, sp.part);
   return cudaGetLastError();
 }
 
 template <int C, int TH2>
 cudaError_t launch_th(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab, float exh_x, float exh_y,
-                      const float* c, float* ch, cudaStream_t s, int nr) {
+                      const float* c, float* ch, cudaStream_t s, int nr, Split sp) {
   const size_t smem = sizeof(float) * (4 * CR * (TW + 2 * R) + (CR + TH2 - 1) * (2 * R + 1));
   const bool sc = K.scaled && omtab;
-  if (K.kernel == 0 && sc) return go(k_agent_large<C, 0, true, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
-  if (K.kernel == 0) return go(k_agent_large<C, 0, false, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
-  if (sc) return go(k_agent_large<C, 1, true, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
-  return go(k_agent_large<C, 1, false, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s);
+  cudaError_t e;
+  if (K.kernel == 0 && sc) e = go(k_agent_large<C, 0, true, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
+  else if (K.kernel == 0) e = go(k_agent_large<C, 0, false, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
+  else if (sc) e = go(k_agent_large<C, 1, true, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
+  else e = go(k_agent_large<C, 1, false, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
+  if (e != cudaSuccess || sp.NS == 1) return e;
+  k_large_combine<C><<<dim3((g.W + 127) / 128, nr, g.nb), 128, 0, s>>>(g, sc ? K.dt_s : K.dt_NR, sp.NS, sp.part, c, ch);
+  return cudaGetLastError();
 }
 
 template <int C>
 cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab, float exh_x, float exh_y,
-                     const float* c, float* ch, cudaStream_t s) {
+                     const float* c, float* ch, cudaStream_t s, float* scratch, size_t scratch_floats, int* launches) {
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   // 32 x 8 tiles unless that leaves SMs idle (fewer than two tiles per SM): then 32 x 2
@@ -135,20 +171,34 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const floa
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const long long tiles8 = (long long)((g.W + TW - 1) / TW) * ((nr + TH - 1) / TH) * g.nb;
-  if (tiles8 < 2LL * sms) return launch_th<C, 2>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr);
-  return launch_th<C, TH>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr);
+  *launches = 1;
+  if (tiles8 >= 2LL * sms) return launch_th<C, TH>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr, Split{1, nullptr});
+  // still under eight 64-thread CTAs per SM: split the window (at most 4 parts, as the scratch
+  // allows, and no more parts than row chunks)
+  static const bool nosplit = getenv("MSA_LARGE_NOSPLIT") != nullptr;  // test hook: the NS = 1 order
+  const long long tiles2 = (long long)((g.W + TW - 1) / TW) * ((nr + 1) / 2) * g.nb;
+  const size_t per_part = (size_t)g.nb * C * g.plane;
+  int NS = (int)std::min<long long>(4, (8LL * sms + tiles2 - 1) / tiles2);
+  NS = std::min(NS, (2 * R + 2 + CR - 1) / CR);
+  NS = std::min<long long>(NS, per_part ? (long long)(scratch_floats / per_part) : 0);
+  if (nosplit || !scratch || NS < 2) NS = 1;
+  if (NS > 1) *launches = 2;
+  return launch_th<C, 2>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr, Split{NS, NS > 1 ? scratch : nullptr});
 }
 
 }  // namespace
 
 cudaError_t msa_launch_agent_large(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab,
-                                   const float* c, float* chalf, cudaStream_t s, float exh_x, float exh_y) {
+                                   const float* c, float* chalf, cudaStream_t s, float exh_x, float exh_y,
+                                   float* scratch, size_t scratch_floats, int* launches) {
+  int dummy = 0;
+  if (!launches) launches = &dummy;
   if (R <= 8 || R > MSA_MAXR) return cudaErrorNotSupported;
   switch (g.C) {
-    case 1: return launch_c<1>(g, K, R, omtab, exh_x, exh_y, c, chalf, s);
-    case 2: return launch_c<2>(g, K, R, omtab, exh_x, exh_y, c, chalf, s);
-    case 3: return launch_c<3>(g, K, R, omtab, exh_x, exh_y, c, chalf, s);
-    case 4: return launch_c<4>(g, K, R, omtab, exh_x, exh_y, c, chalf, s);
+    case 1: return launch_c<1>(g, K, R, omtab, exh_x, exh_y, c, chalf, s, scratch, scratch_floats, launches);
+    case 2: return launch_c<2>(g, K, R, omtab, exh_x, exh_y, c, chalf, s, scratch, scratch_floats, launches);
+    case 3: return launch_c<3>(g, K, R, omtab, exh_x, exh_y, c, chalf, s, scratch, scratch_floats, launches);
+    case 4: return launch_c<4>(g, K, R, omtab, exh_x, exh_y, c, chalf, s, scratch, scratch_floats, launches);
     default: return cudaErrorNotSupported;
   }
 }
@@ -158,11 +208,17 @@ cudaError_t msa_launch_agent_large(const MsaGeom& g, const MsaIterConsts& K, int
 // k_dal_back: same per-term arithmetic in the same order - dy ascending, dx ascending - with the
 // colours and adjoints staged through shared memory as float4 in chunks of CR rows).
 namespace {
-template <int C>
-__global__ void __launch_bounds__(NT) k_dal_back_large(MsaGeom g, int R, int ker, float exh_x, float exh_y, float e_c,
-                                                       float eps_c, float inv_NR, float dt,
+// TH2 = 8, NS = 1: writes lam_out and the block partials itself. Otherwise (small images: 32 x 2
+// tiles, the window's row chunks dealt to NS CTAs, blockIdx.z = part) it writes per-pixel partial
+// sums (C adjoint components, the two eps sums) to part_out[part] and k_dal_back_combine finishes.
+template <int C, int TH2>
+__global__ void __launch_bounds__(32 * TH2) k_dal_back_large(MsaGeom g, int R, int ker, float exh_x, float exh_y,
+                                                       float e_c, float eps_c, float inv_NR, float dt,
                                                        const float* __restrict__ c, const float* __restrict__ lam,
-                                                       float* __restrict__ lam_out, double* __restrict__ partials) {
+                                                       float* __restrict__ lam_out, double* __restrict__ partials,
+                                                       int NS, float* __restrict__ part_out) {
+  constexpr int TH = TH2, NT = 32 * TH2;
+  const int part = blockIdx.z;
   extern __shared__ __align__(16) float smem[];
   const int SWL = TW + 2 * R, OW = 2 * R + 1;
   float4* sc = reinterpret_cast<float4*>(smem);  // [CR][SWL]
@@ -182,7 +238,7 @@ __global__ void __launch_bounds__(NT) k_dal_back_large(MsaGeom g, int R, int ker
     acc[k] = 0.0f;
   }
   float sx = 0.0f, scc = 0.0f;
-  for (int yc = ylo; yc < yhi; yc += CR) {
+  for (int yc = ylo + part * CR; yc < yhi; yc += NS * CR) {
     const int nrow = min(CR, yhi - yc);
     __syncthreads();
     for (int e = threadIdx.x; e < nrow * SWL; e += NT) {
@@ -244,6 +300,14 @@ __global__ void __launch_bounds__(NT) k_dal_back_large(MsaGeom g, int R, int ker
       }
     }
   }
+  if (TH2 != 8 || NS > 1) {
+    if (!own) return;
+#pragma unroll
+    for (int k = 0; k < C; ++k) part_out[msa_idx(g, part, k, C + 2, y, x)] = acc[k];
+    part_out[msa_idx(g, part, C, C + 2, y, x)] = sx;
+    part_out[msa_idx(g, part, C + 1, C + 2, y, x)] = scc;
+    return;
+  }
   double sums[2] = {0.0, 0.0};
   if (own) {
 #pragma unroll
@@ -268,34 +332,100 @@ __global__ void __launch_bounds__(NT) k_dal_back_large(MsaGeom g, int R, int ker
     partials[((long long)blockIdx.y * gridDim.x + blockIdx.x) * 2 + threadIdx.x] = t;
   }
 }
+// parts added in part order, then exactly the tail of the 32 x 8 kernel (same block partials)
+template <int C>
+__global__ void __launch_bounds__(256) k_dal_back_combine(MsaGeom g, int NS, const float* __restrict__ part,
+                                                          float inv_NR, float dt, const float* __restrict__ lam,
+                                                          float* __restrict__ lam_out, double* __restrict__ partials) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x = blockIdx.x * TW + tx, y = blockIdx.y * TH + ty;
+  const bool own = x < g.W && y < g.H;
+  double sums[2] = {0.0, 0.0};
+  if (own) {
+    float v[C + 2];
+#pragma unroll
+    for (int k = 0; k < C + 2; ++k) {
+      v[k] = part[msa_idx(g, 0, k, C + 2, y, x)];
+      for (int q = 1; q < NS; ++q) v[k] = __fadd_rn(v[k], part[msa_idx(g, q, k, C + 2, y, x)]);
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k)
+      lam_out[msa_idx(g, 0, k, C, y, x)] = __fmaf_rn(dt * inv_NR, v[k], lam[msa_idx(g, 0, k, C, y, x)]);
+    sums[0] = (double)v[C] * inv_NR;
+    sums[1] = (double)v[C + 1] * inv_NR;
+  }
+  __shared__ double red[8][2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    double s = sums[q];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp][q] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w][threadIdx.x];
+    partials[((long long)blockIdx.y * gridDim.x + blockIdx.x) * 2 + threadIdx.x] = t;
+  }
+}
+
+template <int C>
+cudaError_t dal_back_c(const MsaGeom& g, int R, int kernel, float exh_x, float exh_y, float e_c, float eps_c,
+                       float inv_NR, float dt, const float* c, const float* lam, float* lam_out, double* partials,
+                       float* scratch, size_t scratch_floats, cudaStream_t s) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const int nx = (g.W + TW - 1) / TW;
+  const long long tiles8 = (long long)nx * ((g.H + TH - 1) / TH);
+  const size_t per_part = (size_t)(C + 2) * g.plane;
+  if (tiles8 >= 2LL * sms || !scratch || scratch_floats < per_part) {
+    const size_t smem = sizeof(float) * (8 * CR * (TW + 2 * R) + (CR + TH - 1) * (2 * R + 1));
+    cudaError_t e = cudaFuncSetAttribute(k_dal_back_large<C, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    if (e != cudaSuccess) return e;
+    k_dal_back_large<C, 8><<<dim3(nx, (g.H + TH - 1) / TH), NT, smem, s>>>(g, R, kernel, exh_x, exh_y, e_c, eps_c,
+                                                                          inv_NR, dt, c, lam, lam_out, partials, 1,
+                                                                          nullptr);
+    return cudaGetLastError();
+  }
+  // small image: 32 x 2 tiles and the window's row chunks split over NS CTAs (as the scratch allows)
+  static const bool nosplit = getenv("MSA_LARGE_NOSPLIT") != nullptr;  // test hook: the NS = 1 order
+  const long long tiles2 = (long long)nx * ((g.H + 1) / 2);
+  int NS = (int)std::min<long long>(4, (8LL * sms + tiles2 - 1) / tiles2);
+  NS = std::min(NS, (2 * R + 2 + CR - 1) / CR);
+  NS = (int)std::min<size_t>((size_t)NS, scratch_floats / per_part);
+  if (nosplit || NS < 1) NS = 1;
+  const size_t smem = sizeof(float) * (8 * CR * (TW + 2 * R) + (CR + 2 - 1) * (2 * R + 1));
+  cudaError_t e = cudaFuncSetAttribute(k_dal_back_large<C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  if (e != cudaSuccess) return e;
+  k_dal_back_large<C, 2><<<dim3(nx, (g.H + 1) / 2, NS), 64, smem, s>>>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR,
+                                                                       dt, c, lam, lam_out, partials, NS, scratch);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_dal_back_combine<C><<<dim3(nx, (g.H + TH - 1) / TH), 256, 0, s>>>(g, NS, scratch, inv_NR, dt, lam, lam_out,
+                                                                       partials);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
 int msa_dal_back_large_blocks(const MsaGeom& g) { return ((g.W + TW - 1) / TW) * ((g.H + TH - 1) / TH); }
 
 cudaError_t msa_dal_back_large(const MsaGeom& g, int R, int kernel, float exh_x, float exh_y, float eps_c,
                                float inv_NR, float dt, const float* c, const float* lam, float* lam_out,
-                               double* partials, cudaStream_t s) {
+                               double* partials, cudaStream_t s, float* scratch, size_t scratch_floats) {
   if (R <= 8 || R > MSA_MAXR) return cudaErrorNotSupported;
-  const size_t smem = sizeof(float) * (8 * CR * (TW + 2 * R) + (CR + TH - 1) * (2 * R + 1));
-  dim3 grd((g.W + TW - 1) / TW, (g.H + TH - 1) / TH);
   const float e_c = 0.5f * eps_c;
-#define DAL_BL(CC)                                                                                                  \
-  case CC: {                                                                                                        \
-    static bool attr = false;                                                                                       \
-    if (!attr) {                                                                                                    \
-      cudaError_t e = cudaFuncSetAttribute(k_dal_back_large<CC>, cudaFuncAttributeMaxDynamicSharedMemorySize,       \
-                                           160 * 1024);                                                             \
-      if (e != cudaSuccess) return e;                                                                               \
-      attr = true;                                                                                                  \
-    }                                                                                                               \
-    k_dal_back_large<CC><<<grd, NT, smem, s>>>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR, dt, c, lam, lam_out, \
-                                               partials);                                                           \
-    break;                                                                                                          \
-  }
   switch (g.C) {
-    DAL_BL(1) DAL_BL(2) DAL_BL(3) DAL_BL(4)
+    case 1: return dal_back_c<1>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR, dt, c, lam, lam_out, partials, scratch, scratch_floats, s);
+    case 2: return dal_back_c<2>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR, dt, c, lam, lam_out, partials, scratch, scratch_floats, s);
+    case 3: return dal_back_c<3>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR, dt, c, lam, lam_out, partials, scratch, scratch_floats, s);
+    case 4: return dal_back_c<4>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR, dt, c, lam, lam_out, partials, scratch, scratch_floats, s);
     default: return cudaErrorNotSupported;
   }
-#undef DAL_BL
-  return cudaGetLastError();
 }

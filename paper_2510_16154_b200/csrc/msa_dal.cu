@@ -273,7 +273,8 @@ static bool dal_large(int R, int C) {
 }
 
 cudaError_t msa_dal_step(const MsaGeom& g, double hx, double hy, double dt, int R, int kernel, int NR, double eps_x,
-                         double eps_c, const float* c, float* c_out, cudaStream_t s) {
+                         double eps_c, const float* c, float* c_out, cudaStream_t s, float* scratch,
+                         size_t scratch_floats) {
   const DalConsts Q = make_consts(MsaDalConstsHost{hx, hy, dt, R, kernel, NR}, eps_x, eps_c);
   if (dal_large(R, g.C)) {  // chunked shared-memory n-body kernel, same arithmetic and order
     MsaIterConsts K;
@@ -284,7 +285,8 @@ cudaError_t msa_dal_step(const MsaGeom& g, double hx, double hy, double dt, int 
     MsaGeom gg = g;
     gg.k1_lo = 0;
     gg.k1_hi = 0;
-    return msa_launch_agent_large(gg, K, R, nullptr, c, c_out, s, Q.ex_half_hx2, Q.ex_half_hy2);
+    return msa_launch_agent_large(gg, K, R, nullptr, c, c_out, s, Q.ex_half_hx2, Q.ex_half_hy2, scratch,
+                                  scratch_floats);
   }
   dim3 blk(32, 8), grd((g.W + 31) / 32, (g.H + 7) / 8);
   if (kernel == 0) {
@@ -300,11 +302,11 @@ int msa_dal_blocks(const MsaGeom& g) { return ((g.W + 31) / 32) * ((g.H + 7) / 8
 // lam_out = lam + dt (dF/dc)^T lam at (c, eps); deps_dev[2] = (<lam, dF/deps_x>, <lam, dF/deps_c>)
 cudaError_t msa_dal_back(const MsaGeom& g, double hx, double hy, double dt, int R, int kernel, int NR, double eps_x,
                          double eps_c, const float* c, const float* lam, float* lam_out, double* partials,
-                         double* deps_dev, cudaStream_t s) {
+                         double* deps_dev, cudaStream_t s, float* scratch, size_t scratch_floats) {
   const DalConsts Q = make_consts(MsaDalConstsHost{hx, hy, dt, R, kernel, NR}, eps_x, eps_c);
   if (dal_large(R, g.C)) {
     cudaError_t e = msa_dal_back_large(g, R, kernel, Q.ex_half_hx2, Q.ex_half_hy2, Q.eps_c, Q.inv_NR, (float)dt, c,
-                                       lam, lam_out, partials, s);
+                                       lam, lam_out, partials, s, scratch, scratch_floats);
     if (e != cudaSuccess) return e;
     k_sum_partials<<<1, 32, 0, s>>>(partials, msa_dal_back_large_blocks(g), 2, deps_dev);
     return cudaGetLastError();

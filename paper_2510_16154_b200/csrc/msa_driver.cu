@@ -523,8 +523,13 @@ int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int 
   const msa_params& P = x->prm;
   // large supports (NEXT-3): step 1 by the chunked n-body kernel into c[o], steps 2-3 generic
   if (P.radius > 8 && P.channels <= 4 && k1_variant() != K1_GENERIC) {
-    cudaError_t e = msa_launch_agent_large(g, KC, P.radius, x->d_omtab, x->c[s], x->c[o], x->stream);
+    // scratch for a window split at small images: cb[o] and p[o] (3C planes, contiguous) are
+    // written only after step 1
+    int nl = 1;
+    cudaError_t e = msa_launch_agent_large(g, KC, P.radius, x->d_omtab, x->c[s], x->c[o], x->stream, 0.0f, 0.0f,
+                                           x->cb[o], (size_t)3 * g.nb * g.C * g.plane, &nl);
     if (e != cudaSuccess) return set_err(MSA_ECUDA, "large-support agent kernel: %s", cudaGetErrorString(e));
+    x->launches += nl - 1;
     if (P.scheme == MSA_SCHEME_LINEARISED_ADMM)
       e = msa_launch_iter_lin_generic(g, KC, x->d_off, x->d_om, x->c[s], x->p[s], x->I, x->c[o], x->p[o], x->stream,
                                       x->c[o]);
@@ -1316,9 +1321,11 @@ namespace {
 struct DalBuffers {
   float* traj = nullptr;   // [M+1][C planes] (or 2 ping-pong slots for cost-only sweeps)
   float *lam0 = nullptr, *lam1 = nullptr, *q = nullptr, *v = nullptr, *mu = nullptr;
+  float* split = nullptr;  // window-split partial sums of the large-support sweeps: 4 (C + 2) planes
+  size_t split_floats = 0;
   double *partials = nullptr, *dev = nullptr;  // dev: [0] J, [2 + 2m] deps of step m
   ~DalBuffers() {
-    void* ps[] = {traj, lam0, lam1, q, v, mu, partials, dev};
+    void* ps[] = {traj, lam0, lam1, q, v, mu, split, partials, dev};
     for (void* p : ps)
       if (p) cudaFree(p);
   }
@@ -1350,6 +1357,10 @@ int dal_alloc(msa_ctx* x, const msa_dal_params* d, const float* v, const float* 
   CUDA_TRY(cudaMalloc((void**)&B.v, sizeof(float) * pf2));
   CUDA_TRY(cudaMalloc((void**)&B.mu, sizeof(float) * pf2));
   CUDA_TRY(cudaMalloc((void**)&B.partials, sizeof(double) * 2 * (size_t)msa_dal_blocks(x->g)));
+  if (x->prm.radius > 8) {
+    B.split_floats = (size_t)4 * (x->g.C + 2) * x->g.plane;
+    CUDA_TRY(cudaMalloc((void**)&B.split, sizeof(float) * B.split_floats));
+  }
   CUDA_TRY(cudaMalloc((void**)&B.dev, sizeof(double) * (2 + 2 * (size_t)d->steps)));
   CUDA_TRY(cudaMemsetAsync(B.v, 0, sizeof(float) * pf2, x->stream));
   CUDA_TRY(cudaMemsetAsync(B.mu, 0, sizeof(float) * pf2, x->stream));
@@ -1376,7 +1387,7 @@ int dal_forward(msa_ctx* x, const msa_dal_params* d, const double* eps, DalBuffe
     const float* cm = B.traj + (full ? (size_t)m : (size_t)(m & 1)) * pf;
     float* cn = B.traj + (full ? (size_t)(m + 1) : (size_t)((m + 1) & 1)) * pf;
     CUDA_TRY(msa_dal_step(x->g, x->hx, x->hy, P.dt, P.radius, P.kernel, x->NR, eps[2 * m], eps[2 * m + 1], cm, cn,
-                          x->stream));
+                          x->stream, B.split, B.split_floats));
     ++x->launches;
   }
   float* last = B.traj + (full ? (size_t)d->steps : (size_t)(d->steps & 1)) * pf;
@@ -1400,7 +1411,8 @@ int dal_grad(msa_ctx* x, const msa_dal_params* d, const double* eps, DalBuffers&
   float *lam = B.lam0, *lam2 = B.lam1;
   for (int m = d->steps - 1; m >= 0; --m) {
     CUDA_TRY(msa_dal_back(x->g, x->hx, x->hy, P.dt, P.radius, P.kernel, x->NR, eps[2 * m], eps[2 * m + 1],
-                          B.traj + (size_t)m * pf, lam, lam2, B.partials, B.dev + 2 + 2 * m, x->stream));
+                          B.traj + (size_t)m * pf, lam, lam2, B.partials, B.dev + 2 + 2 * m, x->stream, B.split,
+                          B.split_floats));
     x->launches += 2;
     std::swap(lam, lam2);
   }

@@ -23,14 +23,19 @@ cudaError_t msa_launch_iter_generic(const MsaGeom& g, const MsaIterConsts& K, co
 
 // Step 1 alone for large supports (msa_agent_large.cu): 8 < R <= 64, C <= 4; omtab = 1 - a_delta for
 // every (dx, dy) in [-R, R]^2 ([dy + R][dx + R]); writes c_half.
+// scratch (may be null): room for a window split at small images (parts of nb * C planes each);
+// *launches (may be null) receives the kernels launched (1, or 2 with a split).
 cudaError_t msa_launch_agent_large(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab,
                                    const float* c, float* chalf, cudaStream_t s, float exh_x = 0.0f,
-                                   float exh_y = 0.0f);
+                                   float exh_y = 0.0f, float* scratch = nullptr, size_t scratch_floats = 0,
+                                   int* launches = nullptr);
 // DAL backward step for large supports (msa_agent_large.cu): one image, partials [blocks][2]
 int msa_dal_back_large_blocks(const MsaGeom& g);
+// scratch: (C + 2) planes per window part for small images (null: one 32 x 8 pass)
 cudaError_t msa_dal_back_large(const MsaGeom& g, int R, int kernel, float exh_x, float exh_y, float eps_c,
                                float inv_NR, float dt, const float* c, const float* lam, float* lam_out,
-                               double* partials, cudaStream_t s);
+                               double* partials, cudaStream_t s, float* scratch = nullptr,
+                               size_t scratch_floats = 0);
 
 // Single-loop linearised ADMM iteration (msa.h MSA_SCHEME_LINEARISED_ADMM), any C: reads c, mu, I,
 // writes c_out, mu_out.
@@ -115,11 +120,12 @@ cudaError_t msa_labels_relabel(int npix, const int32_t* seg_of_pix, int seg_off,
 
 // NEXT-1 DAL building blocks (msa_dal.cu); one image, world 1, C <= 4.
 cudaError_t msa_dal_step(const MsaGeom& g, double hx, double hy, double dt, int R, int kernel, int NR, double eps_x,
-                         double eps_c, const float* c, float* c_out, cudaStream_t s);
+                         double eps_c, const float* c, float* c_out, cudaStream_t s, float* scratch = nullptr,
+                         size_t scratch_floats = 0);
 int msa_dal_blocks(const MsaGeom& g);
 cudaError_t msa_dal_back(const MsaGeom& g, double hx, double hy, double dt, int R, int kernel, int NR, double eps_x,
                          double eps_c, const float* c, const float* lam, float* lam_out, double* partials,
-                         double* deps_dev, cudaStream_t s);
+                         double* deps_dev, cudaStream_t s, float* scratch = nullptr, size_t scratch_floats = 0);
 cudaError_t msa_dal_terminal(const MsaGeom& g, int cost, double rho, double hx, double hy, double alpha,
                              const float* c, const float* I, const float* v, const float* mu, float* q, float* lam,
                              double* partials, double* J_dev, cudaStream_t s);

@@ -78,7 +78,8 @@ def test_dal_algorithm1_matches_oracle():
 @pytest.mark.parametrize("R,C,kernel", [(15, 3, 0), (12, 1, 1), (20, 4, 0)])
 def test_dal_large_support_kernels_bitwise(R, C, kernel, tmp_path):
     """R > 8 runs the forward and backward steps on the chunked shared-memory kernels; they have the
-    generic DAL kernels' arithmetic and summation order: bitwise-equal cost and gradient."""
+    generic DAL kernels' arithmetic and summation order: bitwise-equal cost and gradient (with the
+    window split of small images switched off; with it, equal to fp32 summation order)."""
     import json
     import os
     import subprocess
@@ -101,13 +102,20 @@ np.savez(sys.argv[2], J=np.array([J]), g=g)
 """ % os.path.dirname(HERE_DIR)
     spec = dict(seed=R + C, H=29, W=37, C=C, R=R, M=6, kernel=kernel)
     outs = []
-    for generic in (False, True):
+    for variant in ("large", "generic", "large_split"):
         env = dict(os.environ)
         env.pop("MSA_DAL_GENERIC", None)
-        if generic:
+        env.pop("MSA_LARGE_NOSPLIT", None)
+        if variant == "generic":
             env["MSA_DAL_GENERIC"] = "1"
-        out = str(tmp_path / f"g{int(generic)}.npz")
+        if variant == "large":  # the window of a pixel in one CTA: the generic order
+            env["MSA_LARGE_NOSPLIT"] = "1"
+        out = str(tmp_path / f"{variant}.npz")
         subprocess.run([sys.executable, "-c", script, json.dumps(spec), out], check=True, env=env)
         outs.append(np.load(out))
     assert np.array_equal(outs[0]["J"], outs[1]["J"])
     assert np.array_equal(outs[0]["g"], outs[1]["g"])
+    # small image: the default splits each window over CTAs (partial sums added in part order) -
+    # the same terms in another order
+    np.testing.assert_allclose(outs[2]["J"], outs[0]["J"], rtol=1e-6)
+    np.testing.assert_allclose(outs[2]["g"], outs[0]["g"], rtol=1e-4, atol=1e-6 * float(np.max(np.abs(outs[0]["g"]))))
