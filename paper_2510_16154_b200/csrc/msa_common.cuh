@@ -53,6 +53,8 @@ struct MsaIterConsts {
   int scaled;
   float dt_s;       // dt / N_R * e_c^4                (fp64, rounded once)
   float m4;         // -4 e_c (exact)
+  int no_pdl;       // host side: launch K1 without programmatic dependent launch (rows mode: the
+                    // K1 launches sit between event waits on the halo exchange)
 };
 
 // phi as a function of t = max(1 - r, 0) (eq:kernel PAPER.md:259-267; R3, R21):

@@ -312,6 +312,7 @@ MsaIterConsts iter_consts(const msa_ctx* x, double rho) {
   const double e_c = 0.5 * p.eps_c;
   K.dt_s = (float)(p.dt / (double)x->NR * (e_c * e_c) * (e_c * e_c));
   K.m4 = (float)(-4.0 * e_c);
+  K.no_pdl = (p.world > 1 && p.shard == MSA_SHARD_ROWS) ? 1 : 0;
   return K;
 }
 

@@ -459,7 +459,7 @@ cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = pdl && !K.no_pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, k_iter_fast_c3<R, P, LIN>, g, K, om, tm);
 }
 
