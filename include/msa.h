@@ -175,7 +175,13 @@ int msa_step(msa_ctx* ctx, int32_t n_iters);
 
 /* rounds x K iterations from the current state; fills stats[0 .. rounds) (may be NULL)
  * with the records of the rounds completed by this call; synchronises. Returns
- * MSA_EDIVERGED if any of them saw a non-finite value. */
+ * MSA_EDIVERGED if any of them saw a non-finite value.
+ * One process-local GPU (world = 1, or batch mode) with timing off: the first solve from a given
+ * starting state (ping-pong set, rho, position inside a round) is captured into a CUDA graph on
+ * the context's stream and later solves from that state replay it (same kernels, same results;
+ * environment MSA_NO_GRAPH=1 disables it). The stream must therefore be capturable (not the
+ * legacy default stream; NULL selects a library stream, which is); otherwise the launches are
+ * issued directly. */
 int msa_solve(msa_ctx* ctx, msa_round_stats* stats);
 
 /* Quantisation rule Q(c; delta) (reading R16) of the current c, per image:
