@@ -137,7 +137,11 @@ template <int R, int P, bool MASK>
 __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const FastOm& om, float m4, float qc,
                                             int lx, int strip, int x, int ybase, int W, int H,
                                             const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
-  const f2 M4 = pk(m4, m4), QC = pk(qc, qc);
+  // m4 in an ordinary register (a broadcast operand of FFMA2); left to itself the compiler keeps it
+  // in a uniform register it reloads from the constant bank before most uses
+  // (0 * lane + m4 == m4 exactly, but the value is no longer warp-uniform)
+  const float m4r = __fmaf_rn(0.0f, (float)lx, m4);
+  const f2 M4 = pk(m4r, m4r), QC = pk(qc, qc);
   int o = 0;  // offset index in the kernel's order; compile-time constant after unrolling
 #pragma unroll
   for (int dx = -R; dx <= R; ++dx) {
