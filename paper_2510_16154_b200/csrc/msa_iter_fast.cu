@@ -88,14 +88,15 @@ struct Smem {
 // One parity pass over the neighbour pairs of column dx: cache Cp[q] = rows (2q + PAR,
 // 2q + PAR + 1) of the column (cache row k = strip row k - m). MASK: zero the weight of
 // out-of-image neighbours (column mask cm, row validity from the global row of cache row k).
-template <int R, int P, bool MASK, int PAR>
-__device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx, int m, const FastOm& om, int& o,
-                                            f2 M4, f2 QC, float cm, int yk0, int H,
-                                            const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
+template <int R, int P, bool MASK, int PAR, int M, bool CENTER>
+__device__ __forceinline__ void column_pass_m(const float* __restrict__ s, const FastOm& om, int& o, f2 M4, f2 QC,
+                                              float cm, int yk0, int H, const f2 (&ci)[P / 2][C],
+                                              f2 (&acc)[P / 2][C]) {
   constexpr int SH = NSTRIP * P + 2 * R;
-  constexpr int NQ = (P + 2 * R) / 2;
+  constexpr int NQ = (P + 2 * M) / 2;
+  constexpr int m = M;
   f2 Cp[NQ][C], Mp[NQ];
-  const int nrow = P + 2 * m;
+  constexpr int nrow = P + 2 * m;
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     if (2 * q + PAR + 1 >= nrow) break;
@@ -107,8 +108,8 @@ __device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx,
     }
   }
 #pragma unroll
-  for (int dy = -R; dy <= R; ++dy) {
-    if (dy < -m || dy > m || dx == 0 && dy == 0) continue;
+  for (int dy = -M; dy <= M; ++dy) {
+    if (CENTER && dy == 0) continue;
     if (((dy + m) & 1) != PAR) continue;
     const float omv = om.v[o++];
     const f2 OM = pk(omv, omv);
@@ -133,6 +134,19 @@ __device__ __forceinline__ void column_pass(const float* __restrict__ s, int dx,
   }
 }
 
+// both parity passes of a column of half-height M (even M: pairs starting on even cache rows first)
+template <int R, int P, bool MASK, int M, bool CENTER>
+__device__ __forceinline__ void column_m(const float* __restrict__ s, const FastOm& om, int& o, f2 M4, f2 QC,
+                                         float cm, int yk0, int H, const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
+  if constexpr ((M & 1) == 0) {
+    column_pass_m<R, P, MASK, 0, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+    column_pass_m<R, P, MASK, 1, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+  } else {
+    column_pass_m<R, P, MASK, 1, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+    column_pass_m<R, P, MASK, 0, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+  }
+}
+
 template <int R, int P, bool MASK>
 __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const FastOm& om, float m4, float qc,
                                             int lx, int strip, int x, int ybase, int W, int H,
@@ -142,20 +156,34 @@ __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const 
   // (0 * lane + m4 == m4 exactly, but the value is no longer warp-uniform)
   const float m4r = __fmaf_rn(0.0f, (float)lx, m4);
   const f2 M4 = pk(m4r, m4r), QC = pk(qc, qc);
-  int o = 0;  // offset index in the kernel's order; compile-time constant after unrolling
+  int o = 0;  // offset index in the kernel's order
+#ifdef MSA_K1_ROLLED
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
   for (int dx = -R; dx <= R; ++dx) {
     const int m = col_m(R, dx);
     if (m < 0) continue;
     const float* s = sc + (strip * P - m + R) * SW + SX + lx + dx;
     const float cm = (!MASK || (x + dx >= 0 && x + dx < W)) ? 1.0f : 0.0f;
     const int yk0 = ybase - m;
-    if ((m & 1) == 0) {
-      column_pass<R, P, MASK, 0>(s, dx, m, om, o, M4, QC, cm, yk0, H, ci, acc);
-      column_pass<R, P, MASK, 1>(s, dx, m, om, o, M4, QC, cm, yk0, H, ci, acc);
+    // one code body per half-height (and the centre column): the rolled loop keeps step 1's code
+    // small enough for the instruction cache
+    if (dx == 0) {
+      if constexpr (col_m(R, 0) == 0) {
+      } else if constexpr (col_m(R, 0) == 1) column_m<R, P, MASK, 1, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      else if constexpr (col_m(R, 0) == 2) column_m<R, P, MASK, 2, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      else if constexpr (col_m(R, 0) == 3) column_m<R, P, MASK, 3, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      else column_m<R, P, MASK, 4, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+    } else if (m == 1) {
+      column_m<R, P, MASK, 1, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+    } else if (m == 2) {
+      column_m<R, P, MASK, 2, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+    } else if (m == 3) {
+      if constexpr (R >= 4) column_m<R, P, MASK, 3, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
     } else {
-      column_pass<R, P, MASK, 1>(s, dx, m, om, o, M4, QC, cm, yk0, H, ci, acc);
-      column_pass<R, P, MASK, 0>(s, dx, m, om, o, M4, QC, cm, yk0, H, ci, acc);
+      if constexpr (R >= 5) column_m<R, P, MASK, 4, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
     }
   }
 }
@@ -173,7 +201,7 @@ struct Occ {
 // (in), tm.po mu+ (out); no cbar / mu / cbar+ traffic; the dual step takes grad c from the c tile.
 template <int R, int P, bool LIN>
 __global__ void __launch_bounds__(NT, Occ<P>::blocks)
-    k_iter_fast_c3(MsaGeom g, MsaIterConsts K, FastOm om, const __grid_constant__ TmaSet tm) {
+    k_iter_fast_c3(MsaGeom g, MsaIterConsts K, const __grid_constant__ FastOm om, const __grid_constant__ TmaSet tm) {
   using S = Smem<R, P>;
   constexpr int TH = S::TH, SH = S::SH, BH = S::BH, QH = S::QH, SPH = S::SPH;
   extern __shared__ __align__(128) float smem[];
