@@ -5,9 +5,10 @@ cpu_baseline / ``--impl reference`` legs may import this package. The product
 package (paper_2510_16154_b200) never imports it and shares no code with it.
 
 Parity status: every function here is pinned by tests/test_oracle_pins.py
- except the composite agent+TV trajectory, which is
-"parity unpinned" beyond the invariants P8 (mean) and P9 (constant fixed point)
-(DESIGN.md §3).
+ except the composite agent+TV trajectory, which has no
+closed form and is pinned by invariants only: P8 (mean), P9
+(constant fixed point), P21 (transpose / channel-permutation equivariance,
+tests/test_oracle_symmetry.py).
 """
 from __future__ import annotations
 

@@ -11,8 +11,9 @@
  *   vector fields  p[H][W][2C]           components (x,0..C-1) then (y,0..C-1)
  *
  * Parity status per function is stated in DESIGN.md §3 ("pins"); the composite
- * trajectory with the agent term on is "parity unpinned" beyond the invariants
- * P8/P9.
+ * trajectory with the agent term on has no closed form and is
+ * pinned by invariants only: P8 (means), P9 (constant image), P21 (transpose and
+ * channel-permutation equivariance, tests/test_oracle_symmetry.py).
  */
 #ifndef MSA_ORACLE_H
 #define MSA_ORACLE_H
