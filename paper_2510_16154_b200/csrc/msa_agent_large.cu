@@ -89,8 +89,7 @@ __global__ void __launch_bounds__(32 * TH2) k_agent_large(MsaGeom g, MsaIterCons
       const float4* row = snb + r * SWL + tx + R;
       const float* omr = som + (dy - dyl) * OW + R;
       const int dxl = max(-m, -x), dxh = min(m, W - 1 - x);
-      for (int dx = dxl; dx <= dxh; ++dx) {
-        if (dx == 0 && dy == 0) continue;
+      auto term = [&](int dx) {
         const float4 nb = row[dx];
         const float nv[4] = {nb.x, nb.y, nb.z, nb.w};
         float cj[C];
@@ -100,6 +99,14 @@ __global__ void __launch_bounds__(32 * TH2) k_agent_large(MsaGeom g, MsaIterCons
           msa_agent_term_s<C, KER>(ci, cj, omr[dx], K.m4, acc);
         else
           msa_agent_term<C, KER>(ci, cj, omr[dx], K.e_c, acc);
+      };
+      // ascending dx; the centre (dx = dy = 0) split out of the loop so it can be unrolled
+      const int mid = dy == 0 ? min(-1, dxh) : dxh;
+#pragma unroll 4
+      for (int dx = dxl; dx <= mid; ++dx) term(dx);
+      if (dy == 0) {
+#pragma unroll 4
+        for (int dx = max(1, dxl); dx <= dxh; ++dx) term(dx);
       }
     }
   }
@@ -272,8 +279,7 @@ __global__ void __launch_bounds__(32 * TH2) k_dal_back_large(MsaGeom g, int R, i
       const float4* lrow = sl + r * SWL + tx + R;
       const float* arow = sa + (dy - dyl) * OW + R;
       const int dxl = max(-m, -x), dxh = min(m, W - 1 - x);
-      for (int dx = dxl; dx <= dxh; ++dx) {
-        if (dx == 0 && dy == 0) continue;
+      auto term = [&](int dx) {
         const float4 cv = crow[dx], lv = lrow[dx];
         const float cn[4] = {cv.x, cv.y, cv.z, cv.w}, ln[4] = {lv.x, lv.y, lv.z, lv.w};
         const float a2 = arow[dx];
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(32 * TH2) k_dal_back_large(MsaGeom g, int R, i
           dli = __fmaf_rn(d[k], li[k], dli);
         }
         const float t = fmaxf(1.0f - __fmaf_rn(e_c, s2, a2), 0.0f);
-        if (t <= 0.0f) continue;
+        if (t <= 0.0f) return;
         const float t2 = __fmul_rn(t, t), t4 = __fmul_rn(t2, t2), t3 = __fmul_rn(t2, t);
         const float ph = __fmul_rn(t4, __fmaf_rn(-4.0f, t, ker == 0 ? 5.0f : 3.0f));
         const float rr = 1.0f - t;
@@ -297,6 +303,14 @@ __global__ void __launch_bounds__(32 * TH2) k_dal_back_large(MsaGeom g, int R, i
         for (int k = 0; k < C; ++k) acc[k] = __fmaf_rn(ph, dl[k], __fmaf_rn(f, d[k], acc[k]));
         sx = __fmaf_rn(__fmul_rn(dph, a2), dli, sx);
         scc = __fmaf_rn(__fmul_rn(dph, 0.5f * s2), dli, scc);
+      };
+      // ascending dx; the centre split out of the loop so it can be unrolled
+      const int mid = dy == 0 ? min(-1, dxh) : dxh;
+#pragma unroll 4
+      for (int dx = dxl; dx <= mid; ++dx) term(dx);
+      if (dy == 0) {
+#pragma unroll 4
+        for (int dx = max(1, dxl); dx <= dxh; ++dx) term(dx);
       }
     }
   }
