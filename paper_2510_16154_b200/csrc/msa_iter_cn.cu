@@ -109,15 +109,22 @@ __global__ void __launch_bounds__(NT, CN_OCC)
       ci[k] = sc[(k * SH + ty + R) * CW + CX + tx];
       acc[k] = 0.0f;
     }
-    for (int o = 0; o < T.n; ++o) {
-      const int dx = T.dx[o], dy = T.dy[o];
-      const int xx = x + dx, yy = y + dy;
-      if (xx < 0 || xx >= W || yy < 0 || yy >= H) continue;  // excluded, not padded (R20)
+    auto term = [&](int o) {
+      const float* src = sc + (ty + R + T.dy[o]) * CW + CX + tx + T.dx[o];
       float cj[C];
-      const float* src = sc + (ty + R + dy) * CW + CX + tx + dx;
 #pragma unroll
       for (int k = 0; k < C; ++k) cj[k] = src[k * SH * CW];
       msa_agent_term_s<C, KER>(ci, cj, T.om[o], K.m4, acc);
+    };
+    if (x0 - R >= 0 && x0 + TW + R <= W && y0 - R >= 0 && y0 + TH + R <= H) {  // interior tile
+#pragma unroll 4
+      for (int o = 0; o < T.n; ++o) term(o);
+    } else {
+      for (int o = 0; o < T.n; ++o) {
+        const int xx = x + T.dx[o], yy = y + T.dy[o];
+        if (xx < 0 || xx >= W || yy < 0 || yy >= H) continue;  // excluded, not padded (R20)
+        term(o);
+      }
     }
 #pragma unroll
     for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_s, acc[k], ci[k]);
