@@ -139,6 +139,13 @@ def test_config_parity(case):
     (dict(kappa=1.7, theta=0.0), 3), # penalty growth, no extrapolation
     (dict(eps_x=50.0, radius=4), 3), # small eps_x: ring offsets active -> generic kernel
     (dict(kernel=1), 1),             # printed (repulsive) kernel, grey
+    # the scaled step-1 form (MsaIterConsts::scaled) holds for e_c = eps_c/2 in [1e-3, 1e3]; outside
+    # it the direct form runs (generic kernel): both ends of the range and both sides of it
+    (dict(eps_c=0.0), 3),
+    (dict(eps_c=1e-4), 3),
+    (dict(eps_c=2e-3), 3),
+    (dict(eps_c=1999.0), 3),
+    (dict(eps_c=2100.0), 3),
 ])
 def test_degenerate_and_extreme_params(over, C):
     rng = np.random.default_rng(len(str(over)) + C)
