@@ -244,7 +244,9 @@ int msa_get_timing(msa_ctx* ctx, double* iter_ms, int64_t* iter_launches, double
  * eps: host float64 [steps][2] (initial guess in, optimised control out, projected onto E).
  * v, mu: host float32 [H][W][2C] for cost 1 (NULL = 0). J_hist[iters + 1], sigma_hist[iters]:
  * host or NULL (sigma <= 0: no admissible step that iteration). On return c = cbar = c(T; eps).
- * The trajectory (steps + 1 fields) is kept on the device. Synchronises. */
+ * The trajectory (steps + 1 fields) is kept on the device; when it would take more than 70 % of
+ * the free device memory, sqrt(steps)-spaced checkpoints are kept instead and each segment is
+ * recomputed before its adjoint steps (same gradient bit for bit). Synchronises. */
 typedef struct {
   int32_t steps;      /* M >= 1 */
   int32_t cost;       /* 0 or 1, see above */

@@ -9,6 +9,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "../../include/msa.h"
@@ -1324,6 +1325,10 @@ struct DalBuffers {
   float *lam0 = nullptr, *lam1 = nullptr, *q = nullptr, *v = nullptr, *mu = nullptr;
   float* split = nullptr;  // window-split partial sums of the large-support sweeps: 4 (C + 2) planes
   size_t split_floats = 0;
+  // checkpointing (gradient sweeps, S > 0): traj holds the states c(0), c(S), c(2S), ... (nck of them)
+  // followed by a segment buffer of S + 1 states; the backward sweep recomputes each segment from
+  // its checkpoint. S = 0: traj holds all M + 1 states.
+  int S = 0, nck = 0;
   double *partials = nullptr, *dev = nullptr;  // dev: [0] J, [2 + 2m] deps of step m
   ~DalBuffers() {
     void* ps[] = {traj, lam0, lam1, q, v, mu, split, partials, dev};
@@ -1350,7 +1355,24 @@ size_t plane_floats(const msa_ctx* x) { return (size_t)x->g.C * x->g.plane; }
 
 int dal_alloc(msa_ctx* x, const msa_dal_params* d, const float* v, const float* mu, DalBuffers& B, bool full) {
   const size_t pf = plane_floats(x), pf2 = 2 * pf;
-  const size_t slots = full ? (size_t)d->steps + 1 : 2;
+  size_t slots = full ? (size_t)d->steps + 1 : 2;
+  if (full) {
+    // the full trajectory is M + 1 fields (100 GB at 4096^2 RGB, M = 500): when it would take more
+    // than 70 % of the free memory, keep sqrt(M)-spaced checkpoints and recompute segments
+    // (one more forward sweep; the same states, so the same gradient bit for bit).
+    // MSA_DAL_CHECKPOINT=S forces segments of S steps (test hook).
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const char* e = getenv("MSA_DAL_CHECKPOINT");
+    int S = e ? atoi(e) : 0;
+    if (!e && (double)slots * pf * sizeof(float) > 0.7 * (double)fr)
+      S = (int)std::ceil(std::sqrt((double)d->steps));
+    if (S > 0 && S < d->steps) {
+      B.S = S;
+      B.nck = d->steps / S + 1;
+      slots = (size_t)B.nck + S + 1;
+    }
+  }
   CUDA_TRY(cudaMalloc((void**)&B.traj, sizeof(float) * pf * slots));
   CUDA_TRY(cudaMalloc((void**)&B.lam0, sizeof(float) * pf));
   CUDA_TRY(cudaMalloc((void**)&B.lam1, sizeof(float) * pf));
@@ -1378,20 +1400,29 @@ int dal_alloc(msa_ctx* x, const msa_dal_params* d, const float* v, const float* 
   return MSA_OK;
 }
 
-// forward sweep; full: keep every state in traj[m]; returns J (host) and leaves c(T) in the last slot
+// forward sweep; full: keep every state in traj[m] (or, checkpointed, every S-th state); returns J
+// (host) and leaves c(T) in *cT
 int dal_forward(msa_ctx* x, const msa_dal_params* d, const double* eps, DalBuffers& B, bool full, double* J,
                 float** cT) {
   const msa_params& P = x->prm;
   const size_t pf = plane_floats(x);
-  CUDA_TRY(cudaMemcpyAsync(B.traj, x->I, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
+  const bool ck = full && B.S > 0;
+  float* seg = B.traj + (size_t)B.nck * pf;  // checkpointed: ping-pong in the segment buffer
+  auto slot = [&](int m) -> float* {
+    if (ck) return seg + (size_t)(m & 1) * pf;
+    return B.traj + (full ? (size_t)m : (size_t)(m & 1)) * pf;
+  };
+  CUDA_TRY(cudaMemcpyAsync(slot(0), x->I, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
+  if (ck) CUDA_TRY(cudaMemcpyAsync(B.traj, x->I, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
   for (int m = 0; m < d->steps; ++m) {
-    const float* cm = B.traj + (full ? (size_t)m : (size_t)(m & 1)) * pf;
-    float* cn = B.traj + (full ? (size_t)(m + 1) : (size_t)((m + 1) & 1)) * pf;
-    CUDA_TRY(msa_dal_step(x->g, x->hx, x->hy, P.dt, P.radius, P.kernel, x->NR, eps[2 * m], eps[2 * m + 1], cm, cn,
-                          x->stream, B.split, B.split_floats));
+    CUDA_TRY(msa_dal_step(x->g, x->hx, x->hy, P.dt, P.radius, P.kernel, x->NR, eps[2 * m], eps[2 * m + 1], slot(m),
+                          slot(m + 1), x->stream, B.split, B.split_floats));
     ++x->launches;
+    if (ck && (m + 1) % B.S == 0)
+      CUDA_TRY(cudaMemcpyAsync(B.traj + (size_t)((m + 1) / B.S) * pf, slot(m + 1), sizeof(float) * pf,
+                               cudaMemcpyDeviceToDevice, x->stream));
   }
-  float* last = B.traj + (full ? (size_t)d->steps : (size_t)(d->steps & 1)) * pf;
+  float* last = slot(d->steps);
   CUDA_TRY(msa_dal_terminal(x->g, d->cost, P.rho, x->hx, x->hy, P.alpha, last, x->I, B.v, B.mu, B.q,
                             full ? B.lam0 : nullptr, B.partials, B.dev, x->stream));
   x->launches += full ? 3 : 2;
@@ -1410,12 +1441,31 @@ int dal_grad(msa_ctx* x, const msa_dal_params* d, const double* eps, DalBuffers&
   int rc = dal_forward(x, d, eps, B, true, J, nullptr);
   if (rc != MSA_OK) return rc;
   float *lam = B.lam0, *lam2 = B.lam1;
-  for (int m = d->steps - 1; m >= 0; --m) {
-    CUDA_TRY(msa_dal_back(x->g, x->hx, x->hy, P.dt, P.radius, P.kernel, x->NR, eps[2 * m], eps[2 * m + 1],
-                          B.traj + (size_t)m * pf, lam, lam2, B.partials, B.dev + 2 + 2 * m, x->stream, B.split,
-                          B.split_floats));
+  auto back = [&](int m, const float* cm) -> int {
+    CUDA_TRY(msa_dal_back(x->g, x->hx, x->hy, P.dt, P.radius, P.kernel, x->NR, eps[2 * m], eps[2 * m + 1], cm, lam,
+                          lam2, B.partials, B.dev + 2 + 2 * m, x->stream, B.split, B.split_floats));
     x->launches += 2;
     std::swap(lam, lam2);
+    return MSA_OK;
+  };
+  if (B.S == 0) {
+    for (int m = d->steps - 1; m >= 0; --m)
+      if ((rc = back(m, B.traj + (size_t)m * pf)) != MSA_OK) return rc;
+  } else {  // segments [k S, min((k+1) S, M)) from the last: recompute from checkpoint k, then adjoint
+    float* seg = B.traj + (size_t)B.nck * pf;
+    for (int k = (d->steps - 1) / B.S; k >= 0; --k) {
+      const int m0 = k * B.S, m1 = std::min(m0 + B.S, d->steps);
+      CUDA_TRY(cudaMemcpyAsync(seg, B.traj + (size_t)k * pf, sizeof(float) * pf, cudaMemcpyDeviceToDevice,
+                               x->stream));
+      for (int m = m0; m < m1 - 1; ++m) {
+        CUDA_TRY(msa_dal_step(x->g, x->hx, x->hy, P.dt, P.radius, P.kernel, x->NR, eps[2 * m], eps[2 * m + 1],
+                              seg + (size_t)(m - m0) * pf, seg + (size_t)(m - m0 + 1) * pf, x->stream, B.split,
+                              B.split_floats));
+        ++x->launches;
+      }
+      for (int m = m1 - 1; m >= m0; --m)
+        if ((rc = back(m, seg + (size_t)(m - m0) * pf)) != MSA_OK) return rc;
+    }
   }
   std::vector<double> de(2 * (size_t)d->steps);
   CUDA_TRY(cudaMemcpyAsync(de.data(), B.dev + 2, sizeof(double) * de.size(), cudaMemcpyDeviceToHost, x->stream));

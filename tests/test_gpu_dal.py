@@ -119,3 +119,45 @@ np.savez(sys.argv[2], J=np.array([J]), g=g)
     # the same terms in another order
     np.testing.assert_allclose(outs[2]["J"], outs[0]["J"], rtol=1e-6)
     np.testing.assert_allclose(outs[2]["g"], outs[0]["g"], rtol=1e-4, atol=1e-6 * float(np.max(np.abs(outs[0]["g"]))))
+
+
+@pytest.mark.parametrize("S,R,cost", [(3, 15, 0), (4, 3, 1), (1, 12, 0), (11, 3, 0)])
+def test_dal_gradient_checkpointing_bitwise(S, R, cost, tmp_path):
+    """Checkpointed adjoint (NEXT-1: the trajectory of M + 1 states does not fit at large images):
+    states every S steps, each segment recomputed before its adjoint steps - the same states, so
+    the same cost and gradient bit for bit as with the full trajectory (M = 10, ragged last
+    segment; S = 1 and S >= M - 1 are the degenerate ends)."""
+    import json
+    import subprocess
+    import sys
+    script = r"""
+import json, sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2510_16154_b200 as msa
+spec = json.loads(sys.argv[1])
+rng = np.random.default_rng(spec["seed"])
+H, W, C, R, M = 18, 21, 3, spec["R"], 10
+I = rng.random((1, H, W, C), dtype=np.float32)
+h = 1.0 / (W - 1)
+sp = dict(alpha=0.8 / h, beta=1.0, radius=R, kernel=0, eps_x=0.0, eps_c=57.0, dt=0.25, rho=0.5, gamma=0.5,
+          kappa=1.0, tau=0.0, sigma=0.0, theta=1.0, iters_per_round=1, rounds=1)
+eps = np.stack([rng.uniform(8.0, 200.0, M), rng.uniform(20.0, 120.0, M)], axis=1)
+v = (0.3 * rng.standard_normal((H, W, 2 * C))).astype(np.float32)
+mu = (0.3 * rng.standard_normal((H, W, 2 * C))).astype(np.float32)
+with msa.Solver(msa.Params.from_solver(1, H, W, C, sp), I) as s:
+    d = msa.DalParams(steps=M, cost=spec["cost"])
+    J, g = s.dal_gradient(d, eps, v if spec["cost"] else None, mu if spec["cost"] else None)
+np.savez(sys.argv[2], J=np.array([J]), g=g)
+""" % _os.path.dirname(HERE_DIR)
+    spec = dict(seed=S + R, R=R, cost=cost)
+    outs = []
+    for ck in (None, S):
+        env = dict(_os.environ)
+        env.pop("MSA_DAL_CHECKPOINT", None)
+        if ck is not None:
+            env["MSA_DAL_CHECKPOINT"] = str(ck)
+        out = str(tmp_path / f"ck{ck}.npz")
+        subprocess.run([sys.executable, "-c", script, json.dumps(spec), out], check=True, env=env)
+        outs.append(np.load(out))
+    assert np.array_equal(outs[0]["J"], outs[1]["J"])
+    assert np.array_equal(outs[0]["g"], outs[1]["g"])
