@@ -101,3 +101,10 @@ def test_no_cpu_fallback_without_gpu():
     import numpy as np
     with pytest.raises(RuntimeError, match="CUDA"):
         msa.Solver(_params(), np.zeros((1, 64, 64, 3), np.float32))
+
+
+def test_c_example_builds_against_the_abi():
+    """examples/quantize.c compiles and links against include/msa.h + libmsa.so with plain gcc."""
+    import __graft_entry__ as g
+    exe = g.build_examples()
+    assert os.path.exists(exe) and os.access(exe, os.X_OK)
