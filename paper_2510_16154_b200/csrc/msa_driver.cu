@@ -114,6 +114,10 @@ struct msa_ctx {
   // rows mode: halo exchange on its own stream, overlapped with the interior K1 launch (§8(e))
   cudaStream_t comm_stream = nullptr;
   cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+  // the boundary parts of a split iteration run on their own stream, concurrently with the
+  // interior launch's tail (one slab-edge tile row each: too small to fill the GPU alone)
+  cudaStream_t bnd_stream = nullptr;
+  cudaEvent_t ev_bnd = nullptr;
   // labels
   MsaLabelScratch* lab = nullptr;
   int32_t* lab_buf = nullptr;
@@ -521,23 +525,23 @@ int k1_variant() {
 
 // One K1 launch over the rows of geometry g (the whole slab, or an interior / boundary part):
 // the variant cascade sweep (opt-in) -> tiled C = 3 -> C = 16 -> generic.
-int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int o) {
+int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int o, cudaStream_t st) {
   const msa_params& P = x->prm;
   // large supports (NEXT-3): step 1 by the chunked n-body kernel into c[o], steps 2-3 generic
   if (P.radius > 8 && P.channels <= 4 && k1_variant() != K1_GENERIC) {
     // scratch for a window split at small images: cb[o] and p[o] (3C planes, contiguous) are
     // written only after step 1
     int nl = 1;
-    cudaError_t e = msa_launch_agent_large(g, KC, P.radius, x->d_omtab, x->c[s], x->c[o], x->stream, 0.0f, 0.0f,
+    cudaError_t e = msa_launch_agent_large(g, KC, P.radius, x->d_omtab, x->c[s], x->c[o], st, 0.0f, 0.0f,
                                            x->cb[o], (size_t)3 * g.nb * g.C * g.plane, &nl);
     if (e != cudaSuccess) return set_err(MSA_ECUDA, "large-support agent kernel: %s", cudaGetErrorString(e));
     x->launches += nl - 1;
     if (P.scheme == MSA_SCHEME_LINEARISED_ADMM)
-      e = msa_launch_iter_lin_generic(g, KC, x->d_off, x->d_om, x->c[s], x->p[s], x->I, x->c[o], x->p[o], x->stream,
+      e = msa_launch_iter_lin_generic(g, KC, x->d_off, x->d_om, x->c[s], x->p[s], x->I, x->c[o], x->p[o], st,
                                       x->c[o]);
     else
       e = msa_launch_iter_generic(g, KC, x->d_off, x->d_om, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
-                                  x->cb[o], x->p[o], x->stream, x->c[o]);
+                                  x->cb[o], x->p[o], st, x->c[o]);
     if (e != cudaSuccess) return set_err(MSA_ECUDA, "iteration kernel launch: %s", cudaGetErrorString(e));
     x->launches += 2;
     return MSA_OK;
@@ -546,12 +550,12 @@ int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int 
     int ok = 0;
     cudaError_t e = cudaErrorNotSupported;
     if (k1_variant() != K1_GENERIC)
-      e = msa_launch_iter_fast_lin(g, KC, x->T, P.radius, x->c[s], x->p[s], x->I, x->c[o], x->p[o], x->stream, &ok);
+      e = msa_launch_iter_fast_lin(g, KC, x->T, P.radius, x->c[s], x->p[s], x->I, x->c[o], x->p[o], st, &ok);
     if (!ok && e != cudaErrorNotSupported && e != cudaSuccess)
       return set_err(MSA_ECUDA, "linearised tiled kernel: %s", cudaGetErrorString(e));
     if (!ok)
       e = msa_launch_iter_lin_generic(g, KC, x->d_off, x->d_om, x->c[s], x->p[s], x->I, x->c[o], x->p[o],
-                                      x->stream);
+                                      st);
     if (e != cudaSuccess) return set_err(MSA_ECUDA, "linearised iteration kernel: %s", cudaGetErrorString(e));
     ++x->launches;
     return MSA_OK;
@@ -560,20 +564,20 @@ int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int 
   cudaError_t e = cudaErrorNotSupported;
   if (k1_variant() == K1_SWEEP)
     e = msa_launch_iter_sweep(g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
-                              x->p[o], x->stream, &launched);
+                              x->p[o], st, &launched);
   if (!launched && e != cudaErrorNotSupported && e != cudaSuccess)
     return set_err(MSA_ECUDA, "sweep iteration kernel: %s", cudaGetErrorString(e));
   if (!launched && k1_variant() != K1_GENERIC)
     e = msa_launch_iter_fast(g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
-                             x->p[o], x->stream, &launched);
+                             x->p[o], st, &launched);
   if (!launched && k1_variant() != K1_GENERIC && (e == cudaErrorNotSupported || e == cudaSuccess))
     e = msa_launch_iter_cn(g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
-                           x->p[o], x->stream, &launched);
+                           x->p[o], st, &launched);
   if (!launched) {
     if (e != cudaErrorNotSupported && e != cudaSuccess)
       return set_err(MSA_ECUDA, "fast iteration kernel: %s", cudaGetErrorString(e));
     e = msa_launch_iter_generic(g, KC, x->d_off, x->d_om, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o],
-                                x->cb[o], x->p[o], x->stream);
+                                x->cb[o], x->p[o], st);
   }
   if (e != cudaSuccess) return set_err(MSA_ECUDA, "iteration kernel launch: %s", cudaGetErrorString(e));
   ++x->launches;
@@ -600,6 +604,11 @@ int do_steps(msa_ctx* x, int64_t n) {
   static const bool force_split = getenv("MSA_K1_SPLIT") != nullptr;
   int lo = 0, hi = 0;
   const bool split = (rows && x->comm_stream) || force_split ? split_rows(x->g, &lo, &hi) : false;
+  if (split && !x->bnd_stream) {  // first split iteration: the boundary stream and its events
+    CUDA_TRY(cudaStreamCreateWithFlags(&x->bnd_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&x->ev_bnd, cudaEventDisableTiming));
+    if (!x->ev_ready) CUDA_TRY(cudaEventCreateWithFlags(&x->ev_ready, cudaEventDisableTiming));
+  }
   int rc;
   for (int64_t t = 0; t < n; ++t) {
     const int s = x->cur, o = 1 - s;
@@ -623,12 +632,19 @@ int do_steps(msa_ctx* x, int64_t n) {
       gi.k1_lo = lo; gi.k1_hi = hi;
       gb0.k1_lo = 0; gb0.k1_hi = lo;
       gb1.k1_lo = hi; gb1.k1_hi = x->g.nrows;
-      if ((rc = launch_k1(x, gi, KC, s, o)) != MSA_OK) return rc;
-      if (rows) CUDA_TRY(cudaStreamWaitEvent(x->stream, x->ev_halo, 0));
-      if ((rc = launch_k1(x, gb0, KC, s, o)) != MSA_OK) return rc;
-      if ((rc = launch_k1(x, gb1, KC, s, o)) != MSA_OK) return rc;
+      // fork: the boundary stream starts after everything before this iteration (and, in rows
+      // mode, after the halo exchange, which itself waits for that), so it reads the previous
+      // iteration's c, cbar, p; the interior launch runs meanwhile on the compute stream; join
+      // before the next iteration. The parts write disjoint rows.
+      if (!rows) CUDA_TRY(cudaEventRecord(x->ev_ready, x->stream));
+      if ((rc = launch_k1(x, gi, KC, s, o, x->stream)) != MSA_OK) return rc;
+      CUDA_TRY(cudaStreamWaitEvent(x->bnd_stream, rows ? x->ev_halo : x->ev_ready, 0));
+      if ((rc = launch_k1(x, gb0, KC, s, o, x->bnd_stream)) != MSA_OK) return rc;
+      if ((rc = launch_k1(x, gb1, KC, s, o, x->bnd_stream)) != MSA_OK) return rc;
+      CUDA_TRY(cudaEventRecord(x->ev_bnd, x->bnd_stream));
+      CUDA_TRY(cudaStreamWaitEvent(x->stream, x->ev_bnd, 0));
     } else {
-      if ((rc = launch_k1(x, x->g, KC, s, o)) != MSA_OK) return rc;
+      if ((rc = launch_k1(x, x->g, KC, s, o, x->stream)) != MSA_OK) return rc;
     }
     if (x->timing) ++x->iter_launches_t;  // iterations timed (a split iteration is three launches)
     x->cur = o;
@@ -683,6 +699,9 @@ void free_ctx(msa_ctx* x) {
   if (x->comm_stream) cudaStreamDestroy(x->comm_stream);
   if (x->ev_ready) cudaEventDestroy(x->ev_ready);
   if (x->ev_halo) cudaEventDestroy(x->ev_halo);
+  if (x->bnd_stream) cudaStreamSynchronize(x->bnd_stream);
+  if (x->bnd_stream) cudaStreamDestroy(x->bnd_stream);
+  if (x->ev_bnd) cudaEventDestroy(x->ev_bnd);
   msa_labels_free(x->lab);
   if (x->lab_buf) cudaFree(x->lab_buf);
   if (x->lab_count) cudaFree(x->lab_count);
