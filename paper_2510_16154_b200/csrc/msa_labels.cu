@@ -37,6 +37,7 @@ struct MsaLabelScratch {
   double* dscal = nullptr;                // [6] min/max of the hashed channel means
   void* grid = nullptr;                   // CellGrid (device)
   int32_t* merge_idx = nullptr;           // [N] slab merge: merged index of every concatenated segment
+  unsigned long long* cell_box = nullptr; // [NCELL][2][3] per-cell min / max of the hashed means (ordered bits)
 };
 
 namespace {
@@ -283,6 +284,39 @@ __global__ void k_seg_scatter(const int32_t* __restrict__ scal, const int32_t* _
   sorted[pos] = s;
 }
 
+// order-preserving map of doubles to unsigned 64-bit keys (and back), for atomic min / max
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ __forceinline__ double dunkey(unsigned long long k) {
+  return __longlong_as_double((long long)((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
+__global__ void k_cell_box_init(unsigned long long* box) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= NCELL_MAX) return;
+  for (int k = 0; k < 3; ++k) {
+    box[(size_t)c * 6 + k] = ~0ull;
+    box[(size_t)c * 6 + 3 + k] = 0ull;
+  }
+}
+
+// per-cell bounding box of the hashed channel means: box[cell][0][k] = min, [1][k] = max (keys)
+__global__ void k_cell_box(const int32_t* __restrict__ scal, int C, const double* __restrict__ mean,
+                           const int32_t* __restrict__ seg_cell, const CellGrid* __restrict__ G,
+                           unsigned long long* box) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= scal[0]) return;
+  const int dims = G->dims;
+  unsigned long long* b = box + (size_t)seg_cell[s] * 6;
+  for (int k = 0; k < dims; ++k) {
+    const unsigned long long key = dkey(mean[(size_t)s * C + k]);
+    atomicMin(b + k, key);
+    atomicMax(b + 3 + k, key);
+  }
+}
+
 __device__ __forceinline__ bool close_means(const double* mA, const double* mB, int C, double delta) {
   for (int k = 0; k < C; ++k)
     if (!(fabs(mA[k] - mB[k]) <= delta)) return false;
@@ -296,7 +330,7 @@ __device__ __forceinline__ bool close_means(const double* mA, const double* mB, 
 __global__ void k_seg_pairs(const int32_t* __restrict__ scal, int C, const double* __restrict__ mean,
                             const int32_t* __restrict__ seg_cell, const int32_t* __restrict__ start,
                             const int32_t* __restrict__ sorted, const CellGrid* __restrict__ G, double delta,
-                            int32_t* segP) {
+                            const unsigned long long* __restrict__ box, int32_t* segP) {
   const int q = blockIdx.x * blockDim.x + threadIdx.x;
   const int S = scal[0];
   if (q >= S) return;
@@ -333,6 +367,22 @@ __global__ void k_seg_pairs(const int32_t* __restrict__ scal, int C, const doubl
         int nb = c0;
         if (g.dims > 1) nb = nb * g.n[1] + c1;
         if (g.dims > 2) nb = nb * g.n[2] + c2;
+        if (start[nb] == start[nb + 1]) continue;
+        // the cell's bounding box (exact member values; fl(x - y) is monotone, so these tests agree
+        // with close_means member by member): some hashed channel farther than delta for every
+        // member -> no member is close; every member within delta in every channel (all channels
+        // hashed, cell already one set) -> unite with its first member without scanning
+        bool none = false, all = g.shortcut && g.dims == C;
+        for (int k = 0; k < g.dims; ++k) {
+          const double lo = dunkey(box[(size_t)nb * 6 + k]), hi = dunkey(box[(size_t)nb * 6 + 3 + k]);
+          if (mA[k] - hi > delta || lo - mA[k] > delta) none = true;
+          if (!(fabs(mA[k] - lo) <= delta && fabs(mA[k] - hi) <= delta)) all = false;
+        }
+        if (none) continue;
+        if (all) {
+          uf_unite(segP, A, sorted[start[nb]]);
+          continue;
+        }
         for (int r = start[nb]; r < start[nb + 1]; ++r) {
           const int B = sorted[r];
           if (close_means(mA, mean + (size_t)B * C, C, delta)) {
@@ -505,6 +555,7 @@ cudaError_t ensure_scratch(MsaLabelScratch** scratch, size_t n, int C) {
         (e = grow(&S->sorted, n)) || (e = grow(&S->seg_cell, n)) || (e = grow(&S->cl_sum, n * C)) ||
         (e = grow(&S->cl_cnt, n)) || (e = grow(&S->scalars, 4)) || (e = grow(&S->dscal, 6)) ||
         (e = grow(&S->merge_idx, n)) ||
+        (S->cell_box == nullptr && (e = cudaMalloc((void**)&S->cell_box, sizeof(unsigned long long) * 6 * NCELL_MAX))) ||
         (S->grid == nullptr && (e = cudaMalloc(&S->grid, 256))))
       return e;
     S->cap_px = n;
@@ -532,8 +583,11 @@ cudaError_t stage23(int n, int C, float delta, int32_t* count_dev, float* palett
   *launches += 3;
   if ((e = scan_excl(S->cell_count, NCELL_MAX + 1, S->scan_tmp, S->scan_tmp_n, st, launches))) return e;
   k_seg_scatter<<<nbN, T, 0, st>>>(S->scalars, S->seg_cell, S->cell_count, S->cell_fill, S->sorted);
+  k_cell_box_init<<<(NCELL_MAX + T - 1) / T, T, 0, st>>>(S->cell_box);
+  k_cell_box<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, S->seg_cell, (const CellGrid*)S->grid, S->cell_box);
   k_seg_pairs<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, S->seg_cell, S->cell_count, S->sorted, (const CellGrid*)S->grid, (double)delta,
-                                 S->seg_parent);
+                                 S->cell_box, S->seg_parent);
+  *launches += 2;
   k_seg_compress<<<nbN, T, 0, st>>>(S->scalars, S->seg_parent, S->seg_flag);
   *launches += 3;
   // (iii) cluster ranks = exclusive scan of cluster-root flags over segments (segment order =
@@ -558,7 +612,7 @@ void msa_labels_free(MsaLabelScratch* s) {
   if (!s) return;
   void* ptrs[] = {s->parent, s->flag, s->scan_tmp, s->seg_parent, s->seg_flag, s->flag_copy, s->seg_sum, s->seg_cnt,
                   s->seg_mean, s->cell_count, s->cell_fill, s->sorted, s->seg_cell, s->cl_sum, s->cl_cnt,
-                  s->scalars, s->dscal, s->grid, s->merge_idx};
+                  s->scalars, s->dscal, s->grid, s->merge_idx, s->cell_box};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   delete s;
