@@ -10,6 +10,10 @@
 #include "../../include/msa.h"
 #include "msa_internal.h"
 
+#ifndef MSA_ROUND_RPT
+#define MSA_ROUND_RPT 4  // rows per thread of the round kernel
+#endif
+
 namespace {
 
 // ------------------------------------------------------------------ K1 generic
@@ -230,11 +234,13 @@ __global__ void __launch_bounds__(256) k_round(MsaGeom g, MsaRoundConsts R, cons
                                                double* __restrict__ partials) {
   constexpr int NS = MSA_S_MEAN0 + C;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int jl = blockIdx.y * blockDim.y + threadIdx.y;
   const int b = blockIdx.z;
   double acc[NS];
 #pragma unroll
   for (int s = 0; s < NS; ++s) acc[s] = 0.0;
+  // MSA_ROUND_RPT consecutive rows per thread (one block reduction per 32 x 8 RPT pixels)
+  for (int rr = 0; rr < MSA_ROUND_RPT; ++rr) {
+  const int jl = (blockIdx.y * blockDim.y + threadIdx.y) * MSA_ROUND_RPT + rr;
   if (i < g.W && jl < g.nrows) {
     const int j = g.row0 + jl, W = g.W, H = g.H;
     float gv[2 * C], mv[2 * C], pv[2 * C], a[2 * C];
@@ -283,6 +289,7 @@ __global__ void __launch_bounds__(256) k_round(MsaGeom g, MsaRoundConsts R, cons
     acc[MSA_S_TV] += sqrt((double)g2);
     const double nad = (double)na;
     acc[MSA_S_HUB] += nad <= R.beta / R.rho ? 0.5 * R.rho * nad * nad : R.beta * nad - R.beta * R.beta / (2.0 * R.rho);
+  }
   }
   // block reduction (fixed order): warp shuffle, then warp 0 over the warps
   __shared__ double red[8][NS];
@@ -402,12 +409,12 @@ cudaError_t msa_launch_iter_generic(const MsaGeom& g, const MsaIterConsts& K, co
   }
 }
 
-int msa_round_blocks(const MsaGeom& g) { return ((g.W + 31) / 32) * ((g.nrows + 7) / 8); }
+int msa_round_blocks(const MsaGeom& g) { return ((g.W + 31) / 32) * ((g.nrows + 8 * MSA_ROUND_RPT - 1) / (8 * MSA_ROUND_RPT)); }
 
 cudaError_t msa_launch_round(const MsaGeom& g, const MsaRoundConsts& R, const float* c, const float* p,
                              const float* mu, const float* I, float* mu_out, double* partials, int* nblk,
                              cudaStream_t s) {
-  dim3 blk(32, 8), grd((g.W + 31) / 32, (g.nrows + 7) / 8, g.nb);
+  dim3 blk(32, 8), grd((g.W + 31) / 32, (g.nrows + 8 * MSA_ROUND_RPT - 1) / (8 * MSA_ROUND_RPT), g.nb);
   *nblk = (int)(grd.x * grd.y);
   switch (g.C) {
 #define MSA_CASE(CC) \
