@@ -1,4 +1,5 @@
-// msa_iter_fast.cu - K1, the specialised fused iteration kernel (sm_100a) for C = 3.
+// msa_iter_fast.cu - K1, the specialised fused iteration kernel (sm_100a) for C = 1..4 channels
+// (grey - the paper's own images -, two-channel, RGB, RGBA; template parameter C).
 //
 // One CTA = one 32 x (8P) tile of output pixels, 256 threads: lane = column, 8 strips of P
 // rows. Per pixel it does SURVEY §8(a) steps 1-3 in one pass:
@@ -40,7 +41,6 @@ struct TmaSet {
 using namespace msa_tma;
 using namespace msa_f32x2;
 
-constexpr int C = 3;
 constexpr int TW = 32;           // tile width (= lanes)
 #ifndef MSA_TILE_NS
 #define MSA_TILE_NS 8
@@ -66,7 +66,7 @@ struct FastOm {
   float v[128];
 };
 
-template <int R, int P>
+template <int C, int R, int P>
 struct Smem {
   static constexpr int TH = NSTRIP * P;
   static constexpr int SH = TH + 2 * R;  // c tile rows
@@ -88,7 +88,7 @@ struct Smem {
 // One parity pass over the neighbour pairs of column dx: cache Cp[q] = rows (2q + PAR,
 // 2q + PAR + 1) of the column (cache row k = strip row k - m). MASK: zero the weight of
 // out-of-image neighbours (column mask cm, row validity from the global row of cache row k).
-template <int R, int P, bool MASK, int PAR, int M, bool CENTER>
+template <int C, int R, int P, bool MASK, int PAR, int M, bool CENTER>
 __device__ __forceinline__ void column_pass_m(const float* __restrict__ s, const FastOm& om, int& o, f2 M4, f2 QC,
                                               float cm, int yk0, int H, const f2 (&ci)[P / 2][C],
                                               f2 (&acc)[P / 2][C]) {
@@ -135,19 +135,19 @@ __device__ __forceinline__ void column_pass_m(const float* __restrict__ s, const
 }
 
 // both parity passes of a column of half-height M (even M: pairs starting on even cache rows first)
-template <int R, int P, bool MASK, int M, bool CENTER>
+template <int C, int R, int P, bool MASK, int M, bool CENTER>
 __device__ __forceinline__ void column_m(const float* __restrict__ s, const FastOm& om, int& o, f2 M4, f2 QC,
                                          float cm, int yk0, int H, const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
   if constexpr ((M & 1) == 0) {
-    column_pass_m<R, P, MASK, 0, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
-    column_pass_m<R, P, MASK, 1, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+    column_pass_m<C, R, P, MASK, 0, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+    column_pass_m<C, R, P, MASK, 1, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
   } else {
-    column_pass_m<R, P, MASK, 1, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
-    column_pass_m<R, P, MASK, 0, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+    column_pass_m<C, R, P, MASK, 1, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+    column_pass_m<C, R, P, MASK, 0, M, CENTER>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
   }
 }
 
-template <int R, int P, bool MASK>
+template <int C, int R, int P, bool MASK>
 __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const FastOm& om, float m4, float qc,
                                             int lx, int strip, int x, int ybase, int W, int H,
                                             const f2 (&ci)[P / 2][C], f2 (&acc)[P / 2][C]) {
@@ -172,37 +172,46 @@ __device__ __forceinline__ void agent_phase(const float* __restrict__ sc, const 
     // small enough for the instruction cache
     if (dx == 0) {
       if constexpr (col_m(R, 0) == 0) {
-      } else if constexpr (col_m(R, 0) == 1) column_m<R, P, MASK, 1, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
-      else if constexpr (col_m(R, 0) == 2) column_m<R, P, MASK, 2, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
-      else if constexpr (col_m(R, 0) == 3) column_m<R, P, MASK, 3, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
-      else column_m<R, P, MASK, 4, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      } else if constexpr (col_m(R, 0) == 1) column_m<C, R, P, MASK, 1, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      else if constexpr (col_m(R, 0) == 2) column_m<C, R, P, MASK, 2, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      else if constexpr (col_m(R, 0) == 3) column_m<C, R, P, MASK, 3, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      else column_m<C, R, P, MASK, 4, true>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
     } else if (m == 1) {
-      column_m<R, P, MASK, 1, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      column_m<C, R, P, MASK, 1, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
     } else if (m == 2) {
-      column_m<R, P, MASK, 2, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      column_m<C, R, P, MASK, 2, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
     } else if (m == 3) {
-      if constexpr (R >= 4) column_m<R, P, MASK, 3, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      if constexpr (R >= 4) column_m<C, R, P, MASK, 3, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
     } else {
-      if constexpr (R >= 5) column_m<R, P, MASK, 4, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
+      if constexpr (R >= 5) column_m<C, R, P, MASK, 4, false>(s, om, o, M4, QC, cm, yk0, H, ci, acc);
     }
   }
 }
 
-template <int P>
+// CTAs per SM the launch bounds ask for (register budget 64K / (256 x blocks)): C = 3 with P = 4
+// needs ~128 registers and 109 KB of shared memory (2 per SM); fewer channels need fewer of both
+template <int C, int P>
 struct Occ {
 #ifdef MSA_TILE_OCC
   static constexpr int blocks = MSA_TILE_OCC;
 #else
-  static constexpr int blocks = P >= 4 ? 2 : 3;
+#ifndef MSA_TILE_OCC_C1
+#define MSA_TILE_OCC_C1 4
+#endif
+#ifndef MSA_TILE_OCC_C2
+#define MSA_TILE_OCC_C2 3
+#endif
+  static constexpr int blocks =
+      C == 1 ? MSA_TILE_OCC_C1 : (C == 2 ? MSA_TILE_OCC_C2 : (P >= 4 ? 2 : (C == 4 ? 2 : 3)));
 #endif
 };
 
 // LIN = the single-loop linearised ADMM scheme (msa.h MSA_SCHEME_LINEARISED_ADMM): tm.p is mu
 // (in), tm.po mu+ (out); no cbar / mu / cbar+ traffic; the dual step takes grad c from the c tile.
-template <int R, int P, bool LIN>
-__global__ void __launch_bounds__(NT, Occ<P>::blocks)
-    k_iter_fast_c3(MsaGeom g, MsaIterConsts K, const __grid_constant__ FastOm om, const __grid_constant__ TmaSet tm) {
-  using S = Smem<R, P>;
+template <int C, int R, int P, bool LIN>
+__global__ void __launch_bounds__(NT, (Occ<C, P>::blocks))
+    k_iter_fast(MsaGeom g, MsaIterConsts K, const __grid_constant__ FastOm om, const __grid_constant__ TmaSet tm) {
+  using S = Smem<C, R, P>;
   constexpr int TH = S::TH, SH = S::SH, BH = S::BH, QH = S::QH, SPH = S::SPH;
   extern __shared__ __align__(128) float smem[];
   float* sc = smem;               // [C][SH][SW]    c tile + halo (step 1)
@@ -261,9 +270,9 @@ __global__ void __launch_bounds__(NT, Occ<P>::blocks)
   const float qc = K.kernel == 0 ? 5.0f : 3.0f;
   const bool interior = x0 - R >= 0 && x0 + TW + R <= W && y0 - R >= 0 && y0 + TH + R <= H;
   if (interior)
-    agent_phase<R, P, false>(sc, om, K.m4, qc, lx, strip, x, ybase, W, H, ci, acc);
+    agent_phase<C, R, P, false>(sc, om, K.m4, qc, lx, strip, x, ybase, W, H, ci, acc);
   else
-    agent_phase<R, P, true>(sc, om, K.m4, qc, lx, strip, x, ybase, W, H, ci, acc);
+    agent_phase<C, R, P, true>(sc, om, K.m4, qc, lx, strip, x, ybase, W, H, ci, acc);
   const f2 DT = pk(K.dt_s, K.dt_s);
   float chalf[P][C];
 #pragma unroll
@@ -432,7 +441,7 @@ int kernel_order_index(int dx, int dy) {
 // small cache of encoded map sets (the ping-pong buffers of a few contexts)
 struct MapKey {
   const float *c, *cb, *p, *mu, *I, *co, *cbo, *po;
-  int W, rows, nb, pitch, R, P;
+  int W, rows, nb, pitch, R, P, C;
   long long plane;
   bool operator==(const MapKey& o) const { return memcmp(this, &o, sizeof(MapKey)) == 0; }
 };
@@ -448,6 +457,7 @@ bool get_maps(const MapKey& k, const MsaGeom& g, int SH, int BH, int QH, int TH,
       return true;
     }
   TmaSet t;
+  const int C = k.C;
   if (!encode_map(&t.c, g, k.c, C, SW, SH) || !encode_map(&t.cb, g, k.cb, C, BW, BH) ||
       !encode_map(&t.p, g, k.p, 2 * C, QW, QH) || !encode_map(&t.mu, g, k.mu, 2 * C, QW, QH) ||
       !encode_map(&t.I, g, k.I, C, TW, TH) || !encode_map(&t.co, g, k.co, C, TW, TH, true) ||
@@ -460,21 +470,21 @@ bool get_maps(const MapKey& k, const MsaGeom& g, int SH, int BH, int QH, int TH,
   return true;
 }
 
-template <int R, int P, bool LIN>
+template <int C, int R, int P, bool LIN>
 cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om, const float* c, const float* cb,
                       const float* p, const float* mu, const float* I, float* co, float* cbo, float* po,
                       cudaStream_t s) {
-  using S = Smem<R, P>;
+  using S = Smem<C, R, P>;
   MapKey key;
   memset(&key, 0, sizeof(key));
   key.c = c; key.cb = cb; key.p = p; key.mu = mu; key.I = I; key.co = co; key.cbo = cbo; key.po = po;
-  key.W = g.W; key.rows = g.nrows + 2 * g.G; key.nb = g.nb; key.pitch = g.pitch; key.R = R; key.P = P;
+  key.W = g.W; key.rows = g.nrows + 2 * g.G; key.nb = g.nb; key.pitch = g.pitch; key.R = R; key.P = P; key.C = C;
   key.plane = g.plane;
   TmaSet tm;
   if (!get_maps(key, g, S::SH, S::BH, S::QH, S::TH, &tm)) return cudaErrorNotSupported;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_iter_fast_c3<R, P, LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+    cudaError_t e = cudaFuncSetAttribute(k_iter_fast<C, R, P, LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
@@ -492,11 +502,11 @@ cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = pdl && !K.no_pdl ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, k_iter_fast_c3<R, P, LIN>, g, K, om, tm);
+  return cudaLaunchKernelEx(&cfg, k_iter_fast<C, R, P, LIN>, g, K, om, tm);
 }
 
-template <int R, bool LIN>
-cudaError_t launch_c3(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, const float* c,
+template <int C, int R, bool LIN>
+cudaError_t launch_cr(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, const float* c,
                       const float* cb, const float* p, const float* mu, const float* I, float* co, float* cbo,
                       float* po, cudaStream_t s) {
   // om for every interior offset in the kernel's order. Interior offsets absent from the
@@ -511,9 +521,17 @@ cudaError_t launch_c3(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
     om.v[idx] = T.oms[o];
     prev = idx;
   }
-  static const int rows_per_thread = getenv("MSA_K1_P") ? atoi(getenv("MSA_K1_P")) : 4;  // A/B hook
-  if (rows_per_thread == 4) return launch_rp<R, 4, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
-  return launch_rp<R, 2, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
+  // P = 4 rows per thread (C <= 3); C = 4 takes P = 2 (the P = 4 tiles would need 145 KB of shared
+  // memory, one CTA per SM). MSA_K1_P=2 is an A/B hook for C = 3.
+  static const int rows_per_thread = getenv("MSA_K1_P") ? atoi(getenv("MSA_K1_P")) : 4;
+  if constexpr (C == 4) {
+    return launch_rp<C, R, 2, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
+  } else if constexpr (C == 3) {
+    if (rows_per_thread == 2) return launch_rp<C, R, 2, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
+    return launch_rp<C, R, 4, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
+  } else {
+    return launch_rp<C, R, 4, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
+  }
 }
 
 }  // namespace
@@ -526,18 +544,26 @@ cudaError_t launch_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffse
   *launched = 0;
   // test hook: MSA_FORCE_GENERIC=1 selects the generic kernel (bitwise-identical results)
   static const bool force_generic = getenv("MSA_FORCE_GENERIC") != nullptr;
-  if (g.C != 3 || force_generic || !K.scaled) return cudaErrorNotSupported;  // scaled form only
+  if (g.C < 1 || g.C > 4 || force_generic || !K.scaled) return cudaErrorNotSupported;  // scaled form only
   // every active offset must lie in the interior disc (true for eps_x >= the default)
   for (int o = 0; o < T.n; ++o)
     if (T.dx[o] * T.dx[o] + T.dy[o] * T.dy[o] >= R * R) return cudaErrorNotSupported;
   cudaError_t e;
-  switch (R) {
-    case 2: e = launch_c3<2, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
-    case 3: e = launch_c3<3, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
-    case 4: e = launch_c3<4, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
-    case 5: e = launch_c3<5, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break;
-    default: return cudaErrorNotSupported;
+#define MSA_FAST_R(CC)                                                                           \
+  switch (R) {                                                                                   \
+    case 2: e = launch_cr<CC, 2, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break; \
+    case 3: e = launch_cr<CC, 3, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break; \
+    case 4: e = launch_cr<CC, 4, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break; \
+    case 5: e = launch_cr<CC, 5, LIN>(g, K, T, c, cb, p, mu, I, c_out, cb_out, p_out, s); break; \
+    default: return cudaErrorNotSupported;                                                       \
   }
+  switch (g.C) {
+    case 1: MSA_FAST_R(1) break;
+    case 2: MSA_FAST_R(2) break;
+    case 3: MSA_FAST_R(3) break;
+    default: MSA_FAST_R(4) break;
+  }
+#undef MSA_FAST_R
   if (e == cudaSuccess) *launched = 1;
   return e;
 }

@@ -47,6 +47,9 @@ CASES = [
 ]
 # many-channel tiled kernel (msa_iter_cn.cu, C = 16): same contract, bitwise equal to the generic one
 CN_CASES = [((2, 40, 36, 16), 3, 0), ((1, 33, 70, 16), 4, 1), ((1, 9, 5, 16), 2, 0), ((1, 64, 64, 16), 1, 0)]
+# the tiled kernel for grey (the paper's images), two-channel and RGBA fields (C = 1, 2, 4)
+C_CASES = [((1, 64, 32, 1), 5, 0), ((2, 70, 45, 1), 3, 1), ((1, 37, 29, 2), 4, 0), ((1, 100, 66, 2), 5, 0),
+           ((1, 48, 40, 4), 5, 0), ((2, 33, 70, 4), 2, 1), ((1, 1, 50, 1), 2, 0)]
 
 
 def _spec(shape, R, ker, iters=3):
@@ -57,7 +60,7 @@ def _spec(shape, R, ker, iters=3):
                             gamma=2.5 * h, iters_per_round=2, rounds=1))
 
 
-@pytest.mark.parametrize("shape,R,ker", CASES + CN_CASES)
+@pytest.mark.parametrize("shape,R,ker", CASES + CN_CASES + C_CASES)
 def test_tile_equals_generic_bitwise(shape, R, ker, tmp_path):
     spec = _spec(shape, R, ker)
     a = _run(spec, "generic", tmp_path)
