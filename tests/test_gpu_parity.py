@@ -40,7 +40,8 @@ def _oracle_state(prm, I, c, cb, p, mu):
 
 
 @pytest.mark.parametrize("H,W,C,R", [(23, 37, 1, 2), (40, 33, 3, 2), (45, 70, 3, 3), (50, 61, 3, 5),
-                                     (19, 29, 16, 3), (17, 9, 2, 4), (1, 40, 3, 2), (33, 1, 3, 3), (1, 1, 3, 2)])
+                                     (19, 29, 16, 3), (17, 9, 2, 4), (1, 40, 3, 2), (33, 1, 3, 3), (1, 1, 3, 2),
+                                     (70, 45, 1, 5), (31, 44, 4, 5), (40, 36, 2, 3)])
 def test_single_iteration_random_state(H, W, C, R):
     """Steps 1-3 from an arbitrary state: c+, cbar+, p+ element by element."""
     rng = np.random.default_rng(1000 + H * W + C + R)
@@ -139,6 +140,8 @@ def test_config_parity(case):
     (dict(kappa=1.7, theta=0.0), 3), # penalty growth, no extrapolation
     (dict(eps_x=50.0, radius=4), 3), # small eps_x: ring offsets active -> generic kernel
     (dict(kernel=1), 1),             # printed (repulsive) kernel, grey
+    (dict(radius=5), 1),             # grey (the paper's image type) on the tiled kernel, R = 5
+    (dict(radius=4), 4),             # RGBA on the tiled kernel (P = 2 tiles)
     # the scaled step-1 form (MsaIterConsts::scaled) holds for e_c = eps_c/2 in [1e-3, 1e3]; outside
     # it the direct form runs (generic kernel): both ends of the range and both sides of it
     (dict(eps_c=0.0), 3),
