@@ -1,6 +1,9 @@
 // msa_driver.cu - the C ABI of include/msa.h: validation, partition, device memory,
 // the iteration/round schedule (SURVEY.md §8(c) oracle block, realised on the GPU),
-// NCCL halo exchange + all-reduce for row slabs, labels, state I/O.
+// NCCL halo exchange + all-reduce for row slabs, labels, state I/O, and the
+// host side of Algorithm 1 (DAL: two-way Armijo with the projection onto E).
+// The schedule follows Alg. 2: K fused iterations (reading R1), then the
+// multiplier round (lines 6-7) with rho <- kappa rho (reading R9).
 #include <dlfcn.h>
 #include <math.h>
 #include <nccl.h>

@@ -1,4 +1,6 @@
-// msa_iter_cn.cu - K1 for many channels (C = 16: BASELINE config 5), sm_100a.
+// msa_iter_cn.cu - K1 for many channels (C = 16: BASELINE config 5), sm_100a. The iteration is the
+// one of msa_kernels.cu (eq:MAsystem PAPER.md:86-95, eq:complete_square :397-404, eq:new_adjoint
+// :405-413).
 //
 // At C = 16 the iteration moves 704 bytes per pixel against ~1600 FP32 operations, so it is
 // HBM-bound (3.6 ms HBM floor vs 1.5 ms ALU floor per 32 x 1024^2 iteration): the

@@ -2,7 +2,8 @@
 // (grey - the paper's own images -, two-channel, RGB, RGBA; template parameter C).
 //
 // One CTA = one 32 x (8P) tile of output pixels, 256 threads: lane = column, 8 strips of P
-// rows. Per pixel it does SURVEY §8(a) steps 1-3 in one pass:
+// rows. Per pixel it does SURVEY §8(a) steps 1-3 in one pass (eq:MAsystem
+// PAPER.md:86-95 with eq:kernel :259-267; eq:complete_square :397-404; eq:new_adjoint :405-413):
 //   loads     one elected thread issues TMA bulk-tensor loads (zero-filled outside the tensor) of
 //             the c tile + R halo on mbarrier 0, then - landing while step 1 computes - cbar
 //             (+1 halo), p and mu (+1 low-side halo) and I on mbarrier 1;

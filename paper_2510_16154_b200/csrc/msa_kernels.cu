@@ -4,7 +4,10 @@
 //   K2   msa_round          multiplier round (steps 4-5) + per-block fp64 partial sums
 //   K3   msa_reduce/record  deterministic reduction of the partials into a round record
 //   pack/unpack             interleaved ABI layout <-> planar device layout
-// Passages: see include/msa.h and DESIGN.md §1.
+// Passages: step 1 eq:MAsystem PAPER.md:86-95 with eq:ellipsoid :97-102, eq:kernel :259-267 and the
+// explicit Euler step :270; steps 2-3 eq:complete_square :397-404, eq:soft_threshold :431-440,
+// eq:new_adjoint :405-413; the round Alg. 2 lines 6-7 :456-457; the statistics eq:cost_TV :346-350
+// (readings in DESIGN.md §2; the per-function contract in include/msa.h).
 #include <math.h>
 
 #include "../../include/msa.h"
