@@ -523,24 +523,24 @@ cudaError_t launch_cr(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
     prev = idx;
   }
   // P = 4 rows per thread (C <= 3); C = 4 takes P = 2 (the P = 4 tiles would need 145 KB of shared
-  // memory, one CTA per SM). MSA_K1_P=2 / 4 forces the choice for C = 3 (A/B hook).
+  // memory, one CTA per SM). MSA_K1_P=2 / 4 forces the choice for C <= 3 (A/B hook).
   static const int rows_per_thread = getenv("MSA_K1_P") ? atoi(getenv("MSA_K1_P")) : 0;
   if constexpr (C == 4) {
     return launch_rp<C, R, 2, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
-  } else if constexpr (C == 3) {
-    // small images (fewer 32 x 32 tiles than one wave at two CTAs per SM: cfg 1-2) are latency-bound:
-    // 32 x 16 tiles double the CTAs and halve each one's critical path (cfg1 5.0 -> 3.7 us/iteration)
+  } else {
+    // small images (fewer 32 x 32 tiles than one wave of resident CTAs: cfg 1-2, the paper's
+    // small grey images) are latency-bound: 32 x 16 tiles double the CTAs and halve each one's
+    // critical path (cfg1 5.0 -> 3.7 us/iteration)
     static int sms = 0;
     if (!sms) {
       int dev = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const long long tiles4 = (long long)((g.W + TW - 1) / TW) * ((msa_k1_hi(g) - g.k1_lo + NSTRIP * 4 - 1) / (NSTRIP * 4)) * g.nb;
-    const bool p2 = rows_per_thread ? rows_per_thread == 2 : tiles4 < 2LL * sms;
+    const long long tiles4 = (long long)((g.W + TW - 1) / TW) *
+                             ((msa_k1_hi(g) - g.k1_lo + NSTRIP * 4 - 1) / (NSTRIP * 4)) * g.nb;
+    const bool p2 = rows_per_thread ? rows_per_thread == 2 : tiles4 < (long long)Occ<C, 4>::blocks * sms;
     if (p2) return launch_rp<C, R, 2, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
-    return launch_rp<C, R, 4, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
-  } else {
     return launch_rp<C, R, 4, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
   }
 }
