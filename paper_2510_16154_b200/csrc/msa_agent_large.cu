@@ -171,12 +171,7 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const floa
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   // 32 x 8 tiles unless that leaves SMs idle (fewer than two tiles per SM): then 32 x 2
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = msa_sm_count();
   const long long tiles8 = (long long)((g.W + TW - 1) / TW) * ((nr + TH - 1) / TH) * g.nb;
   *launches = 1;
   if (tiles8 >= 2LL * sms) return launch_th<C, TH>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr, Split{1, nullptr});
@@ -389,12 +384,7 @@ template <int C>
 cudaError_t dal_back_c(const MsaGeom& g, int R, int kernel, float exh_x, float exh_y, float e_c, float eps_c,
                        float inv_NR, float dt, const float* c, const float* lam, float* lam_out, double* partials,
                        float* scratch, size_t scratch_floats, cudaStream_t s) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = msa_sm_count();
   const int nx = (g.W + TW - 1) / TW;
   const long long tiles8 = (long long)nx * ((g.H + TH - 1) / TH);
   const size_t per_part = (size_t)(C + 2) * g.plane;

@@ -12,6 +12,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 #include <cmath>
 #include <vector>
 
@@ -42,6 +43,8 @@ struct NcclApi : MsaNcclFns {
 NcclApi g_nccl;
 
 bool nccl_load() {
+  static std::mutex mu;  // contexts may be created from several threads
+  std::lock_guard<std::mutex> lock(mu);
   if (g_nccl.tried) return g_nccl.ok;
   g_nccl.tried = true;
   if (getenv("MSA_NCCL_LOOPBACK")) {  // test hook: in-process ranks (msa_nccl_loopback.cu)

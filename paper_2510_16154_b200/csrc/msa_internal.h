@@ -146,3 +146,6 @@ struct MsaNcclFns {
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
 };
 MsaNcclFns msa_nccl_loopback();
+
+// SM count of the current device (queried once, thread-safe)
+int msa_sm_count();

@@ -215,12 +215,9 @@ template <int C, int R, int KER>
 cudaError_t launch_k(const MsaGeom& g, const MsaIterConsts& K, const CnOffsets& T, const CnMaps& tm, const float* p,
                      const float* mu, const float* I, float* co, float* cbo, float* po, cudaStream_t s) {
   using S = CnSmem<C, R>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_iter_cn<C, R, KER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static const cudaError_t attr =  // once per instantiation (thread-safe static init)
+      cudaFuncSetAttribute(k_iter_cn<C, R, KER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+  if (attr != cudaSuccess) return attr;
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   dim3 grd((g.W + TW - 1) / TW, (nr + TH - 1) / TH, g.nb);

@@ -483,12 +483,9 @@ cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om
   key.plane = g.plane;
   TmaSet tm;
   if (!get_maps(key, g, S::SH, S::BH, S::QH, S::TH, &tm)) return cudaErrorNotSupported;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_iter_fast<C, R, P, LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static const cudaError_t attr =  // once per instantiation (thread-safe static init)
+      cudaFuncSetAttribute(k_iter_fast<C, R, P, LIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+  if (attr != cudaSuccess) return attr;
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   dim3 grd((g.W + TW - 1) / TW, (nr + S::TH - 1) / S::TH, g.nb);
@@ -531,12 +528,7 @@ cudaError_t launch_cr(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
     // small images (fewer 32 x 32 tiles than one wave of resident CTAs: cfg 1-2, the paper's
     // small grey images) are latency-bound: 32 x 16 tiles double the CTAs and halve each one's
     // critical path (cfg1 5.0 -> 3.7 us/iteration)
-    static int sms = 0;
-    if (!sms) {
-      int dev = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int sms = msa_sm_count();
     const long long tiles4 = (long long)((g.W + TW - 1) / TW) *
                              ((msa_k1_hi(g) - g.k1_lo + NSTRIP * 4 - 1) / (NSTRIP * 4)) * g.nb;
     const bool p2 = rows_per_thread ? rows_per_thread == 2 : tiles4 < (long long)Occ<C, 4>::blocks * sms;

@@ -509,17 +509,16 @@ cudaError_t launch_r(const MsaGeom& g, const MsaIterConsts& K, const SweepOm& om
   SweepMaps tm;
   if (!get_maps(key, g, &tm)) return cudaErrorNotSupported;
   const size_t smem = NW * sizeof(WarpSmem);
-  static int slots = 0;
-  if (slots == 0) {
-    cudaError_t e = cudaFuncSetAttribute(k_iter_sweep_c3<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, nsm = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iter_sweep_c3<R>, NW * 32, smem);
-    if (e != cudaSuccess) return e;
-    slots = std::max(1, nsm * per_sm * NW);
-  }
+  // resident warp slots of the device, computed once per instantiation (thread-safe static init)
+  static const int slots = [&]() -> int {
+    if (cudaFuncSetAttribute(k_iter_sweep_c3<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return -1;
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_iter_sweep_c3<R>, NW * 32, smem) != cudaSuccess)
+      return -1;
+    return std::max(1, msa_sm_count() * per_sm * NW);
+  }();
+  if (slots < 0) return cudaErrorInvalidValue;
   const SweepPlan pl = make_plan(g, OW, slots);
   const int grid = (pl.units + NW - 1) / NW;
   k_iter_sweep_c3<R><<<grid, NW * 32, smem, s>>>(g, K, om, pl, tm);

@@ -455,3 +455,13 @@ cudaError_t msa_launch_unpack(const MsaGeom& g, int nm, const float* inter, floa
   k_unpack<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(g, nm, inter, planar);
   return cudaGetLastError();
 }
+
+int msa_sm_count() {
+  static const int n = [] {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 1;
+  }();
+  return n;
+}
