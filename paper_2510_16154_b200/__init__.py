@@ -244,17 +244,33 @@ def _torch():
     return torch
 
 
-def _ptr_of(x) -> tuple[int, int, object]:
-    """(pointer, on_device, keepalive) of a numpy array or a torch tensor."""
+def _ptr_of(x, n: int | None = None, what: str = "buffer", out: bool = False, dtype=np.float32):
+    """(pointer, on_device, keepalive) of a numpy array or a torch tensor of n elements of dtype.
+    Inputs are converted (numpy) or made contiguous (torch); outputs must already be contiguous
+    and of the right dtype, since the library writes into them. Sizes are checked: the library
+    trusts them."""
     if isinstance(x, np.ndarray):
-        x = np.ascontiguousarray(x)
+        if out:
+            if x.dtype != dtype or not x.flags.c_contiguous or not x.flags.writeable:
+                raise TypeError(f"{what}: need a writeable C-contiguous {np.dtype(dtype).name} array")
+        else:
+            x = np.ascontiguousarray(x, dtype=dtype)
+        if n is not None and x.size != n:
+            raise ValueError(f"{what}: expected {n} elements, got {x.size} (shape {x.shape})")
         return x.ctypes.data, 0, x
     torch = _torch()
     if isinstance(x, torch.Tensor):
+        tdt = {np.float32: torch.float32, np.int32: torch.int32}[dtype]
+        if x.dtype != tdt:
+            raise TypeError(f"{what}: need a {tdt} tensor, got {x.dtype}")
         if not x.is_contiguous():
+            if out:
+                raise TypeError(f"{what}: output tensor must be contiguous")
             x = x.contiguous()
+        if n is not None and x.numel() != n:
+            raise ValueError(f"{what}: expected {n} elements, got {x.numel()} (shape {tuple(x.shape)})")
         return x.data_ptr(), int(x.is_cuda), x
-    raise TypeError(f"unsupported buffer type {type(x)}")
+    raise TypeError(f"{what}: unsupported buffer type {type(x)}")
 
 
 class Solver:
@@ -280,7 +296,7 @@ class Solver:
             stream = torch.cuda.current_stream(dev)
         self._stream = stream
         sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream or 0)
-        ptr, on_dev, keep = _ptr_of(image)
+        ptr, on_dev, keep = _ptr_of(image, params.batch * params.height * params.width * params.channels, "image")
         ctx = ctypes.c_void_p()
         _check(L.msa_init(ctypes.byref(cp), ptr, on_dev, ws_ptr, nbytes, sptr or None, ctypes.byref(ctx)))
         self._ctx = ctx
@@ -305,7 +321,8 @@ class Solver:
 
     # -- hot path
     def reset(self, image) -> None:
-        ptr, on_dev, keep = _ptr_of(image)
+        p = self.params
+        ptr, on_dev, keep = _ptr_of(image, p.batch * p.height * p.width * p.channels, "image")
         _check(lib().msa_reset(self._ctx, ptr, on_dev))
         if not on_dev:
             self.sync()
@@ -332,6 +349,15 @@ class Solver:
                                     pal.ctypes.data if pal is not None else None, max_k, 0))
             return lab, cnt, pal
         lab, cnt, pal = out  # torch CUDA tensors
+        for t, n, dt, what in ((lab, nb * H * W, np.int32, "labels"), (cnt, nb, np.int32, "n_clusters"),
+                               (pal, nb * max_k * C, np.float32, "palette")):
+            if t is None:
+                continue
+            ptr, on_dev, _ = _ptr_of(t, n, what, out=True, dtype=dt)
+            if not on_dev:
+                raise TypeError(f"{what}: out= takes CUDA tensors (device outputs)")
+        if max_k > 0 and pal is None:
+            raise ValueError("palette tensor needed when max_k > 0")
         _check(lib().msa_labels(self._ctx, ctypes.c_float(delta), lab.data_ptr(), cnt.data_ptr(),
                                 pal.data_ptr() if pal is not None else None, max_k, 1))
         return lab, cnt, pal
@@ -345,12 +371,15 @@ class Solver:
             out = np.empty((info.nimages, info.nrows, self.params.width, nm), dtype=np.float32)
             _check(lib().msa_get_field(self._ctx, which, out.ctypes.data, 0, None, None))
             return out
-        ptr, on_dev, keep = _ptr_of(out)
+        ptr, on_dev, keep = _ptr_of(out, info.nimages * info.nrows * self.params.width * nm, "out", out=True)
         _check(lib().msa_get_field(self._ctx, which, ptr, on_dev, None, None))
         return out
 
     def set_field(self, which: int, arr) -> None:
-        ptr, on_dev, keep = _ptr_of(arr if not isinstance(arr, np.ndarray) else np.ascontiguousarray(arr, np.float32))
+        info = self.query()
+        C = self.params.channels
+        nm = 2 * C if which in (FIELD_P, FIELD_MU) else C
+        ptr, on_dev, keep = _ptr_of(arr, info.nimages * info.nrows * self.params.width * nm, "field")
         _check(lib().msa_set_field(self._ctx, which, ptr, on_dev))
 
     def stats(self) -> list[dict]:

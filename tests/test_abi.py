@@ -108,3 +108,26 @@ def test_c_example_builds_against_the_abi():
     import __graft_entry__ as g
     exe = g.build_examples()
     assert os.path.exists(exe) and os.access(exe, os.X_OK)
+
+
+def test_binding_rejects_wrong_buffers():
+    """The binding checks dtype and element count before the library sees a pointer (the C ABI
+    trusts the sizes it is given)."""
+    import numpy as np
+    f = msa._ptr_of
+    ptr, on_dev, keep = f(np.zeros((2, 3), np.float64), 6, "x")  # inputs are converted
+    assert keep.dtype == np.float32 and on_dev == 0
+    with pytest.raises(ValueError):
+        f(np.zeros(5, np.float32), 6, "x")
+    with pytest.raises(TypeError):
+        f(np.zeros(6, np.float64), 6, "x", out=True)  # outputs are not converted
+    with pytest.raises(TypeError):
+        f(np.zeros((3, 4), np.float32)[:, :2], 6, "x", out=True)  # non-contiguous output
+    with pytest.raises(TypeError):
+        f([0.0] * 6, 6, "x")
+    import torch
+    with pytest.raises(TypeError):
+        f(torch.zeros(6, dtype=torch.float64), 6, "x")
+    with pytest.raises(ValueError):
+        f(torch.zeros(7), 6, "x")
+    assert f(torch.zeros(6), 6, "x")[1] == 0
