@@ -60,3 +60,39 @@ def test_random_parameters_match_oracle(seed):
         assert r["rho"] == pytest.approx(o[6], rel=1e-12)
         if sp["alpha"] > 0:
             assert r["primal"] == pytest.approx(o[2], rel=1e-3, abs=1e-6)
+
+
+def _label_field(seed):
+    """Fields built to stress stage (ii): few colour levels plus small noise (many segments whose
+    means straddle delta and the cell boundaries), random shapes, channel counts and delta."""
+    rng = np.random.default_rng(70000 + seed)
+    C = int(rng.choice([1, 2, 3, 4, 7, 16]))
+    H, W = int(rng.integers(1, 120)), int(rng.integers(1, 120))
+    B = int(rng.choice([1, 2]))
+    levels = int(rng.integers(2, 6))
+    base = np.round(rng.random((B, H, W, C)) * (levels - 1)) / (levels - 1)
+    if rng.random() < 0.5:  # blocky regions instead of per-pixel levels
+        bh, bw = max(H // int(rng.integers(1, 6)), 1), max(W // int(rng.integers(1, 6)), 1)
+        base = np.repeat(np.repeat(base[:, ::bh, ::bw], bh, 1), bw, 2)[:, :H, :W]
+    noise = float(rng.choice([0.0, 0.01, 0.03, 0.08]))
+    f = np.clip(base + noise * rng.standard_normal(base.shape), 0, 1).astype(np.float32)
+    delta = float(rng.choice([0.0, 0.02, 0.05, 0.1, 0.25]))
+    return f, delta
+
+
+@pytest.mark.parametrize("seed", range(60))
+def test_random_labels_bitexact(seed):
+    """Q(c; delta) on random fields: GPU labels, counts and palettes equal the oracle's bit for bit."""
+    f, delta = _label_field(seed)
+    B, H, W, C = f.shape
+    sp = dict(alpha=1.0, beta=1.0, radius=2, kernel=0, eps_x=0.0, eps_c=57.0, dt=0.25, rho=1.0, gamma=1.0,
+              kappa=1.0, tau=0.0, sigma=0.0, theta=1.0, iters_per_round=1, rounds=1)
+    with msa.Solver(gpu_params(f, sp), f) as s:  # c = I = f after init
+        glab, gcnt, gpal = s.labels(delta, max_k=16)
+    import oracle
+    for b in range(B):
+        olab, ocnt, opal = oracle.labels(f[b], delta, max_k=16)
+        assert gcnt[b] == ocnt, (seed, b, gcnt[b], ocnt)
+        assert np.array_equal(glab[b], olab), (seed, b)
+        k = min(ocnt, 16)
+        assert np.array_equal(gpal[b][:k], opal[:k]), (seed, b)
