@@ -66,3 +66,22 @@ def test_batch_shards_match_one_context():
     spec = dict(seed=11, shape=list(shape), worlds=[2, 3], shard="batch", params=_params(shape[2], R))
     rep = _run(spec)
     assert rep["worlds"]["3"]["images"] in ([2, 2, 1], [2, 1, 2], [1, 2, 2])
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_row_slabs_random(seed):
+    """Random slab worlds: shape, channels, radius (up to the slab height), world 2-4, scheme."""
+    import numpy as np
+    rng = np.random.default_rng(5000 + seed)
+    world = int(rng.integers(2, 5))
+    R = int(rng.choice([1, 2, 3, 4, 5, 9]))
+    C = int(rng.choice([1, 2, 3, 4, 16]))
+    if C == 16 and R > 8:
+        R = 4
+    H = int(rng.integers(max(R, 1) * world, 140))
+    W = int(rng.integers(8, 70))
+    B = int(rng.choice([1, 2]))
+    scheme = int(rng.random() < 0.3)
+    extra = {"scheme": scheme, "tau": 0.0} if scheme else {"kernel": int(rng.integers(0, 2))}
+    spec = dict(seed=seed, shape=[B, H, W, C], worlds=[world], params=_params(W, R, **extra))
+    assert _run(spec)["worlds"][str(world)]["fields"] == "bitwise"
