@@ -451,3 +451,29 @@ class Solver:
         _check(lib().msa_dal_gradient(self._ctx, ctypes.byref(d.c_struct()), e.ctypes.data, vp, mp, ctypes.byref(J),
                                       g.ctypes.data))
         return J.value, g
+
+
+def quantize(image, delta: float = 0.1, radius: int = 5, iters_per_round: int = 100, rounds: int = 10,
+             max_k: int = 64, scheme: int = SCHEME_CP_ROUNDS, **params):
+    """One call: evolve an image with the pixel multi-agent dynamics + TV control and label it by
+    Q(c; delta). image: float32 [H][W][C] or [B][H][W][C] in [0, 1], row 0 = bottom (numpy or torch).
+    Defaults are the BASELINE recipe in pixel units: alpha h = 8, rho/h = gamma/h =
+    2.5, beta = 1, dt = 0.25, eps_c = 57, Wendland kernel, eps_x by
+    reading R2; any msa_params field can be overridden by keyword (Omega units).
+    Returns (c [B][H][W][C] float32, labels [B][H][W] int32, n_clusters [B] int32,
+    palette [B][max_k][C] float32 or None)."""
+    shape = tuple(image.shape)
+    if len(shape) == 3:
+        image = image[None]
+    B, H, W, C = (int(v) for v in image.shape)
+    h = 1.0 / (W - 1) if W > 1 else 1.0
+    kw = dict(alpha=8.0 / h, beta=1.0, radius=radius, eps_c=57.0, dt=0.25, rho=2.5 * h, gamma=2.5 * h,
+              iters_per_round=iters_per_round, rounds=rounds, scheme=scheme)
+    kw.update(params)
+    with Solver(Params(batch=B, height=H, width=W, channels=C, **kw), image) as s:
+        s.solve()
+        c = s.get_field(FIELD_C)
+        lab, cnt, pal = s.labels(delta, max_k)
+    if len(shape) == 3:
+        return c[0], lab[0], cnt[:1], pal[:1] if pal is not None else None
+    return c, lab, cnt, pal
