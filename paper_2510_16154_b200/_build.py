@@ -32,11 +32,12 @@ def needs_build() -> bool:
     return any(os.path.getmtime(f) > t for f in _deps())
 
 
-def build(force: bool = False, verbose: bool = False, defines: tuple = (), lib: str = LIB, build_dir: str = BUILD) -> str:
+def build(force: bool = False, verbose: bool = False, defines: tuple = (), lib: str = LIB, build_dir: str = BUILD,
+          flags: tuple = ()) -> str:
     if not force and lib == LIB and not needs_build():
         return LIB
     os.makedirs(build_dir, exist_ok=True)
-    extra = (["-Xptxas", "-v"] if verbose else []) + [f"-D{d}" for d in defines]
+    extra = (["-Xptxas", "-v"] if verbose else []) + [f"-D{d}" for d in defines] + list(flags)
 
     def compile_one(src: str) -> str:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
