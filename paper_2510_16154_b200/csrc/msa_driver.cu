@@ -1243,7 +1243,7 @@ int msa_state_bytes(msa_ctx* x, size_t* bytes) {
 }
 
 int msa_get_state(msa_ctx* x, void* blob, size_t bytes) {
-  size_t need;
+  size_t need = 0;
   int rc = msa_state_bytes(x, &need);
   if (rc != MSA_OK) return rc;
   if (!blob || bytes < need) return set_err(MSA_EINVAL, "state buffer too small (%zu < %zu)", bytes, need);
@@ -1262,7 +1262,7 @@ int msa_get_state(msa_ctx* x, void* blob, size_t bytes) {
 }
 
 int msa_set_state(msa_ctx* x, const void* blob, size_t bytes) {
-  size_t need;
+  size_t need = 0;
   int rc = msa_state_bytes(x, &need);
   if (rc != MSA_OK) return rc;
   if (!blob || bytes < need) return set_err(MSA_EINVAL, "state buffer too small (%zu < %zu)", bytes, need);

@@ -113,7 +113,6 @@ __global__ void k_compress_flag(int32_t* P, int32_t* flag, int n) {
 
 // ---- exclusive scan of int32 (in place), 1024 elements per block
 __global__ void k_scan_block(int32_t* a, int n, int32_t* bsum) {
-  __shared__ int32_t s[1024];
   __shared__ int32_t wsum[32];
   const int base = blockIdx.x * 1024;
   const int t = threadIdx.x;  // 256 threads x 4
@@ -147,7 +146,6 @@ __global__ void k_scan_block(int32_t* a, int n, int32_t* bsum) {
     run += v[q];
   }
   if (t == 255 && bsum) bsum[blockIdx.x] = run;
-  (void)s;
 }
 __global__ void k_scan_add(int32_t* a, int n, const int32_t* off) {
   const int x = blockIdx.x * 1024 + threadIdx.x * 4;
