@@ -184,6 +184,15 @@ int msa_step(msa_ctx* ctx, int32_t n_iters);
  * issued directly. */
 int msa_solve(msa_ctx* ctx, msa_round_stats* stats);
 
+/* Alg. 2 with its "UNTIL stop criterion is verified": multiplier rounds of K
+ * iterations from the current state until a round's record has al_residual <= tol_residual or
+ * |gap| <= tol_gap (a tolerance <= 0 disables that test; the paper leaves the quantity open,
+ * reading R13), or max_rounds rounds have run. The rounds are exactly those msa_step
+ * would run (one host check per round); stats[0 .. *rounds_run) receive their records (stats may be
+ * NULL). *converged = 1 if a test passed. Synchronises; MSA_EDIVERGED as for msa_solve. (ABI 2) */
+int msa_solve_until(msa_ctx* ctx, double tol_residual, double tol_gap, int32_t max_rounds, msa_round_stats* stats,
+                    int32_t* rounds_run, int32_t* converged);
+
 /* Quantisation rule Q(c; delta) (reading R16) of the current c, per image:
  *  (i) union 4-neighbours whose fp32 colours differ by <= delta in every channel;
  *  (ii) union segments whose means differ by <= delta in every channel (means from exact

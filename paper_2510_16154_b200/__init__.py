@@ -26,7 +26,8 @@ SCHEME_CP_ROUNDS, SCHEME_LINEARISED_ADMM = 0, 1
 
 # every symbol include/msa.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["msa_abi_version", "msa_last_error", "msa_workspace_bytes", "msa_partition_rows",
-               "msa_nccl_unique_id", "msa_halo_plan", "msa_init", "msa_reset", "msa_step", "msa_solve", "msa_labels",
+               "msa_nccl_unique_id", "msa_halo_plan", "msa_init", "msa_reset", "msa_step", "msa_solve",
+               "msa_solve_until", "msa_labels",
                "msa_get_field", "msa_set_field", "msa_get_stats", "msa_state_bytes", "msa_get_state",
                "msa_set_state", "msa_query", "msa_set_timing", "msa_get_timing", "msa_dal", "msa_dal_gradient",
                "msa_sync", "msa_free"]
@@ -175,6 +176,7 @@ def lib():
             "msa_reset": ([P, V, ctypes.c_int], ctypes.c_int),
             "msa_step": ([P, I32], ctypes.c_int),
             "msa_solve": ([P, V], ctypes.c_int),
+            "msa_solve_until": ([P, ctypes.c_double, ctypes.c_double, I32, V, PI32, PI32], ctypes.c_int),
             "msa_labels": ([P, ctypes.c_float, V, V, V, I32, ctypes.c_int], ctypes.c_int),
             "msa_get_field": ([P, I32, V, ctypes.c_int, PI32, PI32], ctypes.c_int),
             "msa_set_field": ([P, I32, V, ctypes.c_int], ctypes.c_int),
@@ -335,6 +337,15 @@ class Solver:
         buf = (RoundStats * n)()
         _check(lib().msa_solve(self._ctx, buf))
         return [buf[r].as_dict(self.params.channels) for r in range(self.params.rounds)]
+
+    def solve_until(self, tol_residual: float = 0.0, tol_gap: float = 0.0, max_rounds: int = 100):
+        """Rounds until al_residual <= tol_residual or |gap| <= tol_gap (Alg. 2's stop criterion);
+        returns (records, converged)."""
+        buf = (RoundStats * max(max_rounds, 1))()
+        n, conv = ctypes.c_int32(0), ctypes.c_int32(0)
+        _check(lib().msa_solve_until(self._ctx, float(tol_residual), float(tol_gap), int(max_rounds), buf,
+                                     ctypes.byref(n), ctypes.byref(conv)))
+        return [buf[r].as_dict(self.params.channels) for r in range(n.value)], bool(conv.value)
 
     def labels(self, delta: float = 0.1, max_k: int = 0, out=None):
         """Returns (labels int32 [nb][rows][W], n_clusters int32 [nb], palette [nb][max_k][C] or None);

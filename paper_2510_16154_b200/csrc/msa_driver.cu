@@ -998,6 +998,35 @@ int msa_solve(msa_ctx* x, msa_round_stats* stats) {
   return MSA_OK;
 }
 
+int msa_solve_until(msa_ctx* x, double tol_residual, double tol_gap, int32_t max_rounds, msa_round_stats* stats,
+                    int32_t* rounds_run, int32_t* converged) {
+  if (!x || !rounds_run || !converged) return set_err(MSA_EINVAL, "NULL argument");
+  if (max_rounds < 0) return set_err(MSA_EINVAL, "max_rounds must be >= 0");
+  if (!(tol_residual == tol_residual) || !(tol_gap == tol_gap)) return set_err(MSA_EINVAL, "NaN tolerance");
+  *rounds_run = 0;
+  *converged = 0;
+  const int K = x->prm.iters_per_round;
+  for (int32_t r = 0; r < max_rounds; ++r) {
+    // the rest of the current round (a full round from a round boundary), then its record
+    const int64_t n = K - x->iters_done % K;
+    int rc;
+    const size_t before = x->stats.size() + x->rec_pending;
+    if ((rc = do_steps(x, n)) != MSA_OK) return rc;
+    if ((rc = fetch_records(x)) != MSA_OK) return rc;
+    CUDA_TRY(cudaStreamSynchronize(x->stream));
+    if (x->stats.size() <= before) return set_err(MSA_ESTATE, "no round record after a round");
+    const msa_round_stats& s = x->stats.back();
+    if (stats) stats[r] = s;
+    *rounds_run = r + 1;
+    if (s.nonfinite > 0) return set_err(MSA_EDIVERGED, "integration diverged: non-finite colour at round %d", s.round);
+    if ((tol_residual > 0 && s.al_residual <= tol_residual) || (tol_gap > 0 && fabs(s.gap) <= tol_gap)) {
+      *converged = 1;
+      break;
+    }
+  }
+  return MSA_OK;
+}
+
 // Q(c; delta) of image b over row parts: stage (i) per part, the parts' segment
 // tables concatenated in row order, one merge (identical on every rank), relabel of own pixels.
 //  * rows mode, world > 1: the part is this rank's slab; tables meet by ncclAllGather (padded to

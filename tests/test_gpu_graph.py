@@ -49,3 +49,34 @@ def test_graph_replay_bitwise(shape, R, scheme, K, rounds, kappa, tmp_path):
     rec = a["records"]
     assert rec.shape[0] == 6 * rounds
     assert np.all(rec[:rounds, 0] == np.arange(rounds))
+
+
+def test_solve_until_stop_criterion():
+    """msa_solve_until (Alg. 2's UNTIL): stops at the first round whose AL residual is <= tol; the
+    state equals the same number of rounds run with msa_step, bit for bit, and the earlier
+    rounds' residuals are above tol."""
+    import numpy as np
+    rng = np.random.default_rng(4)
+    H, W, C = 40, 48, 3
+    I = np.clip(np.repeat(np.repeat(rng.random((4, 4, C)), 10, 0), 12, 1) + 0.05 * rng.standard_normal((H, W, C)),
+                0, 1).astype(np.float32)[None]
+    h = 1.0 / (W - 1)
+    p = msa.Params(batch=1, height=H, width=W, channels=C, alpha=8.0 / h, beta=1.0, radius=3, eps_c=57.0,
+                   dt=0.25, rho=2.5 * h, gamma=2.5 * h, iters_per_round=10, rounds=1)
+    with msa.Solver(p, I) as s:
+        full, conv0 = s.solve_until(0.0, 0.0, 12)  # no test: exactly 12 rounds
+        assert not conv0 and len(full) == 12
+    res = [r["al_residual"] for r in full]
+    tol = 0.5 * (res[3] + res[4]) if res[4] < res[3] else res[4]  # between rounds 3 and 4
+    with msa.Solver(p, I) as s:
+        recs, conv = s.solve_until(tol, 0.0, 12)
+        c_until = s.get_field(msa.FIELD_C)
+    n = len(recs)
+    assert conv and recs[-1]["al_residual"] <= tol and all(r["al_residual"] > tol for r in recs[:-1])
+    with msa.Solver(p, I) as s:
+        s.step(n * 10)
+        s.sync()
+        c_step = s.get_field(msa.FIELD_C)
+        st = s.stats()
+    assert np.array_equal(c_until, c_step)
+    assert [r["al_residual"] for r in st] == [r["al_residual"] for r in recs]
