@@ -267,6 +267,14 @@ typedef struct {
 } msa_dal_params;
 int msa_dal(msa_ctx* ctx, const msa_dal_params* d, double* eps, const float* v, const float* mu, double* J_hist,
             double* sigma_hist);
+/* Algorithm 2 with Algorithm 1 as its line 5: `outer` times, DAL (d, cost must
+ * be 1) at (v^(j-1), mu^(j)) -> eps, c = c(T; eps); then v^(j) = S_{beta/rho}(grad c - mu^(j)/rho) and
+ * mu^(j+1) = mu^(j) + gamma (v^(j) - grad c) on the device, with a round record of c^(j) in
+ * stats[j] (dual and gap refer to p = 0). v, mu: host [H][W][2C] initial values or NULL (0).
+ * J_hist: [outer][iters + 1] or NULL. eps is updated in place; the final mu is MSA_FIELD_MU.
+ * Synchronises. (ABI 2) */
+int msa_dal_admm(msa_ctx* ctx, const msa_dal_params* d, double* eps, const float* v, const float* mu,
+                 int32_t outer, double* J_hist, msa_round_stats* stats);
 /* J(eps) and its gradient dJ/deps ([steps][2], host) without optimising (may be NULL). */
 int msa_dal_gradient(msa_ctx* ctx, const msa_dal_params* d, const double* eps, const float* v, const float* mu,
                      double* J, double* grad);

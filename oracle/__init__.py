@@ -15,7 +15,7 @@ from __future__ import annotations
 import ctypes
 import os
 import subprocess
-from dataclasses import dataclass, asdict
+from dataclasses import replace, dataclass, asdict
 
 import numpy as np
 
@@ -342,6 +342,29 @@ def dal_cost(p: Params, d: DalParams, eps, I, v=None, mu=None, return_state: boo
     J = _load().mo_dal_cost(ctypes.byref(p.c()), ctypes.byref(d.c_struct()), _ptr(eps), _ptr(I), _ptr(v), _ptr(mu),
                             _ptr(cT))
     return (J, cT) if return_state else J
+
+
+def dal_admm(p: Params, d: DalParams, eps, I, outer: int, v=None, mu=None):
+    """Algorithm 2 with Algorithm 1 as its line 5, step by step: for j = 0 ..
+    outer-1: eps^(j) by dal() with the augmented-Lagrangian terminal at (v^(j-1), mu^(j)) (d.cost = 1),
+    c^(j) = c(T; eps^(j)) by dal_cost(); v^(j) = S_{beta/rho}(grad c^(j) - mu^(j)/rho) (line 6,
+    eq:soft_threshold); mu^(j+1) = mu^(j) + gamma (v^(j) - grad c^(j)) (line 7). v^(-1), mu^(0): the
+    arguments or 0. Returns (eps, J_hist [outer][iters+1], c^(outer-1), v, mu)."""
+    q = derive(p)
+    d = replace(d, rho=q.rho)  # one penalty: the AL terminal of line 5 and the updates of lines 6-7
+    eps = _f64(eps).copy()
+    I = _f64(I)
+    H, W, C = I.shape
+    v = np.zeros((H, W, 2 * C)) if v is None else _f64(v).copy()
+    mu = np.zeros((H, W, 2 * C)) if mu is None else _f64(mu).copy()
+    Jh, c = [], I.copy()
+    for _ in range(outer):
+        eps, J, _ = dal(p, d, eps, I, v, mu)
+        Jh.append(J)
+        _, c = dal_cost(p, d, eps, I, v, mu, return_state=True)
+        v = shrink_field(p, q.rho, c, mu)
+        mu = mu + q.gamma * (v - grad(c, q.hx, q.hy))
+    return eps, np.array(Jh), c, v, mu
 
 
 def dal_gradient(p: Params, d: DalParams, eps, I, v=None, mu=None):

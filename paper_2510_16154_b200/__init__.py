@@ -29,7 +29,7 @@ ABI_SYMBOLS = ["msa_abi_version", "msa_last_error", "msa_workspace_bytes", "msa_
                "msa_nccl_unique_id", "msa_halo_plan", "msa_init", "msa_reset", "msa_step", "msa_solve",
                "msa_solve_until", "msa_labels",
                "msa_get_field", "msa_set_field", "msa_get_stats", "msa_state_bytes", "msa_get_state",
-               "msa_set_state", "msa_query", "msa_set_timing", "msa_get_timing", "msa_dal", "msa_dal_gradient",
+               "msa_set_state", "msa_query", "msa_set_timing", "msa_get_timing", "msa_dal", "msa_dal_gradient", "msa_dal_admm",
                "msa_sync", "msa_free"]
 
 
@@ -190,6 +190,7 @@ def lib():
             "msa_sync": ([P], ctypes.c_int),
             "msa_dal": ([P, ctypes.POINTER(_DalParams), P, P, P, P, P], ctypes.c_int),
             "msa_dal_gradient": ([P, ctypes.POINTER(_DalParams), P, P, P, P, P], ctypes.c_int),
+            "msa_dal_admm": ([P, ctypes.POINTER(_DalParams), P, P, P, I32, P, P], ctypes.c_int),
             "msa_free": ([P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
@@ -430,17 +431,19 @@ class Solver:
         _check(lib().msa_sync(self._ctx))
 
     # -- NEXT-1: DAL control optimisation (Algorithm 1)
-    @staticmethod
-    def _vmu(v, mu):
+    def _vmu(self, v, mu):
         keep = []
         out = []
-        for a in (v, mu):
+        n = self.params.height * self.params.width * 2 * self.params.channels
+        for a, what in ((v, "v"), (mu, "mu")):
             if a is None:
                 out.append(None)
             else:
-                a = np.ascontiguousarray(a, dtype=np.float32)
-                keep.append(a)
-                out.append(a.ctypes.data)
+                ptr, on_dev, k = _ptr_of(a, n, what)
+                if on_dev:
+                    raise TypeError(f"{what}: host array expected")
+                keep.append(k)
+                out.append(ptr)
         return out, keep
 
     def dal(self, d: "DalParams", eps, v=None, mu=None):
@@ -453,6 +456,18 @@ class Solver:
         _check(lib().msa_dal(self._ctx, ctypes.byref(d.c_struct()), e.ctypes.data, vp, mp, Jh.ctypes.data,
                              sh.ctypes.data))
         return e, Jh, sh[:d.iters]
+
+    def dal_admm(self, d: "DalParams", eps, outer: int, v=None, mu=None):
+        """Algorithm 2 with DAL as line 5 (d.cost must be 1): returns (eps, J_hist [outer][iters+1],
+        records [outer]); the final mu is FIELD_MU."""
+        e = np.ascontiguousarray(eps, dtype=np.float64).copy()
+        assert e.shape == (d.steps, 2)
+        Jh = np.zeros((max(outer, 1), d.iters + 1))
+        buf = (RoundStats * max(outer, 1))()
+        (vp, mp), keep = self._vmu(v, mu)
+        _check(lib().msa_dal_admm(self._ctx, ctypes.byref(d.c_struct()), e.ctypes.data, vp, mp, int(outer),
+                                  Jh.ctypes.data, buf))
+        return e, Jh[:outer], [buf[r].as_dict(self.params.channels) for r in range(outer)]
 
     def dal_gradient(self, d: "DalParams", eps, v=None, mu=None):
         e = np.ascontiguousarray(eps, dtype=np.float64)

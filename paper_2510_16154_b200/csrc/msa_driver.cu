@@ -1537,31 +1537,11 @@ void dal_project(const msa_dal_params* d, double* e) {
     e[2 * m + 1] = std::min(std::max(e[2 * m + 1], d->ec_lo), d->ec_hi);
   }
 }
-}  // namespace
 
-int msa_dal_gradient(msa_ctx* x, const msa_dal_params* d, const double* eps, const float* v, const float* mu,
-                     double* J, double* grad) {
-  int rc = dal_check(x, d);
-  if (rc != MSA_OK) return rc;
-  if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
-  DalBuffers B;
-  if ((rc = dal_alloc(x, d, v, mu, B, true)) != MSA_OK) return rc;
-  std::vector<double> g(2 * (size_t)d->steps);
-  double Jv = 0.0;
-  if ((rc = dal_grad(x, d, eps, B, &Jv, g.data())) != MSA_OK) return rc;
-  if (J) *J = Jv;
-  if (grad) std::copy(g.begin(), g.end(), grad);
-  return MSA_OK;
-}
-
-int msa_dal(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, const float* mu, double* J_hist,
-            double* sigma_hist) {
-  int rc = dal_check(x, d);
-  if (rc != MSA_OK) return rc;
-  if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
-  DalBuffers B, Bc;
-  if ((rc = dal_alloc(x, d, v, mu, B, true)) != MSA_OK) return rc;
-  if ((rc = dal_alloc(x, d, v, mu, Bc, false)) != MSA_OK) return rc;
+// Algorithm 1 on allocated buffers (B: gradient sweeps, Bc: cost sweeps); leaves c = cbar = c(T; eps)
+int dal_iterate(msa_ctx* x, const msa_dal_params* d, double* eps, DalBuffers& B, DalBuffers& Bc, double* J_hist,
+                double* sigma_hist) {
+  int rc;
   const int M2 = 2 * d->steps;
   std::vector<double> D(M2), cand(M2);
   dal_project(d, eps);
@@ -1623,6 +1603,100 @@ int msa_dal(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, co
   CUDA_TRY(cudaMemcpyAsync(x->c[x->cur], cT, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
   CUDA_TRY(cudaMemcpyAsync(x->cb[x->cur], cT, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
   CUDA_TRY(cudaStreamSynchronize(x->stream));
+  return MSA_OK;
+}
+}  // namespace
+
+int msa_dal_gradient(msa_ctx* x, const msa_dal_params* d, const double* eps, const float* v, const float* mu,
+                     double* J, double* grad) {
+  int rc = dal_check(x, d);
+  if (rc != MSA_OK) return rc;
+  if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
+  DalBuffers B;
+  if ((rc = dal_alloc(x, d, v, mu, B, true)) != MSA_OK) return rc;
+  std::vector<double> g(2 * (size_t)d->steps);
+  double Jv = 0.0;
+  if ((rc = dal_grad(x, d, eps, B, &Jv, g.data())) != MSA_OK) return rc;
+  if (J) *J = Jv;
+  if (grad) std::copy(g.begin(), g.end(), grad);
+  return MSA_OK;
+}
+
+int msa_dal(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, const float* mu, double* J_hist,
+            double* sigma_hist) {
+  int rc = dal_check(x, d);
+  if (rc != MSA_OK) return rc;
+  if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
+  DalBuffers B, Bc;
+  if ((rc = dal_alloc(x, d, v, mu, B, true)) != MSA_OK) return rc;
+  if ((rc = dal_alloc(x, d, v, mu, Bc, false)) != MSA_OK) return rc;
+  return dal_iterate(x, d, eps, B, Bc, J_hist, sigma_hist);
+}
+
+// Algorithm 2 with Algorithm 1 as its line 5 (SURVEY §8(f) NEXT-1 "Alg. 2 line 5
+// made literal"): for j = 0 .. outer-1: DAL with the cost-1 terminal at (v^(j-1), mu^(j)) -> eps^(j),
+// c^(j) = c(T; eps^(j)); then v^(j) = S_{beta/rho}(grad c^(j) - mu^(j)/rho) and
+// mu^(j+1) = mu^(j) + gamma (v^(j) - grad c^(j)) by the round kernel, whose record (E_TV, E_fid, P,
+// AL residual of c^(j)) goes to stats[j]. v^(-1), mu^(0) from the arguments (NULL = 0); the final
+// mu is left in the context (MSA_FIELD_MU). rho is fixed (kappa is not applied).
+int msa_dal_admm(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, const float* mu, int32_t outer,
+                 double* J_hist, msa_round_stats* stats) {
+  int rc = dal_check(x, d);
+  if (rc != MSA_OK) return rc;
+  if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
+  if (d->cost != 1) return set_err(MSA_EINVAL, "msa_dal_admm needs the augmented-Lagrangian cost (cost = 1)");
+  if (outer < 0) return set_err(MSA_EINVAL, "outer must be >= 0");
+  DalBuffers B, Bc;
+  if ((rc = dal_alloc(x, d, v, mu, B, true)) != MSA_OK) return rc;
+  if ((rc = dal_alloc(x, d, v, mu, Bc, false)) != MSA_OK) return rc;
+  const size_t pf2 = 2 * plane_floats(x);
+  const size_t before = x->stats.size() + x->rec_pending;  // this call's records start here
+  // mu^(0) into the context's mu field (the round kernel updates it in place)
+  CUDA_TRY(cudaMemcpyAsync(x->mu, B.mu, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+  const msa_params& P = x->prm;
+  for (int32_t j = 0; j < outer; ++j) {
+    if ((rc = dal_iterate(x, d, eps, B, Bc, J_hist ? J_hist + (size_t)j * (d->iters + 1) : nullptr, nullptr)) !=
+        MSA_OK)
+      return rc;
+    // line 6-7 on c^(j) (now in c[cur]): v^(j) -> B.v, mu^(j+1) -> mu, and the round record
+    const int s = x->cur;
+    CUDA_TRY(cudaMemsetAsync(x->p[s], 0, sizeof(float) * pf2, x->stream));  // no CP dual here: D is of p = 0
+    MsaRoundConsts R;
+    R.inv_hx = (float)(1.0 / x->hx);
+    R.inv_hy = (float)(1.0 / x->hy);
+    R.inv_rho = (float)(1.0 / x->rho_cur);
+    R.thr = (float)(P.beta / x->rho_cur);
+    R.gamma = (float)P.gamma;
+    R.rho = x->rho_cur;
+    R.beta = P.beta;
+    R.alpha = P.alpha;
+    int nblk = 0;
+    CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->mu, x->I, x->mu, x->partials, &nblk, x->stream, B.v));
+    CUDA_TRY(msa_launch_reduce(x->partials, x->g.nb, nblk, x->sums, x->stream));
+    MsaRecordArgs a;
+    a.w = x->hx * x->hy;
+    a.beta = P.beta;
+    a.alpha = P.alpha;
+    a.rho = x->rho_cur;
+    a.npx = (double)x->g.nrows * P.width * x->g.nb;
+    a.C = P.channels;
+    a.round = x->rounds_done;
+    a.images = x->g.nb;
+    a.iters = x->iters_done;
+    a.lin = 0;
+    if (x->rec_pending >= REC_CAP && (rc = fetch_records(x)) != MSA_OK) return rc;
+    CUDA_TRY(msa_launch_record(x->sums, a, x->d_rec + x->rec_pending, x->stream));
+    x->launches += 3;
+    ++x->rec_pending;
+    ++x->rounds_done;
+    // the next DAL sees v^(j), mu^(j+1)
+    CUDA_TRY(cudaMemcpyAsync(B.mu, x->mu, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+    CUDA_TRY(cudaMemcpyAsync(Bc.mu, x->mu, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+    CUDA_TRY(cudaMemcpyAsync(Bc.v, B.v, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+  }
+  if ((rc = fetch_records(x)) != MSA_OK) return rc;
+  CUDA_TRY(cudaStreamSynchronize(x->stream));
+  for (size_t r = before; stats && r < x->stats.size(); ++r) stats[r - before] = x->stats[r];
   return MSA_OK;
 }
 

@@ -67,10 +67,11 @@ cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const M
                                float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched);
 
 // Round update (steps 4-5): writes mu_out (may alias mu) and per-block fp64 partial sums
-// [nb][nblk][MSA_NSUM]; *nblk receives the number of blocks per image.
+// [nb][nblk][MSA_NSUM]; *nblk receives the number of blocks per image. v_out (may be null):
+// v = S_{beta/rho}(grad c - mu/rho) as a field (Alg. 2 line 6, for the DAL-inside-ADMM loop).
 cudaError_t msa_launch_round(const MsaGeom& g, const MsaRoundConsts& R, const float* c, const float* p,
                              const float* mu, const float* I, float* mu_out, double* partials, int* nblk,
-                             cudaStream_t s);
+                             cudaStream_t s, float* v_out = nullptr);
 int msa_round_blocks(const MsaGeom& g);
 // Deterministic sum of the partials over blocks and over images -> sums[MSA_NSUM].
 cudaError_t msa_launch_reduce(const double* partials, int nb, int nblk, double* sums, cudaStream_t s);

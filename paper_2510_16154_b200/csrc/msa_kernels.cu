@@ -234,7 +234,7 @@ template <int C>
 __global__ void __launch_bounds__(256) k_round(MsaGeom g, MsaRoundConsts R, const float* __restrict__ c,
                                                const float* __restrict__ p, const float* mu,
                                                const float* __restrict__ I, float* mu_out,
-                                               double* __restrict__ partials) {
+                                               double* __restrict__ partials, float* __restrict__ v_out) {
   constexpr int NS = MSA_S_MEAN0 + C;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int b = blockIdx.z;
@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(256) k_round(MsaGeom g, MsaRoundConsts R, cons
       const float vg = __fsub_rn(v, gv[m]);
       res += (double)vg * (double)vg;
       if (mu_out) mu_out[msa_idx(g, b, m, 2 * C, j, i)] = __fmaf_rn(R.gamma, vg, mv[m]);  // null: stats only
+      if (v_out) v_out[msa_idx(g, b, m, 2 * C, j, i)] = v;
     }
     acc[MSA_S_RES] += res;
     acc[MSA_S_TV] += sqrt((double)g2);
@@ -416,13 +417,13 @@ int msa_round_blocks(const MsaGeom& g) { return ((g.W + 31) / 32) * ((g.nrows + 
 
 cudaError_t msa_launch_round(const MsaGeom& g, const MsaRoundConsts& R, const float* c, const float* p,
                              const float* mu, const float* I, float* mu_out, double* partials, int* nblk,
-                             cudaStream_t s) {
+                             cudaStream_t s, float* v_out) {
   dim3 blk(32, 8), grd((g.W + 31) / 32, (g.nrows + 8 * MSA_ROUND_RPT - 1) / (8 * MSA_ROUND_RPT), g.nb);
   *nblk = (int)(grd.x * grd.y);
   switch (g.C) {
 #define MSA_CASE(CC) \
   case CC:           \
-    k_round<CC><<<grd, blk, 0, s>>>(g, R, c, p, mu, I, mu_out, partials); \
+    k_round<CC><<<grd, blk, 0, s>>>(g, R, c, p, mu, I, mu_out, partials, v_out); \
     break;
     MSA_CASE(1) MSA_CASE(2) MSA_CASE(3) MSA_CASE(4) MSA_CASE(5) MSA_CASE(6) MSA_CASE(7) MSA_CASE(8)
     MSA_CASE(9) MSA_CASE(10) MSA_CASE(11) MSA_CASE(12) MSA_CASE(13) MSA_CASE(14) MSA_CASE(15) MSA_CASE(16)

@@ -161,3 +161,23 @@ np.savez(sys.argv[2], J=np.array([J]), g=g)
         outs.append(np.load(out))
     assert np.array_equal(outs[0]["J"], outs[1]["J"])
     assert np.array_equal(outs[0]["g"], outs[1]["g"])
+
+
+@pytest.mark.parametrize("R,C", [(12, 1), (15, 3)])
+def test_dal_admm_matches_oracle(R, C):
+    """Algorithm 2 with DAL as line 5 (msa_dal_admm) against oracle.dal_admm: the same accepted DAL
+    steps and costs per outer iteration, the optimised controls, and the final multiplier."""
+    rng, I, sp, eps = _case(H=16, W=16, C=C, R=R, M=6, seed=R + C)
+    sp = dict(sp, rho=0.4, gamma=0.4)
+    H, W, _ = I.shape
+    kw = dict(iters=3, max_ls=20, sigma0=1e3, b=0.5, c=1e-4, ex_lo=2.0, ex_hi=1100.0, ec_lo=2.0, ec_hi=1100.0)
+    outer = 3
+    with msa.Solver(msa.Params.from_solver(1, H, W, C, sp), I[None]) as s:
+        e, Jh, recs = s.dal_admm(msa.DalParams(steps=6, cost=1, **kw), eps, outer)
+        mu = s.get_field(msa.FIELD_MU)[0]
+    eo, Jho, co, vo, muo = oracle.dal_admm(_oracle_params(I, sp), oracle.DalParams(M=6, cost=1, **kw), eps,
+                                           I.astype(np.float64), outer)
+    assert len(recs) == outer
+    np.testing.assert_allclose(Jh, Jho, rtol=1e-4)
+    np.testing.assert_allclose(e, eo, rtol=2e-3, atol=1e-6)
+    np.testing.assert_allclose(mu, muo, rtol=0, atol=2e-4 * max(1.0, float(np.max(np.abs(muo)))))

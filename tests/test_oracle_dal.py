@@ -95,3 +95,30 @@ def test_D5_armijo_descent_and_projection():
             assert oracle.dal_cost(p, d, cand, I) <= J0 - d.c * sh[it] * np.sum(D * D) + 1e-15
             e = cand
     assert np.allclose(e, eps1, rtol=0, atol=1e-12)
+
+
+def test_dal_admm_multiplier_wiring():
+    """Algorithm 2 around DAL (oracle.dal_admm): with gamma = rho the multiplier step
+    mu + rho (S_{beta/rho}(grad c - mu/rho) - grad c) equals the projection of mu - rho grad c onto
+    the beta-ball per pixel (the Moreau identity, written here as the textbook projection), so after
+    one outer iteration from mu = 0, mu = Pi_beta(-rho grad c(T)); and v is the shrink at that c."""
+    rng = np.random.default_rng(2)
+    H, W, C = 9, 11, 2
+    I = rng.random((H, W, C))
+    h = 1.0 / (W - 1)
+    p = oracle.Params(height=H, width=W, channels=C, radius=9, alpha=0.8 / h, beta=0.7, eps_c=57.0, dt=0.25,
+                      rho=0.4, gamma=0.4, iters_per_round=1, rounds=1)
+    d = oracle.DalParams(M=5, cost=1, iters=2, sigma0=1e3, ex_lo=8.0)
+    eps = np.stack([np.full(5, 40.0), np.full(5, 57.0)], 1)
+    e, Jh, c, v, mu = oracle.dal_admm(p, d, eps, I, 1)
+    q = oracle.derive(p)
+    # independent gradient (forward differences, zero on the last column / row)
+    g = np.zeros((H, W, 2 * C))
+    g[:, :-1, :C] = (c[:, 1:] - c[:, :-1]) / q.hx
+    g[:-1, :, C:] = (c[1:] - c[:-1]) / q.hy
+    a = -q.rho * g
+    n = np.linalg.norm(a, axis=-1, keepdims=True)
+    proj = a * np.minimum(1.0, q.beta / np.maximum(n, 1e-300))
+    np.testing.assert_allclose(mu, proj, rtol=1e-12, atol=1e-13)
+    assert np.all(np.linalg.norm(mu, axis=-1) <= q.beta * (1 + 1e-12))
+    assert np.all(np.diff(Jh[0]) <= 1e-12 * abs(Jh[0][0]))  # Armijo inside
