@@ -77,7 +77,7 @@ typedef struct {
   int32_t batch, height, width, channels; /* B >= 1, H, W >= 1, 1 <= C <= 16 */
   double alpha;       /* fidelity weight alpha >= 0 (eq:cost_TV; alpha = 0 allowed: D, gap = NaN) */
   double beta;        /* TV weight beta >= 0 (1 in eq:cost_TV; reading R27) */
-  int32_t radius;     /* window radius R in pixels, 0 <= R <= 64 (reading R2; R > 8: NEXT-3 large supports) */
+  int32_t radius;     /* window radius R in pixels, 0 <= R <= 255 (reading R2; R > 8: NEXT-3 large supports) */
   int32_t kernel;     /* MSA_KERNEL_WENDLAND (4r+1)(1-r)^4 or MSA_KERNEL_PRINTED (4r-1)(1-r)^4 (R3) */
   double eps_x;       /* eq:ellipsoid spatial control; <= 0 -> 2/(R min(h_x,h_y))^2 (R2) */
   double eps_c;       /* eq:ellipsoid colour control >= 0 (57 in PAPER.md:270) */

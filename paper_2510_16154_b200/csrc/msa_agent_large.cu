@@ -20,7 +20,16 @@
 namespace {
 
 constexpr int TW = 32, TH = 8, NT = TW * TH;
-constexpr int CR = 16;  // neighbour rows per chunk
+constexpr int CR_MAX = 16;  // neighbour rows per chunk (fewer for very large windows: cr_for)
+
+// chunk rows so that nf4 staged float4 rows of SWL columns plus the offset table of CR + th - 1
+// rows fit in `budget` bytes of shared memory
+inline int cr_for(int R, int tw, int th, int nf4, size_t budget) {
+  const size_t swl = (size_t)tw + 2 * R, ow = 2 * (size_t)R + 1;
+  for (int cr = CR_MAX; cr > 1; --cr)
+    if (16 * nf4 * cr * swl + 4 * (cr + th - 1) * ow <= budget) return cr;
+  return 1;
+}
 
 // omtab == null (DAL, a control per step): 1 - a_delta = 1 - (exh_x dx^2 + exh_y dy^2) formed here,
 // exh = eps_x/2 h^2, exactly as the generic DAL step forms it (so the two agree bitwise).
@@ -30,11 +39,15 @@ constexpr int CR = 16;  // neighbour rows per chunk
 // NS > 1: the window's row chunks are dealt round-robin to NS CTAs per tile (blockIdx.z = part *
 // nb + image), each writing its partial sum to part_out[part]; k_large_combine adds the parts in
 // part order (small images: more warps in flight; a different summation order than NS = 1).
-template <int C, int KER, bool SC, int TH2>
+// CRC: the chunk height as a compile-time constant (CR_MAX, every window up to R ~ 100), or 0 for
+// the runtime value cr (larger windows need shorter chunks to fit the shared memory)
+template <int C, int KER, bool SC, int TH2, int CRC>
 __global__ void __launch_bounds__(32 * TH2) k_agent_large(MsaGeom g, MsaIterConsts K, int R, const float* __restrict__ omtab,
                                                     float exh_x, float exh_y, const float* __restrict__ c,
-                                                    float* __restrict__ chalf, int NS, float* __restrict__ part_out) {
+                                                    float* __restrict__ chalf, int NS, float* __restrict__ part_out,
+                                                    int cr) {
   extern __shared__ __align__(16) float smem[];
+  const int CR = CRC ? CRC : cr;
   const int SWL = TW + 2 * R;                  // staged columns x0-R .. x0+31+R
   float4* snb = reinterpret_cast<float4*>(smem);  // [CR][SWL]
   float* som = smem + 4 * CR * SWL;            // [CR + TH - 1][2R+1]: 1 - a_delta for dy = yr - y
@@ -146,20 +159,27 @@ cudaError_t go(F* kern, int th, int nr, size_t smem, const MsaGeom& g, const Msa
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
   if (e != cudaSuccess) return e;
   dim3 grd((g.W + TW - 1) / TW, (nr + th - 1) / th, g.nb * sp.NS);
-  kern<<<grd, 32 * th, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch, sp.NS, sp.part);
+  kern<<<grd, 32 * th, smem, s>>>(g, K, R, omtab, exh_x, exh_y, c, ch, sp.NS, sp.part, cr_for(R, TW, th, 1, 96 * 1024));
   return cudaGetLastError();
+}
+
+template <int C, int TH2, int CRC>
+cudaError_t launch_crc(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab, float exh_x, float exh_y,
+                       const float* c, float* ch, cudaStream_t s, int nr, Split sp, size_t smem, bool sc) {
+  if (K.kernel == 0 && sc) return go(k_agent_large<C, 0, true, TH2, CRC>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
+  if (K.kernel == 0) return go(k_agent_large<C, 0, false, TH2, CRC>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
+  if (sc) return go(k_agent_large<C, 1, true, TH2, CRC>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
+  return go(k_agent_large<C, 1, false, TH2, CRC>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
 }
 
 template <int C, int TH2>
 cudaError_t launch_th(const MsaGeom& g, const MsaIterConsts& K, int R, const float* omtab, float exh_x, float exh_y,
                       const float* c, float* ch, cudaStream_t s, int nr, Split sp) {
+  const int CR = cr_for(R, TW, TH2, 1, 96 * 1024);
   const size_t smem = sizeof(float) * (4 * CR * (TW + 2 * R) + (CR + TH2 - 1) * (2 * R + 1));
   const bool sc = K.scaled && omtab;
-  cudaError_t e;
-  if (K.kernel == 0 && sc) e = go(k_agent_large<C, 0, true, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
-  else if (K.kernel == 0) e = go(k_agent_large<C, 0, false, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
-  else if (sc) e = go(k_agent_large<C, 1, true, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
-  else e = go(k_agent_large<C, 1, false, TH2>, TH2, nr, smem, g, K, R, omtab, exh_x, exh_y, c, ch, s, sp);
+  cudaError_t e = CR == CR_MAX ? launch_crc<C, TH2, CR_MAX>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr, sp, smem, sc)
+                               : launch_crc<C, TH2, 0>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr, sp, smem, sc);
   if (e != cudaSuccess || sp.NS == 1) return e;
   k_large_combine<C><<<dim3((g.W + 127) / 128, nr, g.nb), 128, 0, s>>>(g, sc ? K.dt_s : K.dt_NR, sp.NS, sp.part, c, ch);
   return cudaGetLastError();
@@ -181,6 +201,7 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const floa
   const long long tiles2 = (long long)((g.W + TW - 1) / TW) * ((nr + 1) / 2) * g.nb;
   const size_t per_part = (size_t)g.nb * C * g.plane;
   int NS = (int)std::min<long long>(4, (8LL * sms + tiles2 - 1) / tiles2);
+  const int CR = cr_for(R, TW, 2, 1, 96 * 1024);
   NS = std::min(NS, (2 * R + 2 + CR - 1) / CR);
   NS = std::min<long long>(NS, per_part ? (long long)(scratch_floats / per_part) : 0);
   if (nosplit || !scratch || NS < 2) NS = 1;
@@ -213,12 +234,13 @@ namespace {
 // TH2 = 8, NS = 1: writes lam_out and the block partials itself. Otherwise (small images: 32 x 2
 // tiles, the window's row chunks dealt to NS CTAs, blockIdx.z = part) it writes per-pixel partial
 // sums (C adjoint components, the two eps sums) to part_out[part] and k_dal_back_combine finishes.
-template <int C, int TH2>
+template <int C, int TH2, int CRC>
 __global__ void __launch_bounds__(32 * TH2) k_dal_back_large(MsaGeom g, int R, int ker, float exh_x, float exh_y,
                                                        float e_c, float eps_c, float inv_NR, float dt,
                                                        const float* __restrict__ c, const float* __restrict__ lam,
                                                        float* __restrict__ lam_out, double* __restrict__ partials,
-                                                       int NS, float* __restrict__ part_out) {
+                                                       int NS, float* __restrict__ part_out, int cr) {
+  const int CR = CRC ? CRC : cr;
   constexpr int TH = TH2, NT = 32 * TH2;
   const int part = blockIdx.z;
   extern __shared__ __align__(16) float smem[];
@@ -389,26 +411,29 @@ cudaError_t dal_back_c(const MsaGeom& g, int R, int kernel, float exh_x, float e
   const long long tiles8 = (long long)nx * ((g.H + TH - 1) / TH);
   const size_t per_part = (size_t)(C + 2) * g.plane;
   if (tiles8 >= 2LL * sms || !scratch || scratch_floats < per_part) {
+    const int CR = cr_for(R, TW, TH, 2, 160 * 1024);
     const size_t smem = sizeof(float) * (8 * CR * (TW + 2 * R) + (CR + TH - 1) * (2 * R + 1));
-    cudaError_t e = cudaFuncSetAttribute(k_dal_back_large<C, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    auto kern = CR == CR_MAX ? k_dal_back_large<C, 8, CR_MAX> : k_dal_back_large<C, 8, 0>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
     if (e != cudaSuccess) return e;
-    k_dal_back_large<C, 8><<<dim3(nx, (g.H + TH - 1) / TH), NT, smem, s>>>(g, R, kernel, exh_x, exh_y, e_c, eps_c,
-                                                                          inv_NR, dt, c, lam, lam_out, partials, 1,
-                                                                          nullptr);
+    kern<<<dim3(nx, (g.H + TH - 1) / TH), NT, smem, s>>>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR, dt, c, lam,
+                                                          lam_out, partials, 1, nullptr, CR);
     return cudaGetLastError();
   }
   // small image: 32 x 2 tiles and the window's row chunks split over NS CTAs (as the scratch allows)
   static const bool nosplit = getenv("MSA_LARGE_NOSPLIT") != nullptr;  // test hook: the NS = 1 order
   const long long tiles2 = (long long)nx * ((g.H + 1) / 2);
   int NS = (int)std::min<long long>(4, (8LL * sms + tiles2 - 1) / tiles2);
+  const int CR = cr_for(R, TW, 2, 2, 160 * 1024);
   NS = std::min(NS, (2 * R + 2 + CR - 1) / CR);
   NS = (int)std::min<size_t>((size_t)NS, scratch_floats / per_part);
   if (nosplit || NS < 1) NS = 1;
   const size_t smem = sizeof(float) * (8 * CR * (TW + 2 * R) + (CR + 2 - 1) * (2 * R + 1));
-  cudaError_t e = cudaFuncSetAttribute(k_dal_back_large<C, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  auto kern = CR == CR_MAX ? k_dal_back_large<C, 2, CR_MAX> : k_dal_back_large<C, 2, 0>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
   if (e != cudaSuccess) return e;
-  k_dal_back_large<C, 2><<<dim3(nx, (g.H + 1) / 2, NS), 64, smem, s>>>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR,
-                                                                       dt, c, lam, lam_out, partials, NS, scratch);
+  kern<<<dim3(nx, (g.H + 1) / 2, NS), 64, smem, s>>>(g, R, kernel, exh_x, exh_y, e_c, eps_c, inv_NR, dt, c, lam,
+                                                     lam_out, partials, NS, scratch, CR);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_dal_back_combine<C><<<dim3(nx, (g.H + TH - 1) / TH), 256, 0, s>>>(g, NS, scratch, inv_NR, dt, lam, lam_out,

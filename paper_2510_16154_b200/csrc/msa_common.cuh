@@ -11,7 +11,7 @@
 #include <stdint.h>
 
 #define MSA_MAXC 16
-#define MSA_MAXR 64  // large supports (the paper's eps box E reaches image-size supports)
+#define MSA_MAXR 255  // large supports (the paper's eps box E reaches image-size supports)
 #define MSA_MAXOFF ((2 * MSA_MAXR + 1) * (2 * MSA_MAXR + 1))
 
 struct MsaGeom {

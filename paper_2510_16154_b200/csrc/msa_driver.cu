@@ -161,7 +161,7 @@ int validate(const msa_params* p) {
   if (!finite_all(p)) return set_err(MSA_EINVAL, "non-finite parameter");
   if (p->alpha < 0) return set_err(MSA_EINVAL, "alpha must be >= 0");
   if (p->beta < 0) return set_err(MSA_EINVAL, "beta must be >= 0");
-  if (p->radius < 0 || p->radius > MSA_MAXR) return set_err(MSA_EINVAL, "radius must be in [0,64]");
+  if (p->radius < 0 || p->radius > MSA_MAXR) return set_err(MSA_EINVAL, "radius must be in [0,255]");
   if (p->kernel != MSA_KERNEL_WENDLAND && p->kernel != MSA_KERNEL_PRINTED) return set_err(MSA_EINVAL, "bad kernel");
   if (p->eps_c < 0) return set_err(MSA_EINVAL, "eps_c must be >= 0");
   if (p->dt < 0) return set_err(MSA_EINVAL, "dt must be >= 0");
@@ -224,6 +224,11 @@ int derive(const msa_params* p, Derived* d) {
   const int R = p->radius;
   d->NR = 0;
   d->T.n = 0;
+  const size_t cap = (size_t)(2 * R + 1) * (2 * R + 1);
+  d->T.dx.resize(cap);
+  d->T.dy.resize(cap);
+  d->T.om.resize(cap);
+  d->T.oms.resize(cap);
   d->scaled = use_scaled(p->eps_c) ? 1 : 0;
   // offset order: dx ascending; within a column the even dy ascending, then the odd dy
   // ascending (the order of K1's two parity passes over a cached column). Both kernels sum
@@ -291,9 +296,10 @@ Layout layout(const msa_params* p, const Part& pt) {
   L.nblk = msa_round_blocks(g);
   L.off_partials = o; o += align_up((size_t)pt.nimages * L.nblk * MSA_NSUM * 8, 256);
   L.off_sums = o;     o += align_up(MSA_NSUM * 8, 256);
-  L.off_off = o;      o += align_up(MSA_MAXOFF * sizeof(int2), 256);
-  L.off_om = o;       o += align_up(MSA_MAXOFF * sizeof(float), 256);
-  L.off_omtab = o;    o += align_up(MSA_MAXOFF * sizeof(float), 256);  // [2R+1]^2 table (R > 8)
+  const size_t nwin = (size_t)(2 * p->radius + 1) * (2 * p->radius + 1);  // offsets of the window
+  L.off_off = o;      o += align_up(nwin * sizeof(int2), 256);
+  L.off_om = o;       o += align_up(nwin * sizeof(float), 256);
+  L.off_omtab = o;    o += align_up(nwin * sizeof(float), 256);  // [2R+1]^2 table (R > 8)
   L.off_rec = o;      o += align_up(REC_CAP * sizeof(msa_round_stats), 256);
   L.total = o;
   return L;
@@ -926,7 +932,8 @@ int msa_init(const msa_params* params, const float* image, int image_on_device, 
     if (e == cudaSuccess && x->T.n > 0)
       e = cudaMemcpyAsync(x->d_off, offs.data(), sizeof(int2) * x->T.n, cudaMemcpyHostToDevice, x->stream);
     if (e == cudaSuccess && x->T.n > 0)
-      e = cudaMemcpyAsync(x->d_om, x->scaled ? x->T.oms : x->T.om, sizeof(float) * x->T.n, cudaMemcpyHostToDevice,
+      e = cudaMemcpyAsync(x->d_om, x->scaled ? x->T.oms.data() : x->T.om.data(), sizeof(float) * x->T.n,
+                          cudaMemcpyHostToDevice,
                           x->stream);
     std::vector<float> omtab;
     if (e == cudaSuccess && params->radius > 8) {  // same formula and rounding as the offset table

@@ -5,13 +5,15 @@
 #include <nccl.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "msa_common.cuh"
 
 struct MsaOffsetTable {
-  int n;                   // active offsets
-  int dx[MSA_MAXOFF], dy[MSA_MAXOFF];
-  float om[MSA_MAXOFF];    // 1 - a_delta, a_delta = eps_x/2 ((dx h_x)^2 + (dy h_y)^2)
-  float oms[MSA_MAXOFF];   // the kernels' constant: -om / e_c (scaled form) or om (MsaIterConsts::scaled)
+  int n = 0;                   // active offsets
+  std::vector<int> dx, dy;
+  std::vector<float> om;       // 1 - a_delta, a_delta = eps_x/2 ((dx h_x)^2 + (dy h_y)^2)
+  std::vector<float> oms;      // the kernels' constant: -om / e_c (scaled form) or om (MsaIterConsts::scaled)
 };
 
 // Generic kernels (msa_kernels.cu): any C in [1,16], any R in [0,8].

@@ -57,7 +57,7 @@ def test_workspace_bytes_formula(lib):
 
 
 @pytest.mark.parametrize("bad", [dict(channels=0), dict(channels=17), dict(alpha=-1.0), dict(beta=-0.1),
-                                 dict(radius=65), dict(rho=0.0), dict(gamma=-1.0), dict(kappa=0.0), dict(dt=-0.1),
+                                 dict(radius=256), dict(rho=0.0), dict(gamma=-1.0), dict(kappa=0.0), dict(dt=-0.1),
                                  dict(eps_c=-1.0), dict(iters_per_round=0), dict(rounds=-1), dict(kernel=2),
                                  dict(height=0), dict(world=2, rank=2, shard=1), dict(world=2, shard=0),
                                  dict(tau=1.0, sigma=1.0), dict(alpha=float("nan")), dict(scheme=2),

@@ -66,3 +66,23 @@ def test_large_support_parity_with_oracle(eps_x, R, scheme):
     o = oracle.State(oracle.Params.from_solver(H, W, C, sp), I[0].astype(np.float64))
     o.run(50)
     assert np.max(rel_err_per_pixel(gc, o.c)) <= 1e-4
+
+
+@pytest.mark.parametrize("H,W,C,R,eps_x", [(48, 48, 1, 100, 2.0), (36, 30, 3, 255, 2.0), (80, 72, 2, 140, 2.0)])
+def test_all_pairs_regime_parity_with_oracle(H, W, C, R, eps_x):
+    """The paper's box E = [2, 1100]^2 at its lower end (eps_x = 2): supports of the whole image.
+    With R >= the support radius (up to the new R <= 255) the window sum is the paper's all-pairs
+    sum with 1/N_R, which the oracle evaluates pair by pair."""
+    rng = np.random.default_rng(H + W + C + R)
+    I = np.clip(rng.random((1, H, W, C)) * 0.2 + np.repeat(np.repeat(rng.random((1, 3, 3, C)), H // 3 + 1, 1)[:, :H],
+                                                          W // 3 + 1, 2)[:, :, :W], 0, 1).astype(np.float32)
+    h = 1.0 / (max(W, H) - 1)
+    assert 1.0 / (h * np.sqrt(eps_x / 2.0)) <= R or R >= max(H, W)
+    sp = dict(alpha=8.0 / h, beta=1.0, radius=R, kernel=0, eps_x=eps_x, eps_c=57.0, dt=0.25, rho=2.5 * h,
+              gamma=2.5 * h, kappa=1.0, tau=0.0, sigma=0.0, theta=1.0, iters_per_round=5, rounds=2, scheme=0)
+    with msa.Solver(msa.Params.from_solver(1, H, W, C, sp), I) as s:
+        s.solve()
+        gc = s.get_field(msa.FIELD_C)[0]
+    o = oracle.State(oracle.Params.from_solver(H, W, C, sp), I[0].astype(np.float64))
+    o.run(10)
+    assert np.max(rel_err_per_pixel(gc, o.c)) <= 1e-4

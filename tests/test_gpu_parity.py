@@ -265,6 +265,6 @@ def test_invalid_params_fail_loudly():
         msa.Solver(gpu_params(img, dict(sp, rho=-1.0)), img)
     assert e.value.code == msa.MSA_EINVAL
     with pytest.raises(msa.MsaError):
-        msa.Solver(gpu_params(img, dict(sp, radius=65)), img)
+        msa.Solver(gpu_params(img, dict(sp, radius=256)), img)
     with pytest.raises(msa.MsaError):
         msa.Solver(gpu_params(img, dict(sp, scheme=1, kappa=2.0)), img)
