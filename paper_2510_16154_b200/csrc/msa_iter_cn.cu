@@ -1,4 +1,4 @@
-// msa_iter_cn.cu - K1 for many channels (C = 16: BASELINE config 5), sm_100a. The iteration is the
+// msa_iter_cn.cu - K1 for many channels (C = 5..16; C = 16 is BASELINE config 5), sm_100a. The iteration is the
 // one of msa_kernels.cu (eq:MAsystem PAPER.md:86-95, eq:complete_square :397-404, eq:new_adjoint
 // :405-413).
 //
@@ -248,7 +248,7 @@ cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const M
                                const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
-  if (g.C != 16 || R < 1 || R > 4 || T.n > CN_MAXOFF || !K.scaled) return cudaErrorNotSupported;
+  if (g.C < 5 || g.C > 16 || R < 1 || R > 4 || T.n > CN_MAXOFF || !K.scaled) return cudaErrorNotSupported;
   CnOffsets off;
   off.n = T.n;
   for (int o = 0; o < T.n; ++o) {
@@ -264,7 +264,14 @@ cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const M
   key.plane = g.plane;
   CnMaps tm;
   if (!get_maps(key, g, R, &tm)) return cudaErrorNotSupported;
-  cudaError_t e = launch_c<16>(g, K, off, tm, R, p, mu, I, c_out, cb_out, p_out, s);
+  cudaError_t e;
+  switch (g.C) {  // every channel count above the tiled kernel's C <= 4
+#define CN_C(CC) \
+  case CC: e = launch_c<CC>(g, K, off, tm, R, p, mu, I, c_out, cb_out, p_out, s); break;
+    CN_C(5) CN_C(6) CN_C(7) CN_C(8) CN_C(9) CN_C(10) CN_C(11) CN_C(12) CN_C(13) CN_C(14) CN_C(15) CN_C(16)
+#undef CN_C
+    default: return cudaErrorNotSupported;
+  }
   if (e == cudaSuccess) *launched = 1;
   return e;
 }

@@ -1,5 +1,5 @@
 """K1 time for C = 1..4 channels (cfg4 recipe at 2048^2, R = 5): grey (the paper's own images),
-two-channel, RGB and RGBA fields all run on the tiled kernel. usage: python tools/time_channels.py [side]"""
+two-channel, RGB and RGBA fields all run on the tiled kernel. usage: [RADIUS=r] python tools/time_channels.py [side] [C,C,...]"""
 import os, sys, json
 sys.path.insert(0, os.getcwd())
 import torch, numpy as np
@@ -7,9 +7,11 @@ import paper_2510_16154_b200 as msa
 import synth
 from dataclasses import replace
 SIDE = int(sys.argv[1]) if len(sys.argv) > 1 else 2048
-for C in (1, 2, 3, 4):
+CS = [int(a) for a in sys.argv[2].split(',')] if len(sys.argv) > 2 else [1, 2, 3, 4]
+for C in CS:
     cfg = synth.CONFIGS["cfg4"]
-    rc = replace(cfg, recipe=replace(cfg.recipe, height=SIDE, width=SIDE, channels=C), rounds=2, iters_per_round=50)
+    rc = replace(cfg, recipe=replace(cfg.recipe, height=SIDE, width=SIDE, channels=C), rounds=2, iters_per_round=50,
+                 radius=int(os.environ.get("RADIUS", cfg.radius)))
     img = synth.generate(rc.recipe)
     sp = synth.solver_params(rc)
     B, H, W, Cc = img.shape
