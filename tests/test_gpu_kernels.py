@@ -70,7 +70,10 @@ def test_tile_equals_generic_bitwise(shape, R, ker, tmp_path):
         assert np.array_equal(a[k], b[k]), (k, float(np.max(np.abs(a[k] - b[k]))))
 
 
-SWEEP_CASES = CASES + [((1, 97, 131, 3), 5, 0), ((3, 45, 61, 3), 3, 1), ((1, 33, 28, 3), 5, 0), ((1, 4, 200, 3), 2, 0)]
+# the sweep kernel is opt-in (MSA_K1=sweep): a representative subset - every radius, both kernels,
+# batch, ragged and thin shapes
+SWEEP_CASES = [((1, 64, 32, 3), 5, 0), ((1, 37, 29, 3), 3, 0), ((2, 70, 66, 3), 2, 1), ((1, 5, 7, 3), 4, 0),
+               ((1, 97, 131, 3), 5, 0), ((3, 45, 61, 3), 3, 1), ((1, 4, 200, 3), 2, 0)]
 
 
 @pytest.mark.parametrize("shape,R,ker", SWEEP_CASES)
