@@ -39,8 +39,12 @@ constexpr int TW = 32, TH = MSA_CN_TH, NT = TW * TH;  // one pixel per thread
 #define MSA_CN_OCC 2
 #endif
 constexpr int CN_OCC = MSA_CN_OCC;
-constexpr int CX = 4;           // smem column of tile column 0 (box starts 16-byte aligned)
-constexpr int CW = TW + 2 * CX; // 40
+// smem column of tile column 0 (>= R, box starts 16-byte aligned) and the c / cbar tile width
+template <int R>
+struct CnGeo {
+  static constexpr int CX = R <= 4 ? 4 : 8;
+  static constexpr int CW = TW + 2 * CX;  // 40 or 48
+};
 constexpr int QW = TW + 1;      // p+ tile: columns x0-1 .. x0+31
 constexpr int QH = TH + 1;      // rows y0-1 .. y0+7
 
@@ -57,6 +61,7 @@ struct CnMaps {
 
 template <int C, int R>
 struct CnSmem {
+  static constexpr int CW = CnGeo<R>::CW;
   static constexpr int c_floats = C * (TH + 2 * R) * CW;
   static constexpr int q_floats = 2 * C * QH * QW;
   static constexpr int u_floats = ((c_floats > q_floats ? c_floats : q_floats) + 31) / 32 * 32;
@@ -72,6 +77,7 @@ __global__ void __launch_bounds__(NT, CN_OCC)
               float* __restrict__ c_out, float* __restrict__ cb_out, float* __restrict__ p_out) {
   using S = CnSmem<C, R>;
   constexpr int SH = TH + 2 * R, BH = TH + 2;
+  constexpr int CX = CnGeo<R>::CX, CW = CnGeo<R>::CW;
   extern __shared__ __align__(128) float smem[];
   float* sc = smem;             // [C][SH][CW] c tile (step 1)
   float* sq = smem;             // [2C][QH][QW] p+ (steps 2-3, reuses the c tile)
@@ -200,6 +206,7 @@ bool get_maps(const CnKey& k, const MsaGeom& g, int R, CnMaps* out) {
       return true;
     }
   CnMaps t;
+  const int CX = R <= 4 ? 4 : 8, CW = TW + 2 * CX;  // CnGeo<R>
   if (!encode_map(&t.c, g, k.c, g.C, CW, TH + 2 * R) || !encode_map(&t.cb, g, k.cb, g.C, CW, TH + 2) ||
       !encode_map(&t.p, g, k.p, 2 * g.C, CW - CX, TH + 1) || !encode_map(&t.mu, g, k.mu, 2 * g.C, CW - CX, TH + 1) ||
       !encode_map(&t.I, g, k.I, g.C, TW, TH))
@@ -237,6 +244,7 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, const CnOffsets& 
     CN_CASE(2)
     CN_CASE(3)
     CN_CASE(4)
+    CN_CASE(5)
     default: return cudaErrorNotSupported;
   }
 #undef CN_CASE
@@ -248,7 +256,7 @@ cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const M
                                const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
-  if (g.C < 5 || g.C > 16 || R < 1 || R > 4 || T.n > CN_MAXOFF || !K.scaled) return cudaErrorNotSupported;
+  if (g.C < 5 || g.C > 16 || R < 1 || R > 5 || T.n > CN_MAXOFF || !K.scaled) return cudaErrorNotSupported;
   CnOffsets off;
   off.n = T.n;
   for (int o = 0; o < T.n; ++o) {
