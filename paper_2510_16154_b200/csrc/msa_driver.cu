@@ -563,6 +563,8 @@ int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int 
     cudaError_t e = cudaErrorNotSupported;
     if (k1_variant() != K1_GENERIC)
       e = msa_launch_iter_fast_lin(g, KC, x->T, P.radius, x->c[s], x->p[s], x->I, x->c[o], x->p[o], st, &ok);
+    if (!ok && k1_variant() != K1_GENERIC && (e == cudaErrorNotSupported || e == cudaSuccess))
+      e = msa_launch_iter_cn_lin(g, KC, x->T, P.radius, x->c[s], x->p[s], x->I, x->c[o], x->p[o], st, &ok);
     if (!ok && e != cudaErrorNotSupported && e != cudaSuccess)
       return set_err(MSA_ECUDA, "linearised tiled kernel: %s", cudaGetErrorString(e));
     if (!ok)

@@ -67,6 +67,10 @@ cudaError_t msa_launch_iter_sweep(const MsaGeom& g, const MsaIterConsts& K, cons
 cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
                                const float* c, const float* cb, const float* p, const float* mu, const float* I,
                                float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched);
+// the linearised scheme (MSA_SCHEME_LINEARISED_ADMM) on the many-channel kernel: mu in, mu_out out
+cudaError_t msa_launch_iter_cn_lin(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                                   const float* c, const float* mu, const float* I, float* c_out, float* mu_out,
+                                   cudaStream_t s, int* launched);
 
 // Round update (steps 4-5): writes mu_out (may alias mu) and per-block fp64 partial sums
 // [nb][nblk][MSA_NSUM]; *nblk receives the number of blocks per image. v_out (may be null):

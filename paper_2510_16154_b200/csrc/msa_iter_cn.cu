@@ -187,6 +187,130 @@ __global__ void __launch_bounds__(NT, CN_OCC)
   }
 }
 
+// The single-loop linearised ADMM iteration (msa.h MSA_SCHEME_LINEARISED_ADMM) for C = 5..16: step 1
+// as above; mu+ = Pi_beta(mu - rho grad c) at the tile and its low-side halo, grad c from the c tile
+// (kept: 2 mu+ - mu goes to its own region), mu read through L2 (prefetched); mu+ of own pixels
+// written straight to mu_out; c+ = c_half + (-tau div(2 mu+ - mu) + tau alpha (I - c_half)) /
+// (1 + tau alpha). The arithmetic and order of k_iter_lin_generic: bitwise equal.
+template <int C, int R>
+struct CnSmemLin {
+  static constexpr int CW = CnGeo<R>::CW;
+  static constexpr int c_floats = ((C * (TH + 2 * R) * CW) + 31) / 32 * 32;
+  static constexpr int q_floats = 2 * C * QH * QW;
+  static constexpr size_t bytes = sizeof(float) * (c_floats + q_floats);
+};
+
+template <int C, int R, int KER>
+__global__ void __launch_bounds__(NT, CN_OCC)
+    k_iter_cn_lin(MsaGeom g, MsaIterConsts K, const __grid_constant__ CnOffsets T, const __grid_constant__ CnMaps tm,
+                  const float* __restrict__ mu, const float* __restrict__ I, float* __restrict__ c_out,
+                  float* __restrict__ mu_out) {
+  using S = CnSmemLin<C, R>;
+  constexpr int SH = TH + 2 * R;
+  constexpr int CX = CnGeo<R>::CX, CW = CnGeo<R>::CW;
+  extern __shared__ __align__(128) float smem[];
+  float* sc = smem;                // [C][SH][CW] c tile (step 1 and grad c)
+  float* sb = smem + S::c_floats;  // [2C][QH][QW] 2 mu+ - mu
+  __shared__ __align__(8) unsigned long long bar;
+
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int x0 = blockIdx.x * TW, y0 = g.row0 + g.k1_lo + blockIdx.y * TH, b = blockIdx.z;
+  const int W = g.W, H = g.H;
+  const int x = x0 + tx, y = y0 + ty;
+  const int ys = y0 - g.row0 + g.G;
+  const int yend = g.row0 + g.nrows;  // outputs stop at the slab's end
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, (unsigned)(sizeof(float) * C * SH * CW));
+    tma_load3(sc, &tm.c, x0 - CX, ys - R, b * C, &bar);
+    tma_prefetch3(&tm.mu, x0 - CX, ys - 1, b * 2 * C);
+    tma_prefetch3(&tm.I, x0, ys, b * C);
+  }
+  mbar_wait(&bar, 0);
+
+  float chalf[C];
+  {
+    float ci[C], acc[C];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      ci[k] = sc[(k * SH + ty + R) * CW + CX + tx];
+      acc[k] = 0.0f;
+    }
+    auto term = [&](int o) {
+      const float* src = sc + (ty + R + T.dy[o]) * CW + CX + tx + T.dx[o];
+      float cj[C];
+#pragma unroll
+      for (int k = 0; k < C; ++k) cj[k] = src[k * SH * CW];
+      msa_agent_term_s<C, KER>(ci, cj, T.om[o], K.m4, acc);
+    };
+    if (x0 - R >= 0 && x0 + TW + R <= W && y0 - R >= 0 && y0 + TH + R <= H) {
+#pragma unroll 4
+      for (int o = 0; o < T.n; ++o) term(o);
+    } else {
+      for (int o = 0; o < T.n; ++o) {
+        const int xx = x + T.dx[o], yy = y + T.dy[o];
+        if (xx < 0 || xx >= W || yy < 0 || yy >= H) continue;
+        term(o);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_s, acc[k], ci[k]);
+  }
+
+  // mu+ at tile coordinates (hx - 1, hy - 1), hx < 33, hy < TH + 1
+  for (int idx = threadIdx.x; idx < QW * QH; idx += NT) {
+    const int hy = idx / QW, hx = idx - hy * QW;
+    const int xx = x0 + hx - 1, yy = y0 + hy - 1;
+    if (xx < 0 || yy < 0 || xx >= W || yy >= H) {
+#pragma unroll
+      for (int k = 0; k < 2 * C; ++k) sb[(k * QH + hy) * QW + hx] = 0.0f;
+      continue;
+    }
+    float gx[C], gy[C], mx[C], my[C], qx[C], qy[C];
+    const long long o0 = msa_idx(g, b, 0, 2 * C, yy, xx);
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const float* ck = sc + (k * SH + hy - 1 + R) * CW + CX + hx - 1;
+      const float c0 = ck[0];
+      gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(ck[1], c0), K.inv_hx) : 0.0f;
+      gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(ck[CW], c0), K.inv_hy) : 0.0f;
+      mx[k] = __ldg(mu + o0 + k * g.plane);
+      my[k] = __ldg(mu + o0 + (C + k) * g.plane);
+    }
+    msa_lin_dual<C>(K, gx, gy, mx, my, qx, qy);
+    const bool own = hx >= 1 && hy >= 1 && yy < yend;
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      sb[(k * QH + hy) * QW + hx] = __fmaf_rn(2.0f, qx[k], -mx[k]);
+      sb[((C + k) * QH + hy) * QW + hx] = __fmaf_rn(2.0f, qy[k], -my[k]);
+      if (own) {
+        mu_out[o0 + k * g.plane] = qx[k];
+        mu_out[o0 + (C + k) * g.plane] = qy[k];
+      }
+    }
+  }
+  __syncthreads();
+
+  if (x >= W || y >= yend) return;
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    const float* bx = sb + (k * QH + ty + 1) * QW + tx + 1;
+    const float* by = sb + ((C + k) * QH + ty + 1) * QW + tx + 1;
+    float ax = x < W - 1 ? bx[0] : 0.0f;
+    if (x > 0) ax = __fsub_rn(ax, bx[-1]);
+    float ay = y < H - 1 ? by[0] : 0.0f;
+    if (y > 0) ay = __fsub_rn(ay, by[-QW]);
+    const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
+    float cp, cbp;
+    msa_prox_extrap(K, chalf[k], -d, __ldg(I + msa_idx(g, b, k, C, y, x)), cp, cbp);  // -tau div(2 mu+ - mu)
+    c_out[msa_idx(g, b, k, C, y, x)] = cp;
+  }
+}
+
 struct CnKey {
   const float *c, *cb, *p, *mu, *I;
   int W, rows, nb, pitch, C, R;
@@ -232,13 +356,32 @@ cudaError_t launch_k(const MsaGeom& g, const MsaIterConsts& K, const CnOffsets& 
   return cudaGetLastError();
 }
 
-template <int C>
+template <int C, int R, int KER>
+cudaError_t launch_k_lin(const MsaGeom& g, const MsaIterConsts& K, const CnOffsets& T, const CnMaps& tm,
+                         const float* mu, const float* I, float* co, float* muo, cudaStream_t s) {
+  using S = CnSmemLin<C, R>;
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(k_iter_cn_lin<C, R, KER>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::bytes);
+  if (attr != cudaSuccess) return attr;
+  const int nr = msa_k1_hi(g) - g.k1_lo;
+  if (nr <= 0) return cudaSuccess;
+  dim3 grd((g.W + TW - 1) / TW, (nr + TH - 1) / TH, g.nb);
+  k_iter_cn_lin<C, R, KER><<<grd, NT, S::bytes, s>>>(g, K, T, tm, mu, I, co, muo);
+  return cudaGetLastError();
+}
+
+// LIN: p is mu (in), po mu+ (out); cb / cbo unused
+template <int C, bool LIN>
 cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, const CnOffsets& T, const CnMaps& tm, int R,
                      const float* p, const float* mu, const float* I, float* co, float* cbo, float* po, cudaStream_t s) {
 #define CN_CASE(RR)                                                                                   \
   case RR:                                                                                            \
-    return K.kernel == 0 ? launch_k<C, RR, 0>(g, K, T, tm, p, mu, I, co, cbo, po, s)                  \
-                         : launch_k<C, RR, 1>(g, K, T, tm, p, mu, I, co, cbo, po, s);
+    if constexpr (LIN)                                                                                \
+      return K.kernel == 0 ? launch_k_lin<C, RR, 0>(g, K, T, tm, p, I, co, po, s)                      \
+                           : launch_k_lin<C, RR, 1>(g, K, T, tm, p, I, co, po, s);                     \
+    else                                                                                              \
+      return K.kernel == 0 ? launch_k<C, RR, 0>(g, K, T, tm, p, mu, I, co, cbo, po, s)                \
+                           : launch_k<C, RR, 1>(g, K, T, tm, p, mu, I, co, cbo, po, s);
   switch (R) {
     CN_CASE(1)
     CN_CASE(2)
@@ -252,9 +395,11 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, const CnOffsets& 
 
 }  // namespace
 
-cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
-                               const float* c, const float* cb, const float* p, const float* mu, const float* I,
-                               float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
+namespace {
+template <bool LIN>
+cudaError_t launch_cn(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R, const float* c,
+                      const float* cb, const float* p, const float* mu, const float* I, float* c_out, float* cb_out,
+                      float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
   if (g.C < 5 || g.C > 16 || R < 1 || R > 5 || T.n > CN_MAXOFF || !K.scaled) return cudaErrorNotSupported;
   CnOffsets off;
@@ -275,11 +420,25 @@ cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const M
   cudaError_t e;
   switch (g.C) {  // every channel count above the tiled kernel's C <= 4
 #define CN_C(CC) \
-  case CC: e = launch_c<CC>(g, K, off, tm, R, p, mu, I, c_out, cb_out, p_out, s); break;
+  case CC: e = launch_c<CC, LIN>(g, K, off, tm, R, p, mu, I, c_out, cb_out, p_out, s); break;
     CN_C(5) CN_C(6) CN_C(7) CN_C(8) CN_C(9) CN_C(10) CN_C(11) CN_C(12) CN_C(13) CN_C(14) CN_C(15) CN_C(16)
 #undef CN_C
     default: return cudaErrorNotSupported;
   }
   if (e == cudaSuccess) *launched = 1;
   return e;
+}
+}  // namespace
+
+cudaError_t msa_launch_iter_cn(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                               const float* c, const float* cb, const float* p, const float* mu, const float* I,
+                               float* c_out, float* cb_out, float* p_out, cudaStream_t s, int* launched) {
+  return launch_cn<false>(g, K, T, R, c, cb, p, mu, I, c_out, cb_out, p_out, s, launched);
+}
+
+// the linearised scheme: mu in p (in) and p_out (out); c stands in for the unused cbar maps
+cudaError_t msa_launch_iter_cn_lin(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetTable& T, int R,
+                                   const float* c, const float* mu, const float* I, float* c_out, float* mu_out,
+                                   cudaStream_t s, int* launched) {
+  return launch_cn<true>(g, K, T, R, c, c, mu, mu, I, c_out, nullptr, mu_out, s, launched);
 }

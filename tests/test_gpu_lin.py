@@ -108,10 +108,12 @@ def test_lin_split_bitwise(tmp_path):
 
 
 @pytest.mark.parametrize("shape,R", [((1, 64, 32, 3), 5), ((1, 130, 97, 3), 5), ((2, 70, 66, 3), 2),
-                                     ((1, 37, 29, 3), 3), ((1, 5, 7, 3), 4)])
+                                     ((1, 37, 29, 3), 3), ((1, 5, 7, 3), 4), ((1, 48, 40, 1), 5),
+                                     ((1, 40, 36, 16), 3), ((2, 33, 41, 7), 5), ((1, 9, 70, 12), 2)])
 def test_lin_tile_equals_generic_bitwise(shape, R, tmp_path):
-    """The tiled C = 3 kernel of the single-loop scheme (msa_iter_fast.cu, LIN) has the generic
-    kernel's per-pixel arithmetic: bitwise-identical fields, across a round."""
+    """The tiled kernels of the single-loop scheme (msa_iter_fast.cu LIN for C <= 4, msa_iter_cn.cu
+    LIN for C = 5..16) have the generic kernel's per-pixel arithmetic: bitwise-identical fields,
+    across a round."""
     B, H, W, C = shape
     h = 1.0 / (W - 1) if W > 1 else 1.0
     spec = dict(seed=H * 100 + W + R, shape=list(shape), iters=3,
