@@ -216,7 +216,7 @@ cudaError_t msa_launch_agent_large(const MsaGeom& g, const MsaIterConsts& K, int
                                    float* scratch, size_t scratch_floats, int* launches) {
   int dummy = 0;
   if (!launches) launches = &dummy;
-  if (R <= 8 || R > MSA_MAXR) return cudaErrorNotSupported;
+  if (R <= 5 || R > MSA_MAXR) return cudaErrorNotSupported;
   switch (g.C) {
     case 1: return launch_c<1>(g, K, R, omtab, exh_x, exh_y, c, chalf, s, scratch, scratch_floats, launches);
     case 2: return launch_c<2>(g, K, R, omtab, exh_x, exh_y, c, chalf, s, scratch, scratch_floats, launches);

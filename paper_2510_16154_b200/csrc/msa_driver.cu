@@ -540,7 +540,9 @@ int k1_variant() {
 int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int o, cudaStream_t st) {
   const msa_params& P = x->prm;
   // large supports (NEXT-3): step 1 by the chunked n-body kernel into c[o], steps 2-3 generic
-  if (P.radius > 8 && P.channels <= 4 && k1_variant() != K1_GENERIC) {
+  // large supports (NEXT-3), and the radii between the tiled kernel's R <= 5 and 8 (C <= 4)
+  static const int large_from = getenv("MSA_LARGE_FROM") ? atoi(getenv("MSA_LARGE_FROM")) : 6;  // A/B hook
+  if (P.radius >= large_from && P.radius > 5 && P.channels <= 4 && k1_variant() != K1_GENERIC) {
     // scratch for a window split at small images: cb[o] and p[o] (3C planes, contiguous) are
     // written only after step 1
     int nl = 1;
@@ -938,7 +940,7 @@ int msa_init(const msa_params* params, const float* image, int image_on_device, 
                           cudaMemcpyHostToDevice,
                           x->stream);
     std::vector<float> omtab;
-    if (e == cudaSuccess && params->radius > 8) {  // same formula and rounding as the offset table
+    if (e == cudaSuccess && params->radius > 5) {  // same formula and rounding as the offset table
       const int R = params->radius, OW = 2 * R + 1;
       omtab.resize((size_t)OW * OW);
       for (int dy = -R; dy <= R; ++dy)

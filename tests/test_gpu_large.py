@@ -29,7 +29,8 @@ def _run(spec, variant, tmp_path):
     return np.load(out)
 
 
-@pytest.mark.parametrize("shape,R,ker,scheme", [((1, 48, 40, 3), 9, 0, 0), ((1, 70, 66, 3), 16, 0, 0),
+@pytest.mark.parametrize("shape,R,ker,scheme", [((1, 48, 40, 3), 6, 0, 0), ((1, 41, 37, 1), 8, 1, 0),
+                                                ((1, 48, 40, 3), 9, 0, 0), ((1, 70, 66, 3), 16, 0, 0),
                                                 ((2, 37, 29, 3), 12, 1, 0), ((1, 90, 50, 1), 24, 0, 0),
                                                 ((1, 64, 64, 3), 40, 0, 0), ((1, 66, 70, 3), 16, 0, 1),
                                                 ((1, 40, 41, 4), 20, 0, 0)])
