@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define MSA_ABI_VERSION 2 /* 2: msa_params.scheme */
+#define MSA_ABI_VERSION 3 /* 2: msa_params.scheme; 3: msa_info.halo_exchanges / halo_ms */
 
 enum {
   MSA_OK = 0,
@@ -77,7 +77,7 @@ typedef struct {
   int32_t batch, height, width, channels; /* B >= 1, H, W >= 1, 1 <= C <= 16 */
   double alpha;       /* fidelity weight alpha >= 0 (eq:cost_TV; alpha = 0 allowed: D, gap = NaN) */
   double beta;        /* TV weight beta >= 0 (1 in eq:cost_TV; reading R27) */
-  int32_t radius;     /* window radius R in pixels, 0 <= R <= 255 (reading R2; R > 8: NEXT-3 large supports) */
+  int32_t radius;     /* window radius R in pixels, 0 <= R <= 255 (reading R2; R >= 6: NEXT-3 large supports) */
   int32_t kernel;     /* MSA_KERNEL_WENDLAND (4r+1)(1-r)^4 or MSA_KERNEL_PRINTED (4r-1)(1-r)^4 (R3) */
   double eps_x;       /* eq:ellipsoid spatial control; <= 0 -> 2/(R min(h_x,h_y))^2 (R2) */
   double eps_c;       /* eq:ellipsoid colour control >= 0 (57 in PAPER.md:270) */
@@ -121,6 +121,10 @@ typedef struct {
   int64_t iters_done;       /* global iteration counter */
   int64_t launches;         /* kernels launched by this context so far */
   double rho;               /* current penalty */
+  /* (ABI 3) rows mode with msa_set_timing(1): halo exchanges run since then and their summed
+   * device time (gather kernel + grouped NCCL send/recv + scatter kernel), in ms; synchronises */
+  int64_t halo_exchanges;
+  double halo_ms;
 } msa_info;
 
 int msa_abi_version(void);
@@ -264,17 +268,33 @@ typedef struct {
   double sigma0;      /* initial step sigma^(0) > 0 */
   double b, c;        /* Armijo factors in (0, 1) */
   double ex_lo, ex_hi, ec_lo, ec_hi; /* the box E = [ex_lo, ex_hi] x [ec_lo, ec_hi], ex_lo > 0 */
+  /* (ABI 3) Remark 3.4 stopping rules, checked at the top of iteration j >= 1; <= 0
+   * disables a rule: eta: |J(eps^(j)) - J(eps^(j-1))| / J(eps^(j-1)) < eta (cost stationarity, the
+   * paper's rule, eta = 1e-10 at PAPER.md:270); eta_grad: max |projected D| < eta_grad (a component of
+   * D counts as 0 on the lower contact set if D >= 0 and on the upper one if D <= 0). */
+  double eta, eta_grad;
+  /* (ABI 3) msa_dal_admm only: 1 = choose the ascent step gamma^(j) of Alg. 2 line 7 by the two-way
+   * Armijo search of Algorithm 1 (the remark after Algorithm 2) on the dual value
+   * Phi(mu) = min_v L(c(mu), v, mu), c(mu) the line-5 solution at mu: accept t when
+   * Phi(mu + t g) >= Phi(mu) + c t |g|^2, g = v^(j) - grad c^(j); grow t / b while it passes, else
+   * shrink b t until it passes (max_ls evaluations; none passes: no ascent step). The search starts
+   * from params.gamma, then from the last accepted step. 0 = the fixed step params.gamma. */
+  int32_t gamma_ls;
+  int32_t reserved_;
 } msa_dal_params;
+/* stop (ABI 3, may be NULL): stop[0] = DAL iterations run, stop[1] = 0 (iteration cap), 1 (cost
+ * stationarity), 2 (projected gradient); J_hist[0 .. stop[0]] and sigma_hist[0 .. stop[0]) are written. */
 int msa_dal(msa_ctx* ctx, const msa_dal_params* d, double* eps, const float* v, const float* mu, double* J_hist,
-            double* sigma_hist);
+            double* sigma_hist, int32_t* stop);
 /* Algorithm 2 with Algorithm 1 as its line 5: `outer` times, DAL (d, cost must
  * be 1) at (v^(j-1), mu^(j)) -> eps, c = c(T; eps); then v^(j) = S_{beta/rho}(grad c - mu^(j)/rho) and
  * mu^(j+1) = mu^(j) + gamma (v^(j) - grad c) on the device, with a round record of c^(j) in
  * stats[j] (dual and gap refer to p = 0). v, mu: host [H][W][2C] initial values or NULL (0).
- * J_hist: [outer][iters + 1] or NULL. eps is updated in place; the final mu is MSA_FIELD_MU.
- * Synchronises. (ABI 2) */
+ * J_hist: [outer][iters + 1] or NULL (a DAL run stopped early by eta / eta_grad repeats its last cost).
+ * gamma_hist: [outer] ascent steps taken (d->gamma_ls) or NULL. eps is updated in place; the final mu
+ * is MSA_FIELD_MU. Synchronises. (ABI 2; gamma_hist ABI 3) */
 int msa_dal_admm(msa_ctx* ctx, const msa_dal_params* d, double* eps, const float* v, const float* mu,
-                 int32_t outer, double* J_hist, msa_round_stats* stats);
+                 int32_t outer, double* J_hist, msa_round_stats* stats, double* gamma_hist);
 /* J(eps) and its gradient dJ/deps ([steps][2], host) without optimising (may be NULL). */
 int msa_dal_gradient(msa_ctx* ctx, const msa_dal_params* d, const double* eps, const float* v, const float* mu,
                      double* J, double* grad);

@@ -92,7 +92,8 @@ class _DalParams(ctypes.Structure):
     _fields_ = [("M", ctypes.c_int32), ("cost", ctypes.c_int32), ("iters", ctypes.c_int32),
                 ("max_ls", ctypes.c_int32), ("sigma0", ctypes.c_double), ("b", ctypes.c_double),
                 ("c", ctypes.c_double), ("ex_lo", ctypes.c_double), ("ex_hi", ctypes.c_double),
-                ("ec_lo", ctypes.c_double), ("ec_hi", ctypes.c_double), ("rho", ctypes.c_double)]
+                ("ec_lo", ctypes.c_double), ("ec_hi", ctypes.c_double), ("rho", ctypes.c_double),
+                ("eta", ctypes.c_double), ("eta_grad", ctypes.c_double)]
 
 
 @dataclass
@@ -110,6 +111,8 @@ class DalParams:
     ec_lo: float = 2.0
     ec_hi: float = 1100.0
     rho: float = 1.0
+    eta: float = 0.0        # Remark 3.4 cost stationarity tolerance (1e-10); 0: off
+    eta_grad: float = 0.0   # Remark 3.4 projected-gradient tolerance; 0: off
 
     def c_struct(self) -> _DalParams:
         return _DalParams(**asdict(self))
@@ -147,7 +150,7 @@ def _load():
             "mo_agent_deps": ([P, ctypes.c_double, ctypes.c_double, _D, _D, _D], None),
             "mo_dal_cost": ([P, ctypes.POINTER(_DalParams), _D, _D, _D, _D, _D], ctypes.c_double),
             "mo_dal_gradient": ([P, ctypes.POINTER(_DalParams), _D, _D, _D, _D, _D], ctypes.c_double),
-            "mo_dal": ([P, ctypes.POINTER(_DalParams), _D, _D, _D, _D, _D, _D], ctypes.c_int),
+            "mo_dal": ([P, ctypes.POINTER(_DalParams), _D, _D, _D, _D, _D, _D, _D], ctypes.c_int),
             "mo_labels": ([_D, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_float, _D,
                            ctypes.POINTER(ctypes.c_int32), _D, ctypes.c_int32], ctypes.c_int),
         }
@@ -344,27 +347,75 @@ def dal_cost(p: Params, d: DalParams, eps, I, v=None, mu=None, return_state: boo
     return (J, cT) if return_state else J
 
 
-def dal_admm(p: Params, d: DalParams, eps, I, outer: int, v=None, mu=None):
+def dual_value(p: Params, rho: float, c, mu, I) -> float:
+    """Phi(mu) = min_v L(c, v, mu) at a fixed state c: the augmented Lagrangian of eq:complete_square
+    at v = S_{beta/rho}(grad c - mu/rho) (eq:soft_threshold is the exact minimiser over v; pins P12/P13)."""
+    v = shrink_field(p, rho, c, mu)
+    return energy_L(p, rho, c, v, mu, I)
+
+
+def dal_admm(p: Params, d: DalParams, eps, I, outer: int, v=None, mu=None, gamma_search: bool = False):
     """Algorithm 2 with Algorithm 1 as its line 5, step by step: for j = 0 ..
     outer-1: eps^(j) by dal() with the augmented-Lagrangian terminal at (v^(j-1), mu^(j)) (d.cost = 1),
     c^(j) = c(T; eps^(j)) by dal_cost(); v^(j) = S_{beta/rho}(grad c^(j) - mu^(j)/rho) (line 6,
-    eq:soft_threshold); mu^(j+1) = mu^(j) + gamma (v^(j) - grad c^(j)) (line 7). v^(-1), mu^(0): the
-    arguments or 0. Returns (eps, J_hist [outer][iters+1], c^(outer-1), v, mu)."""
+    eq:soft_threshold); mu^(j+1) = mu^(j) + gamma^(j) (v^(j) - grad c^(j)) (line 7). v^(-1), mu^(0): the
+    arguments or 0.
+
+    gamma^(j): the fixed gamma, or (gamma_search) the two-way Armijo search of Algorithm 1 used for the
+    ascent step as the remark after Algorithm 2 proposes: with g = v^(j) - grad c^(j)
+    and Phi(mu') = min_v L(c(mu'), v, mu'), c(mu') the line-5 solution at (v^(j), mu') from eps^(j),
+    a step t passes when Phi(mu^(j) + t g) >= Phi(mu^(j)) + c t |g|_w^2 (Phi(mu^(j)) at c^(j)); starting
+    from gamma (then from the last accepted step) t grows by 1/b while it passes (the last passing t is
+    kept) or shrinks by b until it passes, at most max_ls tests; none passes: no ascent step.
+    Returns (eps, J_hist [outer][iters+1], c^(outer-1), v, mu[, gamma_hist])."""
     q = derive(p)
     d = replace(d, rho=q.rho)  # one penalty: the AL terminal of line 5 and the updates of lines 6-7
     eps = _f64(eps).copy()
     I = _f64(I)
     H, W, C = I.shape
+    w = q.hx * q.hy
     v = np.zeros((H, W, 2 * C)) if v is None else _f64(v).copy()
     mu = np.zeros((H, W, 2 * C)) if mu is None else _f64(mu).copy()
-    Jh, c = [], I.copy()
+    Jh, gh, c, gam = [], [], I.copy(), q.gamma
     for _ in range(outer):
         eps, J, _ = dal(p, d, eps, I, v, mu)
-        Jh.append(J)
+        Jh.append(np.concatenate([J, np.full(d.iters + 1 - len(J), J[-1])]))  # an early stop repeats its cost
         _, c = dal_cost(p, d, eps, I, v, mu, return_state=True)
         v = shrink_field(p, q.rho, c, mu)
-        mu = mu + q.gamma * (v - grad(c, q.hx, q.hy))
-    return eps, np.array(Jh), c, v, mu
+        g = v - grad(c, q.hx, q.hy)
+        step = q.gamma
+        if gamma_search:
+            phi0 = energy_L(p, q.rho, c, v, mu, I)
+            g2 = w * float(np.sum(g * g))
+
+            def passes(t):
+                mt = mu + t * g
+                et, _, _ = dal(p, d, eps, I, v, mt)
+                _, ct = dal_cost(p, d, et, I, v, mt, return_state=True)
+                return dual_value(p, q.rho, ct, mt, I) >= phi0 + d.c * t * g2
+
+            tau, acc, evals = gam, -1.0, 1
+            if passes(tau):
+                acc = tau
+                while evals < d.max_ls:
+                    evals += 1
+                    if not passes(tau / d.b):
+                        break
+                    tau /= d.b
+                    acc = tau
+            else:
+                while evals < d.max_ls:
+                    evals += 1
+                    tau *= d.b
+                    if passes(tau):
+                        acc = tau
+                        break
+            step = acc if acc > 0 else 0.0
+            gam = acc if acc > 0 else tau
+        gh.append(step)
+        mu = mu + step * g
+    out = (eps, np.array(Jh), c, v, mu)
+    return out + (np.array(gh),) if gamma_search else out
 
 
 def dal_gradient(p: Params, d: DalParams, eps, I, v=None, mu=None):
@@ -376,13 +427,18 @@ def dal_gradient(p: Params, d: DalParams, eps, I, v=None, mu=None):
     return J, g
 
 
-def dal(p: Params, d: DalParams, eps, I, v=None, mu=None):
-    """Algorithm 1 from eps ([M][2], updated copy returned) -> (eps, J_hist[iters+1], sigma_hist[iters])."""
+def dal(p: Params, d: DalParams, eps, I, v=None, mu=None, return_stop: bool = False):
+    """Algorithm 1 from eps ([M][2], updated copy returned) -> (eps, J_hist, sigma_hist[, stop]).
+    With the Remark 3.4 rules (d.eta, d.eta_grad) the run may end early: J_hist then has run + 1
+    entries and sigma_hist run; stop = (iterations run, 0 cap | 1 cost stationarity | 2 gradient)."""
     eps = _f64(eps).copy()
     I = _f64(I)
     v, mu = _vmu(p, v, mu)
     Jh = np.zeros(d.iters + 1)
     sh = np.zeros(max(d.iters, 1))
+    stop = np.zeros(2, dtype=np.int32)
     _load().mo_dal(ctypes.byref(p.c()), ctypes.byref(d.c_struct()), _ptr(eps), _ptr(I), _ptr(v), _ptr(mu), _ptr(Jh),
-                   _ptr(sh))
-    return eps, Jh, sh[:d.iters]
+                   _ptr(sh), _ptr(stop))
+    run = int(stop[0])
+    out = (eps, Jh[:run + 1], sh[:run])
+    return out + ((run, int(stop[1])),) if return_stop else out

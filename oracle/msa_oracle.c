@@ -783,17 +783,36 @@ static int armijo_ok(const mo_params* prm, const mo_dal_params* d, const double*
   return mo_dal_cost(prm, d, cand, I, v, mu, NULL) <= J0 - d->c * t * D2;
 }
 
+/* Remark 3.4's projected gradient: D_i, or 0 where eps_i sits on the box and -D_i points outward */
+static double proj_grad_max(const mo_dal_params* d, const double* eps, const double* D, int M) {
+  double mx = 0.0;
+  for (int m = 0; m < M; ++m)
+    for (int i = 0; i < 2; ++i) {
+      const double lo = i == 0 ? d->ex_lo : d->ec_lo, hi = i == 0 ? d->ex_hi : d->ec_hi;
+      const double e = eps[2 * m + i], g = D[2 * m + i];
+      const int inactive = (e <= lo && g >= 0.0) || (e >= hi && g <= 0.0);
+      const double a = inactive ? 0.0 : fabs(g);
+      if (a > mx) mx = a;
+    }
+  return mx;
+}
+
 int mo_dal(const mo_params* prm_in, const mo_dal_params* d, double* eps, const double* I, const double* v,
-           const double* mu, double* J_hist, double* sigma_hist) {
+           const double* mu, double* J_hist, double* sigma_hist, int32_t* stop) {
   const int M = d->M;
   double* D = (double*)malloc(2 * (size_t)M * sizeof(double));
   double* cand = (double*)malloc(2 * (size_t)M * sizeof(double));
   double sigma = d->sigma0;
-  int taken = 0;
+  int taken = 0, run = d->iters, why = 0;
+  double J_prev = 0.0;
   project_E(d, eps, M);
   for (int it = 0; it < d->iters; ++it) {
     const double J0 = mo_dal_gradient(prm_in, d, eps, I, v, mu, D);
     if (J_hist) J_hist[it] = J0;
+    /* UNTIL convergence (Remark 3.4) */
+    if (it > 0 && d->eta > 0.0 && fabs(J0 - J_prev) / J_prev < d->eta) { run = it; why = 1; break; }
+    if (d->eta_grad > 0.0 && proj_grad_max(d, eps, D, M) < d->eta_grad) { run = it; why = 2; break; }
+    J_prev = J0;
     double D2 = 0.0;
     for (int m = 0; m < 2 * M; ++m) D2 += D[m] * D[m];
     double tau = sigma, acc_tau = -1.0;
@@ -826,7 +845,8 @@ int mo_dal(const mo_params* prm_in, const mo_dal_params* d, double* eps, const d
       sigma = tau;  /* no admissible step within the cap: start the next search from the smallest tried */
     }
   }
-  if (J_hist) J_hist[d->iters] = mo_dal_cost(prm_in, d, eps, I, v, mu, NULL);
+  if (J_hist) J_hist[run] = mo_dal_cost(prm_in, d, eps, I, v, mu, NULL);
+  if (stop) { stop[0] = run; stop[1] = why; }
   free(D); free(cand);
   return taken;
 }

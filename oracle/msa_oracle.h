@@ -88,6 +88,13 @@ typedef struct {
   double b, c;        /* Armijo factors b, c in (0,1) */
   double ex_lo, ex_hi, ec_lo, ec_hi; /* box E ([2,1100]^2) */
   double rho;         /* L~ penalty (cost 1) */
+  /* Remark 3.4 stopping rules, checked at the top of iteration j >= 1 once
+   * J(eps^(j)) and D^(j) are known; <= 0 disables a rule (then `iters` iterations run):
+   *   eta:      |J(eps^(j)) - J(eps^(j-1))| / J(eps^(j-1)) < eta  (the paper's choice, eta = 1e-10 at :270)
+   *   eta_grad: max |projected D| < eta_grad, where a component of D counts as 0 on the lower contact
+   *             set {eps_i = min} if D_i >= 0 and on the upper one {eps_i = max} if D_i <= 0 (the
+   *             variational inequalities of the constrained case; descent along -D, reading R25). */
+  double eta, eta_grad;
 } mo_dal_params;
 
 double mo_phi_prime(double r, int kernel);
@@ -99,8 +106,10 @@ double mo_dal_cost(const mo_params* prm, const mo_dal_params* d, const double* e
                    const double* mu, double* cT);
 double mo_dal_gradient(const mo_params* prm, const mo_dal_params* d, const double* eps, const double* I,
                        const double* v, const double* mu, double* grad);
+/* stop (may be NULL): stop[0] = iterations run, stop[1] = 0 (iteration cap), 1 (cost stationarity),
+ * 2 (projected gradient). J_hist[0 .. stop[0]] and sigma_hist[0 .. stop[0]) are written. */
 int mo_dal(const mo_params* prm, const mo_dal_params* d, double* eps, const double* I, const double* v,
-           const double* mu, double* J_hist, double* sigma_hist);
+           const double* mu, double* J_hist, double* sigma_hist, int32_t* stop);
 
 #ifdef __cplusplus
 }

@@ -43,7 +43,8 @@ class _DalParams(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_int32), ("cost", ctypes.c_int32), ("iters", ctypes.c_int32),
                 ("max_ls", ctypes.c_int32), ("sigma0", ctypes.c_double), ("b", ctypes.c_double),
                 ("c", ctypes.c_double), ("ex_lo", ctypes.c_double), ("ex_hi", ctypes.c_double),
-                ("ec_lo", ctypes.c_double), ("ec_hi", ctypes.c_double)]
+                ("ec_lo", ctypes.c_double), ("ec_hi", ctypes.c_double), ("eta", ctypes.c_double),
+                ("eta_grad", ctypes.c_double), ("gamma_ls", ctypes.c_int32), ("reserved_", ctypes.c_int32)]
 
 
 @dataclass
@@ -60,9 +61,12 @@ class DalParams:
     ex_hi: float = 1100.0
     ec_lo: float = 2.0
     ec_hi: float = 1100.0
+    eta: float = 0.0       # Remark 3.4 cost stationarity (1e-10); 0: run `iters` iterations
+    eta_grad: float = 0.0  # Remark 3.4 projected-gradient tolerance; 0: off
+    gamma_ls: int = 0      # dal_admm: two-way Armijo search for the ascent step (remark after Alg. 2)
 
     def c_struct(self) -> "_DalParams":
-        return _DalParams(**asdict(self))
+        return _DalParams(**asdict(self), reserved_=0)
 
 
 class _CParams(ctypes.Structure):
@@ -95,7 +99,8 @@ class Info(ctypes.Structure):
                 ("hx", ctypes.c_double), ("hy", ctypes.c_double), ("eps_x", ctypes.c_double),
                 ("tau", ctypes.c_double), ("sigma", ctypes.c_double), ("theta", ctypes.c_double),
                 ("window_size", ctypes.c_int32), ("active_offsets", ctypes.c_int32),
-                ("iters_done", ctypes.c_int64), ("launches", ctypes.c_int64), ("rho", ctypes.c_double)]
+                ("iters_done", ctypes.c_int64), ("launches", ctypes.c_int64), ("rho", ctypes.c_double),
+                ("halo_exchanges", ctypes.c_int64), ("halo_ms", ctypes.c_double)]
 
 
 @dataclass
@@ -188,9 +193,9 @@ def lib():
             "msa_set_timing": ([P, ctypes.c_int], ctypes.c_int),
             "msa_get_timing": ([P, PD, PI64, PD, PI64], ctypes.c_int),
             "msa_sync": ([P], ctypes.c_int),
-            "msa_dal": ([P, ctypes.POINTER(_DalParams), P, P, P, P, P], ctypes.c_int),
+            "msa_dal": ([P, ctypes.POINTER(_DalParams), P, P, P, P, P, P], ctypes.c_int),
             "msa_dal_gradient": ([P, ctypes.POINTER(_DalParams), P, P, P, P, P], ctypes.c_int),
-            "msa_dal_admm": ([P, ctypes.POINTER(_DalParams), P, P, P, I32, P, P], ctypes.c_int),
+            "msa_dal_admm": ([P, ctypes.POINTER(_DalParams), P, P, P, I32, P, P, P], ctypes.c_int),
             "msa_free": ([P], ctypes.c_int),
         }
         for name, (args, res) in sig.items():
@@ -247,11 +252,13 @@ def _torch():
     return torch
 
 
-def _ptr_of(x, n: int | None = None, what: str = "buffer", out: bool = False, dtype=np.float32):
+def _ptr_of(x, n: int | None = None, what: str = "buffer", out: bool = False, dtype=np.float32,
+            device: int | None = None):
     """(pointer, on_device, keepalive) of a numpy array or a torch tensor of n elements of dtype.
     Inputs are converted (numpy) or made contiguous (torch); outputs must already be contiguous
     and of the right dtype, since the library writes into them. Sizes are checked: the library
-    trusts them."""
+    trusts them. A CUDA tensor must live on the context's device (params.device): the library's
+    kernels and copies run there."""
     if isinstance(x, np.ndarray):
         if out:
             if x.dtype != dtype or not x.flags.c_contiguous or not x.flags.writeable:
@@ -272,6 +279,8 @@ def _ptr_of(x, n: int | None = None, what: str = "buffer", out: bool = False, dt
             x = x.contiguous()
         if n is not None and x.numel() != n:
             raise ValueError(f"{what}: expected {n} elements, got {x.numel()} (shape {tuple(x.shape)})")
+        if x.is_cuda and device is not None and x.device.index != device:
+            raise ValueError(f"{what}: tensor is on cuda:{x.device.index}, the context runs on cuda:{device}")
         return x.data_ptr(), int(x.is_cuda), x
     raise TypeError(f"{what}: unsupported buffer type {type(x)}")
 
@@ -299,7 +308,8 @@ class Solver:
             stream = torch.cuda.current_stream(dev)
         self._stream = stream
         sptr = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream or 0)
-        ptr, on_dev, keep = _ptr_of(image, params.batch * params.height * params.width * params.channels, "image")
+        ptr, on_dev, keep = _ptr_of(image, params.batch * params.height * params.width * params.channels, "image",
+                                     device=params.device)
         ctx = ctypes.c_void_p()
         _check(L.msa_init(ctypes.byref(cp), ptr, on_dev, ws_ptr, nbytes, sptr or None, ctypes.byref(ctx)))
         self._ctx = ctx
@@ -325,7 +335,7 @@ class Solver:
     # -- hot path
     def reset(self, image) -> None:
         p = self.params
-        ptr, on_dev, keep = _ptr_of(image, p.batch * p.height * p.width * p.channels, "image")
+        ptr, on_dev, keep = _ptr_of(image, p.batch * p.height * p.width * p.channels, "image", device=p.device)
         _check(lib().msa_reset(self._ctx, ptr, on_dev))
         if not on_dev:
             self.sync()
@@ -365,7 +375,7 @@ class Solver:
                                (pal, nb * max_k * C, np.float32, "palette")):
             if t is None:
                 continue
-            ptr, on_dev, _ = _ptr_of(t, n, what, out=True, dtype=dt)
+            ptr, on_dev, _ = _ptr_of(t, n, what, out=True, dtype=dt, device=self.params.device)
             if not on_dev:
                 raise TypeError(f"{what}: out= takes CUDA tensors (device outputs)")
         if max_k > 0 and pal is None:
@@ -383,7 +393,8 @@ class Solver:
             out = np.empty((info.nimages, info.nrows, self.params.width, nm), dtype=np.float32)
             _check(lib().msa_get_field(self._ctx, which, out.ctypes.data, 0, None, None))
             return out
-        ptr, on_dev, keep = _ptr_of(out, info.nimages * info.nrows * self.params.width * nm, "out", out=True)
+        ptr, on_dev, keep = _ptr_of(out, info.nimages * info.nrows * self.params.width * nm, "out", out=True,
+                                     device=self.params.device)
         _check(lib().msa_get_field(self._ctx, which, ptr, on_dev, None, None))
         return out
 
@@ -391,7 +402,8 @@ class Solver:
         info = self.query()
         C = self.params.channels
         nm = 2 * C if which in (FIELD_P, FIELD_MU) else C
-        ptr, on_dev, keep = _ptr_of(arr, info.nimages * info.nrows * self.params.width * nm, "field")
+        ptr, on_dev, keep = _ptr_of(arr, info.nimages * info.nrows * self.params.width * nm, "field",
+                                     device=self.params.device)
         _check(lib().msa_set_field(self._ctx, which, ptr, on_dev))
 
     def stats(self) -> list[dict]:
@@ -439,35 +451,43 @@ class Solver:
             if a is None:
                 out.append(None)
             else:
-                ptr, on_dev, k = _ptr_of(a, n, what)
+                ptr, on_dev, k = _ptr_of(a, n, what, device=self.params.device)
                 if on_dev:
                     raise TypeError(f"{what}: host array expected")
                 keep.append(k)
                 out.append(ptr)
         return out, keep
 
-    def dal(self, d: "DalParams", eps, v=None, mu=None):
-        """Optimises eps ([steps][2]) from the given guess; returns (eps, J_hist, sigma_hist)."""
+    def dal(self, d: "DalParams", eps, v=None, mu=None, return_stop: bool = False):
+        """Optimises eps ([steps][2]) from the given guess; returns (eps, J_hist, sigma_hist[, stop]). With
+        d.eta / d.eta_grad (Remark 3.4) the run may stop early: J_hist has run + 1 entries, sigma_hist run,
+        stop = (iterations run, 0 cap | 1 cost stationarity | 2 projected gradient)."""
         e = np.ascontiguousarray(eps, dtype=np.float64).copy()
         assert e.shape == (d.steps, 2)
         Jh = np.zeros(d.iters + 1)
         sh = np.zeros(max(d.iters, 1))
+        stop = np.zeros(2, dtype=np.int32)
         (vp, mp), keep = self._vmu(v, mu)
         _check(lib().msa_dal(self._ctx, ctypes.byref(d.c_struct()), e.ctypes.data, vp, mp, Jh.ctypes.data,
-                             sh.ctypes.data))
-        return e, Jh, sh[:d.iters]
+                             sh.ctypes.data, stop.ctypes.data))
+        run = int(stop[0])
+        out = (e, Jh[:run + 1], sh[:run])
+        return out + ((run, int(stop[1])),) if return_stop else out
 
-    def dal_admm(self, d: "DalParams", eps, outer: int, v=None, mu=None):
+    def dal_admm(self, d: "DalParams", eps, outer: int, v=None, mu=None, return_gamma: bool = False):
         """Algorithm 2 with DAL as line 5 (d.cost must be 1): returns (eps, J_hist [outer][iters+1],
-        records [outer]); the final mu is FIELD_MU."""
+        records [outer][, gamma_hist [outer]]); the final mu is FIELD_MU. d.gamma_ls = 1 chooses each
+        ascent step by the two-way Armijo search (the remark after Algorithm 2)."""
         e = np.ascontiguousarray(eps, dtype=np.float64).copy()
         assert e.shape == (d.steps, 2)
         Jh = np.zeros((max(outer, 1), d.iters + 1))
+        gh = np.zeros(max(outer, 1))
         buf = (RoundStats * max(outer, 1))()
         (vp, mp), keep = self._vmu(v, mu)
         _check(lib().msa_dal_admm(self._ctx, ctypes.byref(d.c_struct()), e.ctypes.data, vp, mp, int(outer),
-                                  Jh.ctypes.data, buf))
-        return e, Jh[:outer], [buf[r].as_dict(self.params.channels) for r in range(outer)]
+                                  Jh.ctypes.data, buf, gh.ctypes.data))
+        out = (e, Jh[:outer], [buf[r].as_dict(self.params.channels) for r in range(outer)])
+        return out + (gh[:outer],) if return_gamma else out
 
     def dal_gradient(self, d: "DalParams", eps, v=None, mu=None):
         e = np.ascontiguousarray(eps, dtype=np.float64)

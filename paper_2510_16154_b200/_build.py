@@ -11,8 +11,13 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "build")
 LIB = os.path.join(PKG, "libmsa.so")
-SOURCES = ["msa_driver.cu", "msa_kernels.cu", "msa_iter_fast.cu", "msa_iter_sweep.cu", "msa_iter_cn.cu", "msa_agent_large.cu", "msa_dal.cu", "msa_labels.cu",
-           "msa_nccl_loopback.cu"]
+# the testing library: the same sources with -DMSA_TESTING (environment test hooks) plus
+# the experimental pair-symmetric sweep K1 and the in-process NCCL transport; tests and tools load it
+# through MSA_LIB. The product library never reads the environment.
+TEST_LIB = os.path.join(PKG, "libmsa_testing.so")
+SOURCES = ["msa_driver.cu", "msa_kernels.cu", "msa_iter_fast.cu", "msa_iter_cn.cu", "msa_agent_large.cu", "msa_dal.cu",
+           "msa_labels.cu"]
+TEST_SOURCES = SOURCES + ["msa_iter_sweep.cu", "msa_nccl_loopback.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
@@ -25,17 +30,25 @@ def _deps() -> list[str]:
     return fs
 
 
-def needs_build() -> bool:
-    if not os.path.exists(LIB):
+def needs_build(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(f) > t for f in _deps())
 
 
 def build(force: bool = False, verbose: bool = False, defines: tuple = (), lib: str = LIB, build_dir: str = BUILD,
-          flags: tuple = ()) -> str:
-    if not force and lib == LIB and not needs_build():
-        return LIB
+          flags: tuple = (), testing: bool = True) -> str:
+    """Builds libmsa.so (and, with testing=True, libmsa_testing.so); returns the product path."""
+    if lib == LIB and testing:
+        _build_one(force, verbose, ("MSA_TESTING",) + tuple(defines), TEST_LIB, BUILD + "_testing", flags,
+                   TEST_SOURCES)
+    return _build_one(force, verbose, defines, lib, build_dir, flags, SOURCES if lib == LIB else TEST_SOURCES)
+
+
+def _build_one(force, verbose, defines, lib, build_dir, flags, sources) -> str:
+    if not force and lib in (LIB, TEST_LIB) and not needs_build(lib):
+        return lib
     os.makedirs(build_dir, exist_ok=True)
     extra = (["-Xptxas", "-v"] if verbose else []) + [f"-D{d}" for d in defines] + list(flags)
 
@@ -49,8 +62,8 @@ def build(force: bool = False, verbose: bool = False, defines: tuple = (), lib: 
             sys.stderr.write(r.stderr)
         return obj
 
-    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        objs = list(ex.map(compile_one, SOURCES))
+    with ThreadPoolExecutor(max_workers=len(sources)) as ex:
+        objs = list(ex.map(compile_one, sources))
     tmp = lib + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
     r = subprocess.run(cmd, capture_output=True, text=True)

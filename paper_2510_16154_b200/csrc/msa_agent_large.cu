@@ -1,5 +1,6 @@
 // msa_agent_large.cu - step 1 (the agent Euler step) for large interaction supports, C <= 4,
-// 8 < R <= 64. sm_100a.
+// 6 <= R <= 255 in the solver's K1 (beyond the tiled kernel's R <= 5) and R > 8 in the DAL sweeps
+// (whose per-pixel kernels cover R <= 8). sm_100a.
 //
 // The paper's control box E = [2, 1100]^2 gives supports from a few pixels up to
 // the whole image; the window D_R then holds hundreds to thousands of offsets and step 1 is an
@@ -197,7 +198,7 @@ cudaError_t launch_c(const MsaGeom& g, const MsaIterConsts& K, int R, const floa
   if (tiles8 >= 2LL * sms) return launch_th<C, TH>(g, K, R, omtab, exh_x, exh_y, c, ch, s, nr, Split{1, nullptr});
   // still under eight 64-thread CTAs per SM: split the window (at most 4 parts, as the scratch
   // allows, and no more parts than row chunks)
-  static const bool nosplit = getenv("MSA_LARGE_NOSPLIT") != nullptr;  // test hook: the NS = 1 order
+  static const bool nosplit = MSA_HOOK("MSA_LARGE_NOSPLIT") != nullptr;  // test hook: the NS = 1 order
   const long long tiles2 = (long long)((g.W + TW - 1) / TW) * ((nr + 1) / 2) * g.nb;
   const size_t per_part = (size_t)g.nb * C * g.plane;
   int NS = (int)std::min<long long>(4, (8LL * sms + tiles2 - 1) / tiles2);
@@ -421,7 +422,7 @@ cudaError_t dal_back_c(const MsaGeom& g, int R, int kernel, float exh_x, float e
     return cudaGetLastError();
   }
   // small image: 32 x 2 tiles and the window's row chunks split over NS CTAs (as the scratch allows)
-  static const bool nosplit = getenv("MSA_LARGE_NOSPLIT") != nullptr;  // test hook: the NS = 1 order
+  static const bool nosplit = MSA_HOOK("MSA_LARGE_NOSPLIT") != nullptr;  // test hook: the NS = 1 order
   const long long tiles2 = (long long)nx * ((g.H + 1) / 2);
   int NS = (int)std::min<long long>(4, (8LL * sms + tiles2 - 1) / tiles2);
   const int CR = cr_for(R, TW, 2, 2, 160 * 1024);

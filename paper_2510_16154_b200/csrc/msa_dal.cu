@@ -268,7 +268,7 @@ static DalConsts make_consts(const MsaDalConstsHost& h, double eps_x, double eps
   }
 
 static bool dal_large(int R, int C) {
-  static const bool force_generic = getenv("MSA_DAL_GENERIC") != nullptr;  // A/B and test hook
+  static const bool force_generic = MSA_HOOK("MSA_DAL_GENERIC") != nullptr;  // A/B and test hook
   return R > 8 && C <= 4 && !force_generic;
 }
 

@@ -39,6 +39,7 @@ static int set_err(int code, const char* fmt, ...) {
 namespace {
 struct NcclApi : MsaNcclFns {
   bool tried = false, ok = false;
+  bool loopback = false;  // the testing build's in-process transport (host rendezvous: not capturable)
 };
 NcclApi g_nccl;
 
@@ -47,11 +48,14 @@ bool nccl_load() {
   std::lock_guard<std::mutex> lock(mu);
   if (g_nccl.tried) return g_nccl.ok;
   g_nccl.tried = true;
-  if (getenv("MSA_NCCL_LOOPBACK")) {  // test hook: in-process ranks (msa_nccl_loopback.cu)
+#ifdef MSA_TESTING
+  if (MSA_HOOK("MSA_NCCL_LOOPBACK")) {  // test hook: in-process ranks (msa_nccl_loopback.cu, testing build only)
     static_cast<MsaNcclFns&>(g_nccl) = msa_nccl_loopback();
     g_nccl.ok = true;
+    g_nccl.loopback = true;
     return true;
   }
+#endif
   // prefer the NCCL already mapped into the process (torch's), else the system one
   void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
   if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -114,7 +118,7 @@ struct msa_ctx {
   bool timing = false, in_iter_batch = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> iter_ev, round_ev;
   int64_t iter_launches_t = 0, round_launches_t = 0;
-  float* d_omtab = nullptr;  // 1 - a_delta for every (dx, dy) of the window, large supports (R > 8)
+  float* d_omtab = nullptr;  // 1 - a_delta for every (dx, dy) of the window: large-support K1 (R >= 6), DAL (R > 8)
   // nccl
   ncclComm_t comm = nullptr;
   // rows mode: halo exchange on its own stream, overlapped with the interior K1 launch (§8(e))
@@ -124,6 +128,23 @@ struct msa_ctx {
   // interior launch's tail (one slab-edge tile row each: too small to fill the GPU alone)
   cudaStream_t bnd_stream = nullptr;
   cudaEvent_t ev_bnd = nullptr;
+  // packed halo exchange: per (phase, ping-pong set) the plan's row runs as gather / scatter
+  // descriptor tables (device), one staging buffer [send lo | send hi | recv lo | recv hi]
+  struct HaloPack {
+    bool built = false;
+    int peer[2] = {-1, -1};              // neighbour below / above
+    long long n_send[2] = {0, 0}, n_recv[2] = {0, 0};
+    long long off_send[2] = {0, 0}, off_recv[2] = {0, 0};
+    MsaHaloSeg* d_seg = nullptr;         // send segments, then receive segments
+    int n_sseg = 0, n_rseg = 0;
+    long long max_n = 0;
+  };
+  HaloPack halo[3][2];
+  float* halo_buf = nullptr;
+  long long halo_buf_floats = 0;
+  // halo timing (msa_info::halo_ms with msa_set_timing on): events around each exchange
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> halo_ev;
+  int64_t halo_exchanges_t = 0;
   // labels
   MsaLabelScratch* lab = nullptr;
   int32_t* lab_buf = nullptr;
@@ -136,6 +157,7 @@ struct msa_ctx {
     cudaGraphExec_t exec = nullptr;
     int cur0 = 0, cur1 = 0;
     double rho0 = 0, rho1 = 0;
+    bool mu_dirty0 = true, mu_dirty1 = true;  // rows mode: mu ghost row stale at the start / end
     int64_t phase = 0, iters_base = 0, launches_delta = 0;
     int32_t rounds_base = 0;
   } graphs[2];
@@ -196,7 +218,7 @@ struct Derived {
 // Scaled step-1 form (msa_common.cuh MsaIterConsts::scaled) for e_c = eps_c/2 in [1e-3, 1e3];
 // MSA_NO_SCALED=1 (test hook) keeps the direct form (then only the generic kernels run).
 bool use_scaled(double eps_c) {
-  static const bool off = getenv("MSA_NO_SCALED") != nullptr;
+  static const bool off = MSA_HOOK("MSA_NO_SCALED") != nullptr;
   const double e_c = 0.5 * eps_c;
   return !off && e_c >= 1e-3 && e_c <= 1e3;
 }
@@ -299,7 +321,7 @@ Layout layout(const msa_params* p, const Part& pt) {
   const size_t nwin = (size_t)(2 * p->radius + 1) * (2 * p->radius + 1);  // offsets of the window
   L.off_off = o;      o += align_up(nwin * sizeof(int2), 256);
   L.off_om = o;       o += align_up(nwin * sizeof(float), 256);
-  L.off_omtab = o;    o += align_up(nwin * sizeof(float), 256);  // [2R+1]^2 table (R > 8)
+  L.off_omtab = o;    o += align_up(nwin * sizeof(float), 256);  // [2R+1]^2 table (K1 R >= 6, DAL R > 8)
   L.off_rec = o;      o += align_up(REC_CAP * sizeof(msa_round_stats), 256);
   L.total = o;
   return L;
@@ -428,33 +450,120 @@ int halo_plan(int H, int world, int rank, int R, int phase, std::vector<msa_halo
   return MSA_OK;
 }
 
-// --- halo exchange of the current state (rows mode, world > 1): the plan's ops as one NCCL group
-int halo_exchange(msa_ctx* x, int phase, cudaStream_t st = nullptr) {
-  if (!st) st = x->stream;
+// --- halo exchange of the current state (rows mode, world > 1). The plan's ops are grouped per
+// neighbour and direction: one gather kernel packs every row run to send (all fields, component
+// planes and images) into a staging buffer, one grouped ncclSend / ncclRecv per neighbour moves it,
+// one scatter kernel unpacks what arrived into the ghost rows. Per iteration of 4096^2 RGB at R = 5
+// that is 2 NCCL p2p calls per neighbour instead of one per plane and field (24 for RGB).
+int build_halo_pack(msa_ctx* x, int phase, int s, msa_ctx::HaloPack* hp) {
   const msa_params& P = x->prm;
-  if (!(P.world > 1 && P.shard == MSA_SHARD_ROWS)) return MSA_OK;
+  const MsaGeom& g = x->g;
   std::vector<msa_halo_op> ops;
   int rc = halo_plan(P.height, P.world, P.rank, P.radius, phase, &ops);
   if (rc != MSA_OK) return rc;
-  const MsaGeom& g = x->g;
-  const int C = P.channels;
-  const int s = x->cur;
-  NCCL_TRY(g_nccl.GroupStart());
+  const int lo = P.rank - 1, hi = P.rank + 1;
+  hp->peer[0] = lo >= 0 ? lo : -1;
+  hp->peer[1] = hi < P.world ? hi : -1;
+  std::vector<MsaHaloSeg> seg[2][2];  // [send/recv][lo/hi]
+  long long n[2][2] = {{0, 0}, {0, 0}};
   for (const msa_halo_op& op : ops) {
+    const int dir = op.peer == lo ? 0 : 1, sr = op.send ? 0 : 1;
     float* f = field_ptr(x, op.field, s);
     const int nm = field_nm(x, op.field);
     for (int b = 0; b < g.nb; ++b)
       for (int m = 0; m < nm; ++m) {
-        float* rows = f + ((size_t)b * nm + m) * g.plane + (size_t)(op.row0 - g.row0 + g.G) * g.pitch;
-        const size_t n = (size_t)op.nrows * g.pitch;
-        if (op.send)
-          NCCL_TRY(g_nccl.Send(rows, n, ncclFloat, op.peer, x->comm, st));
-        else
-          NCCL_TRY(g_nccl.Recv(rows, n, ncclFloat, op.peer, x->comm, st));
+        MsaHaloSeg q;
+        q.ptr = f + ((size_t)b * nm + m) * g.plane + (size_t)(op.row0 - g.row0 + g.G) * g.pitch;
+        q.n = (long long)op.nrows * g.pitch;
+        q.off = n[sr][dir];
+        n[sr][dir] += q.n;
+        hp->max_n = std::max(hp->max_n, q.n);
+        seg[sr][dir].push_back(q);
       }
   }
+  // staging layout: send lo, send hi, recv lo, recv hi
+  hp->off_send[0] = 0;
+  hp->off_send[1] = n[0][0];
+  hp->off_recv[0] = n[0][0] + n[0][1];
+  hp->off_recv[1] = hp->off_recv[0] + n[1][0];
+  const long long total = hp->off_recv[1] + n[1][1];
+  std::vector<MsaHaloSeg> all;
+  for (int sr = 0; sr < 2; ++sr)
+    for (int dir = 0; dir < 2; ++dir)
+      for (MsaHaloSeg q : seg[sr][dir]) {
+        q.off += sr == 0 ? hp->off_send[dir] : hp->off_recv[dir];
+        all.push_back(q);
+      }
+  for (int dir = 0; dir < 2; ++dir) {
+    hp->n_send[dir] = n[0][dir];
+    hp->n_recv[dir] = n[1][dir];
+  }
+  hp->n_sseg = (int)(seg[0][0].size() + seg[0][1].size());
+  hp->n_rseg = (int)(seg[1][0].size() + seg[1][1].size());
+  if (total > x->halo_buf_floats) {  // grow the staging buffer (first use of a larger phase)
+    CUDA_TRY(cudaDeviceSynchronize());  // an earlier exchange may still read the old buffer
+    if (x->halo_buf) CUDA_TRY(cudaFree(x->halo_buf));
+    x->halo_buf = nullptr;
+    CUDA_TRY(cudaMalloc((void**)&x->halo_buf, sizeof(float) * std::max<long long>(total, 4)));
+    x->halo_buf_floats = total;
+  }
+  if (!all.empty()) {
+    CUDA_TRY(cudaMalloc((void**)&hp->d_seg, sizeof(MsaHaloSeg) * all.size()));
+    CUDA_TRY(cudaMemcpy(hp->d_seg, all.data(), sizeof(MsaHaloSeg) * all.size(), cudaMemcpyHostToDevice));
+  }
+  hp->built = true;
+  return MSA_OK;
+}
+
+// the descriptor tables of every phase and set, built before the first exchange (so no allocation
+// or host copy happens while a solve is being captured into a graph)
+int build_halo_packs(msa_ctx* x) {
+  const int phases[3] = {MSA_HALO_ITER, MSA_HALO_ROUND, MSA_HALO_MU};
+  for (int ph = 0; ph < 3; ++ph)
+    for (int s = 0; s < 2; ++s)
+      if (!x->halo[ph][s].built) {
+        int rc = build_halo_pack(x, phases[ph], s, &x->halo[ph][s]);
+        if (rc != MSA_OK) return rc;
+      }
+  return MSA_OK;
+}
+
+int halo_exchange(msa_ctx* x, int phase, cudaStream_t st = nullptr) {
+  if (!st) st = x->stream;
+  const msa_params& P = x->prm;
+  if (!(P.world > 1 && P.shard == MSA_SHARD_ROWS)) return MSA_OK;
+  if (phase != MSA_HALO_ITER && phase != MSA_HALO_ROUND && phase != MSA_HALO_MU)
+    return set_err(MSA_EINVAL, "bad halo phase %d", phase);
+  int rc;
+  if ((rc = build_halo_packs(x)) != MSA_OK) return rc;
+  const int ph = phase == MSA_HALO_ITER ? 0 : (phase == MSA_HALO_ROUND ? 1 : 2);
+  msa_ctx::HaloPack& hp = x->halo[ph][x->cur];
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (x->timing) {
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    CUDA_TRY(cudaEventRecord(e0, st));
+  }
+  CUDA_TRY(msa_launch_halo_pack(hp.d_seg, hp.n_sseg, hp.max_n, x->halo_buf, 1, st));
+  if (hp.n_sseg) ++x->launches;
+  NCCL_TRY(g_nccl.GroupStart());
+  for (int dir = 0; dir < 2; ++dir) {
+    if (hp.peer[dir] < 0) continue;
+    if (hp.n_send[dir])
+      NCCL_TRY(g_nccl.Send(x->halo_buf + hp.off_send[dir], (size_t)hp.n_send[dir], ncclFloat, hp.peer[dir], x->comm,
+                           st));
+    if (hp.n_recv[dir])
+      NCCL_TRY(g_nccl.Recv(x->halo_buf + hp.off_recv[dir], (size_t)hp.n_recv[dir], ncclFloat, hp.peer[dir], x->comm,
+                           st));
+  }
   NCCL_TRY(g_nccl.GroupEnd());
-  (void)C;
+  CUDA_TRY(msa_launch_halo_pack(hp.d_seg + hp.n_sseg, hp.n_rseg, hp.max_n, x->halo_buf, 0, st));
+  if (hp.n_rseg) ++x->launches;
+  if (x->timing) {
+    CUDA_TRY(cudaEventRecord(e1, st));
+    x->halo_ev.emplace_back(e0, e1);
+    ++x->halo_exchanges_t;
+  }
   return MSA_OK;
 }
 
@@ -526,13 +635,19 @@ int do_round(msa_ctx* x) {
 enum { K1_SWEEP = 0, K1_TILE = 1, K1_GENERIC = 2 };
 int k1_variant() {
   static const int v = [] {
-    if (getenv("MSA_FORCE_GENERIC")) return (int)K1_GENERIC;
-    const char* e = getenv("MSA_K1");
+    if (MSA_HOOK("MSA_FORCE_GENERIC")) return (int)K1_GENERIC;
+    const char* e = MSA_HOOK("MSA_K1");
     if (!e || !strcmp(e, "tile")) return (int)K1_TILE;
     if (!strcmp(e, "sweep")) return (int)K1_SWEEP;
     return (int)K1_GENERIC;
   }();
   return v;
+}
+
+// Step 1 by the chunked large-support kernel (NEXT-3): radii beyond the tiled kernel's R <= 5, C <= 4
+bool uses_large_kernel(const msa_params& P) {
+  static const int large_from = MSA_HOOK("MSA_LARGE_FROM") ? atoi(MSA_HOOK("MSA_LARGE_FROM")) : 6;  // A/B hook
+  return P.radius >= large_from && P.radius > 5 && P.channels <= 4 && k1_variant() != K1_GENERIC;
 }
 
 // One K1 launch over the rows of geometry g (the whole slab, or an interior / boundary part):
@@ -541,8 +656,7 @@ int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int 
   const msa_params& P = x->prm;
   // large supports (NEXT-3): step 1 by the chunked n-body kernel into c[o], steps 2-3 generic
   // large supports (NEXT-3), and the radii between the tiled kernel's R <= 5 and 8 (C <= 4)
-  static const int large_from = getenv("MSA_LARGE_FROM") ? atoi(getenv("MSA_LARGE_FROM")) : 6;  // A/B hook
-  if (P.radius >= large_from && P.radius > 5 && P.channels <= 4 && k1_variant() != K1_GENERIC) {
+  if (uses_large_kernel(P)) {
     // scratch for a window split at small images: cb[o] and p[o] (3C planes, contiguous) are
     // written only after step 1
     int nl = 1;
@@ -578,11 +692,13 @@ int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int 
   }
   int launched = 0;
   cudaError_t e = cudaErrorNotSupported;
+#ifdef MSA_TESTING  // the pair-symmetric sweep K1 is experimental (slower; DESIGN.md §5 K1s): testing build only
   if (k1_variant() == K1_SWEEP)
     e = msa_launch_iter_sweep(g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
                               x->p[o], st, &launched);
   if (!launched && e != cudaErrorNotSupported && e != cudaSuccess)
     return set_err(MSA_ECUDA, "sweep iteration kernel: %s", cudaGetErrorString(e));
+#endif
   if (!launched && k1_variant() != K1_GENERIC)
     e = msa_launch_iter_fast(g, KC, x->T, P.radius, x->c[s], x->cb[s], x->p[s], x->mu, x->I, x->c[o], x->cb[o],
                              x->p[o], st, &launched);
@@ -600,14 +716,19 @@ int launch_k1(msa_ctx* x, const MsaGeom& g, const MsaIterConsts& KC, int s, int 
   return MSA_OK;
 }
 
-// Interior / boundary split of a slab: rows within SPLIT of either slab edge read ghost rows (or,
-// for the top edge, produce the rows the exchange sends), the rest do not. SPLIT = 32 is a
-// multiple of every K1 tile height, so the parts are whole tile rows.
+// Interior / boundary split of a slab. The interior launch covers rows [lo, hi) and runs while the
+// exchange writes the ghost rows, so it must read none: rows [lo, hi) read c in [lo - R, hi + R)
+// and cbar, p in [lo - 1, hi + 1), hence lo >= R + 1 and hi <= nrows - R - 1. The margin is
+// max(R + 1, SPLIT) rounded up to SPLIT = 32 (a multiple of every K1 tile height, so the parts are
+// whole tile rows). No split when the large-support kernels run: their window split keeps partial
+// sums in scratch planes that concurrent launches would share.
 constexpr int SPLIT = 32;
-bool split_rows(const MsaGeom& g, int* lo, int* hi) {
-  if (g.nrows < 3 * SPLIT) return false;
-  *lo = SPLIT;
-  *hi = SPLIT + (g.nrows - 2 * SPLIT) / SPLIT * SPLIT;
+bool split_rows(const MsaGeom& g, int R, bool large, int* lo, int* hi) {
+  if (large) return false;
+  const int m = (std::max(R + 1, SPLIT) + SPLIT - 1) / SPLIT * SPLIT;
+  if (g.nrows < 3 * m) return false;
+  *lo = m;
+  *hi = m + (g.nrows - 2 * m) / SPLIT * SPLIT;  // <= nrows - m
   return true;
 }
 
@@ -617,9 +738,10 @@ int do_steps(msa_ctx* x, int64_t n) {
   MsaIterConsts KC = iter_consts(x, x->rho_cur);
   const bool rows = P.world > 1 && P.shard == MSA_SHARD_ROWS;
   // test hook: MSA_K1_SPLIT=1 runs the interior / boundary launches on one GPU (no exchange)
-  static const bool force_split = getenv("MSA_K1_SPLIT") != nullptr;
+  static const bool force_split = MSA_HOOK("MSA_K1_SPLIT") != nullptr;
   int lo = 0, hi = 0;
-  const bool split = (rows && x->comm_stream) || force_split ? split_rows(x->g, &lo, &hi) : false;
+  const bool split =
+      (rows && x->comm_stream) || force_split ? split_rows(x->g, P.radius, uses_large_kernel(P), &lo, &hi) : false;
   if (split && !x->bnd_stream) {  // first split iteration: the boundary stream and its events
     CUDA_TRY(cudaStreamCreateWithFlags(&x->bnd_stream, cudaStreamNonBlocking));
     CUDA_TRY(cudaEventCreateWithFlags(&x->ev_bnd, cudaEventDisableTiming));
@@ -718,6 +840,11 @@ void free_ctx(msa_ctx* x) {
   if (x->bnd_stream) cudaStreamSynchronize(x->bnd_stream);
   if (x->bnd_stream) cudaStreamDestroy(x->bnd_stream);
   if (x->ev_bnd) cudaEventDestroy(x->ev_bnd);
+  for (auto& ph : x->halo)
+    for (auto& hp : ph)
+      if (hp.d_seg) cudaFree(hp.d_seg);
+  if (x->halo_buf) cudaFree(x->halo_buf);
+  for (auto& e : x->halo_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   msa_labels_free(x->lab);
   if (x->lab_buf) cudaFree(x->lab_buf);
   if (x->lab_count) cudaFree(x->lab_count);
@@ -734,13 +861,17 @@ void free_ctx(msa_ctx* x) {
 // in the round) is captured and instantiated, later ones replay it. Kernel arguments are
 // pointers into the context's fixed workspace and constants that depend only on that state,
 // except the round / iteration numbers baked into the record kernel, which msa_solve shifts
-// after the fetch. Not used in rows mode (NCCL calls and the comm stream), with timing on, or
-// with MSA_NO_GRAPH set; any capture failure falls back to direct launches for this context.
+// after the fetch. Rows mode is captured too: NCCL point-to-point and all-reduce calls are
+// stream-capturable, and the comm / boundary streams join the capture through the fork / join
+// events of do_steps (the halo descriptor tables are built before the capture starts). Not used
+// with timing on, over the testing build's in-process transport (host rendezvous), or with
+// MSA_NO_GRAPH set (testing build); any capture failure falls back to direct launches.
 bool graph_ok(const msa_ctx* x) {
-  static const bool off = getenv("MSA_NO_GRAPH") != nullptr;
+  static const bool off = MSA_HOOK("MSA_NO_GRAPH") != nullptr;
   const msa_params& P = x->prm;
-  return !off && !x->graphs_off && !x->timing && !(P.world > 1 && P.shard == MSA_SHARD_ROWS) &&
-         P.rounds <= REC_CAP && (int64_t)P.rounds * P.iters_per_round > 0;
+  const bool rows = P.world > 1 && P.shard == MSA_SHARD_ROWS;
+  return !off && !x->graphs_off && !x->timing && !(rows && g_nccl.loopback) && P.rounds <= REC_CAP &&
+         (int64_t)P.rounds * P.iters_per_round > 0;
 }
 
 // Runs one solve's steps through a (possibly new) graph. Returns MSA_OK with *done = false when
@@ -756,14 +887,17 @@ int solve_graph(msa_ctx* x, int64_t n, bool* done, int32_t* shift_round, int64_t
   msa_ctx::SolveGraph* G = nullptr;
   for (int i = 0; i < x->n_graphs; ++i) {
     msa_ctx::SolveGraph& c = x->graphs[i];
-    if (c.cur0 == x->cur && c.rho0 == x->rho_cur && c.phase == x->iters_done % K) G = &c;
+    if (c.cur0 == x->cur && c.rho0 == x->rho_cur && c.phase == x->iters_done % K && c.mu_dirty0 == x->halo_mu_dirty)
+      G = &c;
   }
+  if (!G && x->prm.world > 1 && x->prm.shard == MSA_SHARD_ROWS && (rc = build_halo_packs(x)) != MSA_OK) return rc;
   if (!G) {
     // capture: do_steps enqueues into the capturing stream and advances the host state
     const int cur0 = x->cur;
     const double rho0 = x->rho_cur;
     const int64_t it0 = x->iters_done, l0 = x->launches;
     const int32_t r0 = x->rounds_done;
+    const bool md0 = x->halo_mu_dirty;
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaError_t e = cudaStreamBeginCapture(x->stream, cudaStreamCaptureModeThreadLocal);
@@ -776,9 +910,11 @@ int solve_graph(msa_ctx* x, int64_t n, bool* done, int32_t* shift_round, int64_t
     }
     const int cur1 = x->cur;
     const double rho1 = x->rho_cur;
+    const bool md1 = x->halo_mu_dirty;
     const int64_t dl = x->launches - l0;
     // restore the host state either way; on success the replay below advances it again
     x->cur = cur0; x->rho_cur = rho0; x->iters_done = it0; x->launches = l0; x->rounds_done = r0;
+    x->halo_mu_dirty = md0;
     x->rec_pending = 0;
     if (e != cudaSuccess || rc != MSA_OK) {
       cudaGetLastError();
@@ -796,6 +932,8 @@ int solve_graph(msa_ctx* x, int64_t n, bool* done, int32_t* shift_round, int64_t
     c.cur1 = cur1;
     c.rho0 = rho0;
     c.rho1 = rho1;
+    c.mu_dirty0 = md0;
+    c.mu_dirty1 = md1;
     c.phase = it0 % K;
     c.iters_base = it0;
     c.rounds_base = r0;
@@ -812,7 +950,7 @@ int solve_graph(msa_ctx* x, int64_t n, bool* done, int32_t* shift_round, int64_t
   x->rounds_done += (int32_t)rounds;
   x->rec_pending += (int)rounds;
   x->launches += G->launches_delta;
-  if (rounds) x->halo_mu_dirty = true;
+  x->halo_mu_dirty = G->mu_dirty1;
   *done = true;
   return MSA_OK;
 }
@@ -959,7 +1097,7 @@ int msa_init(const msa_params* params, const float* image, int image_on_device, 
     memcpy(&id, params->nccl_id, sizeof(id));
     ncclResult_t r = g_nccl.CommInitRank(&x->comm, params->world, id, params->rank);
     if (r != ncclSuccess) return fail(set_err(MSA_ENCCL, "ncclCommInitRank: %s", g_nccl.GetErrorString(r)));
-    if (!getenv("MSA_NO_OVERLAP")) {  // A/B hook: serial exchange -> K1
+    if (!MSA_HOOK("MSA_NO_OVERLAP")) {  // A/B hook: serial exchange -> K1
       cudaError_t e1 = cudaStreamCreateWithFlags(&x->comm_stream, cudaStreamNonBlocking);
       if (e1 == cudaSuccess) e1 = cudaEventCreateWithFlags(&x->ev_ready, cudaEventDisableTiming);
       if (e1 == cudaSuccess) e1 = cudaEventCreateWithFlags(&x->ev_halo, cudaEventDisableTiming);
@@ -1071,10 +1209,10 @@ int labels_parts(msa_ctx* x, int b, float delta, int nparts, int32_t* labels_dev
   const size_t cap_tab = dist ? (size_t)x->prm.height * W : npix;     // concatenated segments <= pixels
   int32_t *roots = nullptr, *bounds = nullptr, *cl = nullptr, *sop = nullptr, *nseg = nullptr;
   unsigned long long *cnt = nullptr, *sum = nullptr;
+  std::vector<void*> held;  // every temporary of this call, freed on every exit path
   auto cleanup = [&]() {
-    void* ps[] = {roots, bounds, cl, sop, nseg, cnt, sum};
-    for (void* q : ps)
-      if (q) cudaFreeAsync(q, st);
+    for (void* q : held) cudaFreeAsync(q, st);
+    held.clear();
   };
 #define LB_TRY(expr)                                                                        \
   do {                                                                                      \
@@ -1084,13 +1222,26 @@ int labels_parts(msa_ctx* x, int b, float delta, int nparts, int32_t* labels_dev
       return set_err(MSA_ECUDA, "labels (parts): %s: %s", #expr, cudaGetErrorString(e_));   \
     }                                                                                       \
   } while (0)
-  LB_TRY(cudaMallocAsync((void**)&roots, sizeof(int32_t) * (cap_tab + 1), st));
-  LB_TRY(cudaMallocAsync((void**)&cl, sizeof(int32_t) * (cap_tab + 1), st));
-  LB_TRY(cudaMallocAsync((void**)&cnt, sizeof(unsigned long long) * (cap_tab + 1), st));
-  LB_TRY(cudaMallocAsync((void**)&sum, sizeof(unsigned long long) * (cap_tab + 1) * C, st));
-  LB_TRY(cudaMallocAsync((void**)&bounds, sizeof(int32_t) * 3 * W * nparts, st));
-  LB_TRY(cudaMallocAsync((void**)&sop, sizeof(int32_t) * (npix + 1), st));
-  LB_TRY(cudaMallocAsync((void**)&nseg, sizeof(int32_t) * nparts, st));
+#define LB_NCCL(expr)                                                                       \
+  do {                                                                                      \
+    ncclResult_t r_ = (expr);                                                               \
+    if (r_ != ncclSuccess) {                                                                \
+      cleanup();                                                                            \
+      return set_err(MSA_ENCCL, "labels (parts): %s: %s", #expr, g_nccl.GetErrorString(r_)); \
+    }                                                                                       \
+  } while (0)
+#define LB_ALLOC(ptr, bytes)                                                                \
+  do {                                                                                      \
+    LB_TRY(cudaMallocAsync((void**)&(ptr), (bytes), st));                                   \
+    held.push_back((void*)(ptr));                                                           \
+  } while (0)
+  LB_ALLOC(roots, sizeof(int32_t) * (cap_tab + 1));
+  LB_ALLOC(cl, sizeof(int32_t) * (cap_tab + 1));
+  LB_ALLOC(cnt, sizeof(unsigned long long) * (cap_tab + 1));
+  LB_ALLOC(sum, sizeof(unsigned long long) * (cap_tab + 1) * C);
+  LB_ALLOC(bounds, sizeof(int32_t) * 3 * W * nparts);
+  LB_ALLOC(sop, sizeof(int32_t) * (npix + 1));
+  LB_ALLOC(nseg, sizeof(int32_t) * nparts);
   if (!dist) {
     for (int p = 0; p < nparts; ++p) {
       MsaLabelPart part;
@@ -1111,16 +1262,16 @@ int labels_parts(msa_ctx* x, int b, float delta, int nparts, int32_t* labels_dev
     const size_t own = (size_t)g.nrows * W;
     int32_t *o_roots = nullptr, *o_bounds = nullptr, *o_n = nullptr, *g_roots = nullptr, *g_n = nullptr;
     unsigned long long *o_cnt = nullptr, *o_sum = nullptr, *g_cnt = nullptr, *g_sum = nullptr;
-    LB_TRY(cudaMallocAsync((void**)&o_roots, sizeof(int32_t) * (own + 1), st));
-    LB_TRY(cudaMallocAsync((void**)&o_cnt, sizeof(unsigned long long) * (own + 1), st));
-    LB_TRY(cudaMallocAsync((void**)&o_sum, sizeof(unsigned long long) * (own + 1) * C, st));
-    LB_TRY(cudaMallocAsync((void**)&o_bounds, sizeof(int32_t) * 3 * W, st));
-    LB_TRY(cudaMallocAsync((void**)&o_n, sizeof(int32_t), st));
+    LB_ALLOC(o_roots, sizeof(int32_t) * (own + 1));
+    LB_ALLOC(o_cnt, sizeof(unsigned long long) * (own + 1));
+    LB_ALLOC(o_sum, sizeof(unsigned long long) * (own + 1) * C);
+    LB_ALLOC(o_bounds, sizeof(int32_t) * 3 * W);
+    LB_ALLOC(o_n, sizeof(int32_t));
     MsaLabelPart part{sop, o_roots, o_cnt, o_sum, o_bounds, o_n};
     LB_TRY(msa_labels_part(g, x->c[x->cur], b, g.row0, g.nrows, delta, part, &x->lab, st, &launches));
-    LB_TRY(cudaMallocAsync((void**)&g_n, sizeof(int32_t) * nparts, st));
-    NCCL_TRY(g_nccl.AllGather(o_n, g_n, 1, ncclInt32, x->comm, st));
-    NCCL_TRY(g_nccl.AllGather(o_bounds, bounds, 3 * (size_t)W, ncclInt32, x->comm, st));
+    LB_ALLOC(g_n, sizeof(int32_t) * nparts);
+    LB_NCCL(g_nccl.AllGather(o_n, g_n, 1, ncclInt32, x->comm, st));
+    LB_NCCL(g_nccl.AllGather(o_bounds, bounds, 3 * (size_t)W, ncclInt32, x->comm, st));
     LB_TRY(cudaMemcpyAsync(S.data(), g_n, sizeof(int32_t) * nparts, cudaMemcpyDeviceToHost, st));
     LB_TRY(cudaStreamSynchronize(st));
     int maxS = 1;
@@ -1131,20 +1282,20 @@ int labels_parts(msa_ctx* x, int b, float delta, int nparts, int32_t* labels_dev
     // padded tables: own table copied into a maxS-slot send buffer (own capacity may be smaller)
     int32_t* s_roots = nullptr;
     unsigned long long *s_cnt = nullptr, *s_sum = nullptr;
-    LB_TRY(cudaMallocAsync((void**)&s_roots, sizeof(int32_t) * maxS, st));
-    LB_TRY(cudaMallocAsync((void**)&s_cnt, sizeof(unsigned long long) * maxS, st));
-    LB_TRY(cudaMallocAsync((void**)&s_sum, sizeof(unsigned long long) * maxS * C, st));
+    LB_ALLOC(s_roots, sizeof(int32_t) * maxS);
+    LB_ALLOC(s_cnt, sizeof(unsigned long long) * maxS);
+    LB_ALLOC(s_sum, sizeof(unsigned long long) * maxS * C);
     LB_TRY(cudaMemcpyAsync(s_roots, o_roots, sizeof(int32_t) * S[me], cudaMemcpyDeviceToDevice, st));
     LB_TRY(cudaMemcpyAsync(s_cnt, o_cnt, sizeof(unsigned long long) * S[me], cudaMemcpyDeviceToDevice, st));
     LB_TRY(cudaMemcpyAsync(s_sum, o_sum, sizeof(unsigned long long) * S[me] * C, cudaMemcpyDeviceToDevice, st));
-    LB_TRY(cudaMallocAsync((void**)&g_roots, sizeof(int32_t) * (size_t)maxS * nparts, st));
-    LB_TRY(cudaMallocAsync((void**)&g_cnt, sizeof(unsigned long long) * (size_t)maxS * nparts, st));
-    LB_TRY(cudaMallocAsync((void**)&g_sum, sizeof(unsigned long long) * (size_t)maxS * C * nparts, st));
-    NCCL_TRY(g_nccl.GroupStart());
-    NCCL_TRY(g_nccl.AllGather(s_roots, g_roots, maxS, ncclInt32, x->comm, st));
-    NCCL_TRY(g_nccl.AllGather(s_cnt, g_cnt, maxS, ncclUint64, x->comm, st));
-    NCCL_TRY(g_nccl.AllGather(s_sum, g_sum, (size_t)maxS * C, ncclUint64, x->comm, st));
-    NCCL_TRY(g_nccl.GroupEnd());
+    LB_ALLOC(g_roots, sizeof(int32_t) * (size_t)maxS * nparts);
+    LB_ALLOC(g_cnt, sizeof(unsigned long long) * (size_t)maxS * nparts);
+    LB_ALLOC(g_sum, sizeof(unsigned long long) * (size_t)maxS * C * nparts);
+    LB_NCCL(g_nccl.GroupStart());
+    LB_NCCL(g_nccl.AllGather(s_roots, g_roots, maxS, ncclInt32, x->comm, st));
+    LB_NCCL(g_nccl.AllGather(s_cnt, g_cnt, maxS, ncclUint64, x->comm, st));
+    LB_NCCL(g_nccl.AllGather(s_sum, g_sum, (size_t)maxS * C, ncclUint64, x->comm, st));
+    LB_NCCL(g_nccl.GroupEnd());
     for (int p = 0; p < nparts; ++p) {  // compact in rank (= row) order
       LB_TRY(cudaMemcpyAsync(roots + off[p], g_roots + (size_t)p * maxS, sizeof(int32_t) * S[p],
                              cudaMemcpyDeviceToDevice, st));
@@ -1153,8 +1304,6 @@ int labels_parts(msa_ctx* x, int b, float delta, int nparts, int32_t* labels_dev
       LB_TRY(cudaMemcpyAsync(sum + (size_t)off[p] * C, g_sum + (size_t)p * maxS * C,
                              sizeof(unsigned long long) * S[p] * C, cudaMemcpyDeviceToDevice, st));
     }
-    void* tmp[] = {o_roots, o_cnt, o_sum, o_bounds, o_n, g_n, s_roots, s_cnt, s_sum, g_roots, g_cnt, g_sum};
-    for (void* q : tmp) cudaFreeAsync(q, st);
   }
   LB_TRY(msa_labels_merge(nparts, off[nparts], W, C, roots, cnt, sum, bounds, delta, cl, count_dev, pal_dev, max_k,
                           &x->lab, st, &launches));
@@ -1167,6 +1316,8 @@ int labels_parts(msa_ctx* x, int b, float delta, int nparts, int32_t* labels_dev
   x->launches += launches + (dist ? 1 : nparts);
   cleanup();
 #undef LB_TRY
+#undef LB_NCCL
+#undef LB_ALLOC
   return MSA_OK;
 }
 
@@ -1177,7 +1328,7 @@ int msa_labels(msa_ctx* x, float delta, int32_t* labels, int32_t* n_clusters, fl
   if (!labels || !n_clusters) return set_err(MSA_EINVAL, "labels and n_clusters must not be NULL");
   if (max_k < 0 || (max_k > 0 && !palette)) return set_err(MSA_EINVAL, "palette needs max_k > 0 and a buffer");
   const bool dist = x->prm.world > 1 && x->prm.shard == MSA_SHARD_ROWS;
-  static const int test_parts = getenv("MSA_LABELS_PARTS") ? atoi(getenv("MSA_LABELS_PARTS")) : 0;  // test hook
+  static const int test_parts = MSA_HOOK("MSA_LABELS_PARTS") ? atoi(MSA_HOOK("MSA_LABELS_PARTS")) : 0;  // test hook
   const MsaGeom& g = x->g;
   const int nparts = dist ? x->prm.world : std::min(test_parts, g.H);
   if (dist) {  // stage (i) across the slab boundary needs the current c row above each slab
@@ -1345,6 +1496,18 @@ int msa_query(msa_ctx* x, msa_info* info) {
   info->iters_done = x->iters_done;
   info->launches = x->launches;
   info->rho = x->rho_cur;
+  // halo exchanges timed since msa_set_timing(1) (rows mode): device time of pack + NCCL + unpack
+  info->halo_ms = 0.0;
+  info->halo_exchanges = x->halo_exchanges_t;
+  if (!x->halo_ev.empty()) {
+    if (x->comm_stream) CUDA_TRY(cudaStreamSynchronize(x->comm_stream));
+    CUDA_TRY(cudaStreamSynchronize(x->stream));
+    for (auto& e : x->halo_ev) {
+      float ms = 0.0f;
+      CUDA_TRY(cudaEventElapsedTime(&ms, e.first, e.second));
+      info->halo_ms += ms;
+    }
+  }
   return MSA_OK;
 }
 
@@ -1353,9 +1516,12 @@ int msa_set_timing(msa_ctx* x, int enable) {
   CUDA_TRY(cudaStreamSynchronize(x->stream));
   for (auto& e : x->iter_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (auto& e : x->round_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  if (x->comm_stream) CUDA_TRY(cudaStreamSynchronize(x->comm_stream));
+  for (auto& e : x->halo_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   x->iter_ev.clear();
   x->round_ev.clear();
-  x->iter_launches_t = x->round_launches_t = 0;
+  x->halo_ev.clear();
+  x->iter_launches_t = x->round_launches_t = x->halo_exchanges_t = 0;
   x->in_iter_batch = false;
   x->timing = enable != 0;
   return MSA_OK;
@@ -1413,6 +1579,8 @@ int dal_check(msa_ctx* x, const msa_dal_params* d) {
     return set_err(MSA_EINVAL, "DAL needs sigma0 > 0 and b, c in (0, 1)");
   if (!(d->ex_lo > 0) || d->ex_hi < d->ex_lo || d->ec_lo < 0 || d->ec_hi < d->ec_lo)
     return set_err(MSA_EINVAL, "bad box E (need 0 < ex_lo <= ex_hi, 0 <= ec_lo <= ec_hi)");
+  if (!(d->eta >= 0) || !(d->eta_grad >= 0) || (d->gamma_ls != 0 && d->gamma_ls != 1))
+    return set_err(MSA_EINVAL, "DAL needs eta, eta_grad >= 0 and gamma_ls in {0, 1}");
   return MSA_OK;
 }
 
@@ -1428,7 +1596,7 @@ int dal_alloc(msa_ctx* x, const msa_dal_params* d, const float* v, const float* 
     // MSA_DAL_CHECKPOINT=S forces segments of S steps (test hook).
     size_t fr = 0, tot = 0;
     cudaMemGetInfo(&fr, &tot);
-    const char* e = getenv("MSA_DAL_CHECKPOINT");
+    const char* e = MSA_HOOK("MSA_DAL_CHECKPOINT");
     int S = e ? atoi(e) : 0;
     if (!e && (double)slots * pf * sizeof(float) > 0.7 * (double)fr)
       S = (int)std::ceil(std::sqrt((double)d->steps));
@@ -1550,18 +1718,39 @@ void dal_project(const msa_dal_params* d, double* e) {
 }
 
 // Algorithm 1 on allocated buffers (B: gradient sweeps, Bc: cost sweeps); leaves c = cbar = c(T; eps)
+// Remark 3.4: the largest component of the projected gradient (a component
+// counts as 0 where eps sits on the box and the descent direction -D points out of it)
+double dal_proj_grad_max(const msa_dal_params* d, const double* eps, const double* D) {
+  double mx = 0.0;
+  for (int m = 0; m < d->steps; ++m)
+    for (int i = 0; i < 2; ++i) {
+      const double lo = i == 0 ? d->ex_lo : d->ec_lo, hi = i == 0 ? d->ex_hi : d->ec_hi;
+      const double e = eps[2 * m + i], g = D[2 * m + i];
+      const bool inactive = (e <= lo && g >= 0.0) || (e >= hi && g <= 0.0);
+      mx = std::max(mx, inactive ? 0.0 : std::fabs(g));
+    }
+  return mx;
+}
+
 int dal_iterate(msa_ctx* x, const msa_dal_params* d, double* eps, DalBuffers& B, DalBuffers& Bc, double* J_hist,
-                double* sigma_hist) {
+                double* sigma_hist, int32_t* stop = nullptr) {
   int rc;
   const int M2 = 2 * d->steps;
   std::vector<double> D(M2), cand(M2);
   dal_project(d, eps);
   double sigma = d->sigma0;
+  int run = d->iters, why = 0;
+  double J_prev = 0.0;
   auto cost = [&](const double* e, double* J) { return dal_forward(x, d, e, Bc, false, J, nullptr); };
   for (int it = 0; it < d->iters; ++it) {
     double J0 = 0.0;
     if ((rc = dal_grad(x, d, eps, B, &J0, D.data())) != MSA_OK) return rc;
     if (J_hist) J_hist[it] = J0;
+    // UNTIL convergence (Remark 3.4): cost stationarity (the paper's rule, eta at PAPER.md:270) or
+    // the projected-gradient / variational-inequality test
+    if (it > 0 && d->eta > 0.0 && std::fabs(J0 - J_prev) / J_prev < d->eta) { run = it; why = 1; break; }
+    if (d->eta_grad > 0.0 && dal_proj_grad_max(d, eps, D.data()) < d->eta_grad) { run = it; why = 2; break; }
+    J_prev = J0;
     double D2 = 0.0;
     for (double g : D) D2 += g * g;
     auto ok = [&](double t, bool* pass) {
@@ -1609,7 +1798,11 @@ int dal_iterate(msa_ctx* x, const msa_dal_params* d, double* eps, DalBuffers& B,
   double Jf = 0.0;
   float* cT = nullptr;
   if ((rc = dal_forward(x, d, eps, Bc, false, &Jf, &cT)) != MSA_OK) return rc;
-  if (J_hist) J_hist[d->iters] = Jf;
+  if (J_hist) J_hist[run] = Jf;
+  if (stop) {
+    stop[0] = run;
+    stop[1] = why;
+  }
   const size_t pf = plane_floats(x);
   CUDA_TRY(cudaMemcpyAsync(x->c[x->cur], cT, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
   CUDA_TRY(cudaMemcpyAsync(x->cb[x->cur], cT, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
@@ -1634,14 +1827,14 @@ int msa_dal_gradient(msa_ctx* x, const msa_dal_params* d, const double* eps, con
 }
 
 int msa_dal(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, const float* mu, double* J_hist,
-            double* sigma_hist) {
+            double* sigma_hist, int32_t* stop) {
   int rc = dal_check(x, d);
   if (rc != MSA_OK) return rc;
   if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
   DalBuffers B, Bc;
   if ((rc = dal_alloc(x, d, v, mu, B, true)) != MSA_OK) return rc;
   if ((rc = dal_alloc(x, d, v, mu, Bc, false)) != MSA_OK) return rc;
-  return dal_iterate(x, d, eps, B, Bc, J_hist, sigma_hist);
+  return dal_iterate(x, d, eps, B, Bc, J_hist, sigma_hist, stop);
 }
 
 // Algorithm 2 with Algorithm 1 as its line 5 (SURVEY §8(f) NEXT-1 "Alg. 2 line 5
@@ -1651,7 +1844,7 @@ int msa_dal(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, co
 // AL residual of c^(j)) goes to stats[j]. v^(-1), mu^(0) from the arguments (NULL = 0); the final
 // mu is left in the context (MSA_FIELD_MU). rho is fixed (kappa is not applied).
 int msa_dal_admm(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, const float* mu, int32_t outer,
-                 double* J_hist, msa_round_stats* stats) {
+                 double* J_hist, msa_round_stats* stats, double* gamma_hist) {
   int rc = dal_check(x, d);
   if (rc != MSA_OK) return rc;
   if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
@@ -1660,15 +1853,36 @@ int msa_dal_admm(msa_ctx* x, const msa_dal_params* d, double* eps, const float* 
   DalBuffers B, Bc;
   if ((rc = dal_alloc(x, d, v, mu, B, true)) != MSA_OK) return rc;
   if ((rc = dal_alloc(x, d, v, mu, Bc, false)) != MSA_OK) return rc;
-  const size_t pf2 = 2 * plane_floats(x);
+  const size_t pf = plane_floats(x), pf2 = 2 * pf;
   const size_t before = x->stats.size() + x->rec_pending;  // this call's records start here
   // mu^(0) into the context's mu field (the round kernel updates it in place)
   CUDA_TRY(cudaMemcpyAsync(x->mu, B.mu, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
   const msa_params& P = x->prm;
+  // gamma search scratch: mu^(j), c^(j), and outputs the trial evaluations discard
+  struct Scratch {
+    float *mu_save = nullptr, *c_save = nullptr, *v_tmp = nullptr, *mu_tmp = nullptr;
+    msa_round_stats* rec = nullptr;
+    ~Scratch() {
+      void* ps[] = {mu_save, c_save, v_tmp, mu_tmp, rec};
+      for (void* q : ps)
+        if (q) cudaFree(q);
+    }
+  } S;
+  if (d->gamma_ls) {
+    CUDA_TRY(cudaMalloc((void**)&S.mu_save, sizeof(float) * pf2));
+    CUDA_TRY(cudaMalloc((void**)&S.c_save, sizeof(float) * pf));
+    CUDA_TRY(cudaMalloc((void**)&S.v_tmp, sizeof(float) * pf2));
+    CUDA_TRY(cudaMalloc((void**)&S.mu_tmp, sizeof(float) * pf2));
+    CUDA_TRY(cudaMalloc((void**)&S.rec, sizeof(msa_round_stats)));
+  }
+  std::vector<double> Jbuf(d->iters + 1);
+  std::vector<float> hmu(pf2);
+  double gam = P.gamma;  // the search starts from gamma, then from the last accepted step
   for (int32_t j = 0; j < outer; ++j) {
-    if ((rc = dal_iterate(x, d, eps, B, Bc, J_hist ? J_hist + (size_t)j * (d->iters + 1) : nullptr, nullptr)) !=
-        MSA_OK)
-      return rc;
+    int32_t stop[2] = {d->iters, 0};
+    if ((rc = dal_iterate(x, d, eps, B, Bc, Jbuf.data(), nullptr, stop)) != MSA_OK) return rc;
+    if (J_hist)
+      for (int i = 0; i <= d->iters; ++i) J_hist[(size_t)j * (d->iters + 1) + i] = Jbuf[std::min(i, stop[0])];
     // line 6-7 on c^(j) (now in c[cur]): v^(j) -> B.v, mu^(j+1) -> mu, and the round record
     const int s = x->cur;
     CUDA_TRY(cudaMemsetAsync(x->p[s], 0, sizeof(float) * pf2, x->stream));  // no CP dual here: D is of p = 0
@@ -1681,9 +1895,6 @@ int msa_dal_admm(msa_ctx* x, const msa_dal_params* d, double* eps, const float* 
     R.rho = x->rho_cur;
     R.beta = P.beta;
     R.alpha = P.alpha;
-    int nblk = 0;
-    CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->mu, x->I, x->mu, x->partials, &nblk, x->stream, B.v));
-    CUDA_TRY(msa_launch_reduce(x->partials, x->g.nb, nblk, x->sums, x->stream));
     MsaRecordArgs a;
     a.w = x->hx * x->hy;
     a.beta = P.beta;
@@ -1695,9 +1906,101 @@ int msa_dal_admm(msa_ctx* x, const msa_dal_params* d, double* eps, const float* 
     a.images = x->g.nb;
     a.iters = x->iters_done;
     a.lin = 0;
+    // one round kernel on (c[s], mu): v -> v_out, mu + gamma (v - grad c) -> mu_out, record -> rec
+    auto round_into = [&](double gamma_t, float* mu_out, float* v_out, msa_round_stats* rec) -> int {
+      R.gamma = (float)gamma_t;
+      int nblk = 0;
+      CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->mu, x->I, mu_out, x->partials, &nblk, x->stream, v_out));
+      CUDA_TRY(msa_launch_reduce(x->partials, x->g.nb, nblk, x->sums, x->stream));
+      CUDA_TRY(msa_launch_record(x->sums, a, rec, x->stream));
+      x->launches += 3;
+      return MSA_OK;
+    };
+    double step = P.gamma;
+    if (d->gamma_ls) {
+      // Phi(mu) = min_v L(c(mu), v, mu) = P(c, mu) - <mu, mu>/(2 rho) (eq:complete_square; P the
+      // record's primal), g = v^(j) - grad c^(j) with |g|_w = the record's AL residual
+      auto mu_sq = [&](const float* dmu, double* out) -> int {
+        CUDA_TRY(cudaMemcpyAsync(hmu.data(), dmu, sizeof(float) * pf2, cudaMemcpyDeviceToHost, x->stream));
+        CUDA_TRY(cudaStreamSynchronize(x->stream));
+        double acc = 0.0;
+        for (int m = 0; m < 2 * P.channels; ++m)
+          for (int r = 0; r < x->g.nrows; ++r)
+            for (int i = 0; i < P.width; ++i) {
+              const double q = hmu[(size_t)m * x->g.plane + (size_t)(r + x->g.G) * x->g.pitch + i];
+              acc += q * q;
+            }
+        *out = acc * x->hx * x->hy;
+        return MSA_OK;
+      };
+      auto fetch_rec = [&](msa_round_stats* h) -> int {
+        CUDA_TRY(cudaMemcpyAsync(h, S.rec, sizeof(msa_round_stats), cudaMemcpyDeviceToHost, x->stream));
+        CUDA_TRY(cudaStreamSynchronize(x->stream));
+        return MSA_OK;
+      };
+      CUDA_TRY(cudaMemcpyAsync(S.mu_save, x->mu, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+      CUDA_TRY(cudaMemcpyAsync(S.c_save, x->c[s], sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
+      msa_round_stats h0;
+      double m2 = 0.0;
+      if ((rc = round_into(0.0, S.mu_tmp, S.v_tmp, S.rec)) != MSA_OK || (rc = fetch_rec(&h0)) != MSA_OK ||
+          (rc = mu_sq(S.mu_save, &m2)) != MSA_OK)
+        return rc;
+      const double phi0 = h0.primal - m2 / (2.0 * x->rho_cur), g2 = h0.al_residual * h0.al_residual;
+      const std::vector<double> eps0(eps, eps + 2 * (size_t)d->steps);
+      std::vector<double> et(eps0.size());
+      // one Armijo test: mu_t = mu^(j) + t g, the line-5 DAL at (v^(j), mu_t) from eps^(j), Phi(mu_t)
+      auto ok = [&](double t, bool* pass) -> int {
+        CUDA_TRY(cudaMemcpyAsync(x->mu, S.mu_save, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+        CUDA_TRY(cudaMemcpyAsync(x->c[s], S.c_save, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
+        int r;
+        if ((r = round_into(t, x->mu, B.v, S.rec)) != MSA_OK) return r;
+        CUDA_TRY(cudaMemcpyAsync(B.mu, x->mu, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+        CUDA_TRY(cudaMemcpyAsync(Bc.mu, x->mu, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+        CUDA_TRY(cudaMemcpyAsync(Bc.v, B.v, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+        et = eps0;
+        if ((r = dal_iterate(x, d, et.data(), B, Bc, nullptr, nullptr)) != MSA_OK) return r;
+        msa_round_stats ht;
+        double mt2 = 0.0;
+        if ((r = round_into(0.0, S.mu_tmp, S.v_tmp, S.rec)) != MSA_OK || (r = fetch_rec(&ht)) != MSA_OK ||
+            (r = mu_sq(x->mu, &mt2)) != MSA_OK)
+          return r;
+        *pass = ht.primal - mt2 / (2.0 * x->rho_cur) >= phi0 + d->c * t * g2;
+        return MSA_OK;
+      };
+      double tau = gam, acc = -1.0;
+      int evals = 1;
+      bool pass = false;
+      if ((rc = ok(tau, &pass)) != MSA_OK) return rc;
+      if (pass) {
+        acc = tau;
+        while (evals < d->max_ls) {
+          ++evals;
+          if ((rc = ok(tau / d->b, &pass)) != MSA_OK) return rc;
+          if (!pass) break;
+          tau /= d->b;
+          acc = tau;
+        }
+      } else {
+        while (evals < d->max_ls) {
+          ++evals;
+          tau *= d->b;
+          if ((rc = ok(tau, &pass)) != MSA_OK) return rc;
+          if (pass) {
+            acc = tau;
+            break;
+          }
+        }
+      }
+      step = acc > 0 ? acc : 0.0;
+      gam = acc > 0 ? acc : tau;
+      // back to c^(j), mu^(j) for the official round below
+      CUDA_TRY(cudaMemcpyAsync(x->mu, S.mu_save, sizeof(float) * pf2, cudaMemcpyDeviceToDevice, x->stream));
+      CUDA_TRY(cudaMemcpyAsync(x->c[s], S.c_save, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
+      CUDA_TRY(cudaMemcpyAsync(x->cb[s], S.c_save, sizeof(float) * pf, cudaMemcpyDeviceToDevice, x->stream));
+    }
+    if (gamma_hist) gamma_hist[j] = step;
     if (x->rec_pending >= REC_CAP && (rc = fetch_records(x)) != MSA_OK) return rc;
-    CUDA_TRY(msa_launch_record(x->sums, a, x->d_rec + x->rec_pending, x->stream));
-    x->launches += 3;
+    if ((rc = round_into(step, x->mu, B.v, x->d_rec + x->rec_pending)) != MSA_OK) return rc;
     ++x->rec_pending;
     ++x->rounds_done;
     // the next DAL sees v^(j), mu^(j+1)

@@ -1,6 +1,17 @@
 // msa_internal.h - host-side launcher interface between the C-ABI driver
 // (msa_driver.cu) and the kernel translation units. Not part of the ABI.
 #pragma once
+
+// Test hooks. Environment switches that pick an A/B kernel variant, a summation order, a launch
+// path or the in-process NCCL transport exist only in the testing build (-DMSA_TESTING,
+// libmsa_testing.so, used by tests/ and tools/). In the product library (libmsa.so) MSA_HOOK is
+// always null, so its numerics depend on the msa_params it is given and nothing else.
+#include <cstdlib>
+#ifdef MSA_TESTING
+#define MSA_HOOK(name) getenv(name)
+#else
+#define MSA_HOOK(name) ((const char*)nullptr)
+#endif
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>
@@ -94,6 +105,16 @@ cudaError_t msa_launch_record(const double* sums, MsaRecordArgs a, void* record,
 // Layout conversions: interleaved [nb][rows][W][nm] <-> planar field (owned rows only).
 cudaError_t msa_launch_pack(const MsaGeom& g, int nm, const float* planar, float* inter, cudaStream_t s);
 cudaError_t msa_launch_unpack(const MsaGeom& g, int nm, const float* inter, float* planar, cudaStream_t s);
+
+// Packed halo exchange (rows mode, §8(e)): a segment is a contiguous run of n floats (whole stored
+// rows of one component plane) at ptr <-> buf[off, off + n); n and off are multiples of 4.
+struct MsaHaloSeg {
+  float* ptr;
+  long long n, off;
+};
+// to_buf = 1 gathers every segment into buf (the send side), 0 scatters buf into the segments.
+cudaError_t msa_launch_halo_pack(const MsaHaloSeg* d_segs, int nseg, long long max_n, float* buf, int to_buf,
+                                 cudaStream_t s);
 
 // Labels (msa_labels.cu): Q(c; delta) of reading R16 on image b of the planar field c.
 struct MsaLabelScratch;

@@ -489,7 +489,7 @@ cudaError_t launch_rp(const MsaGeom& g, const MsaIterConsts& K, const FastOm& om
   const int nr = msa_k1_hi(g) - g.k1_lo;
   if (nr <= 0) return cudaSuccess;
   dim3 grd((g.W + TW - 1) / TW, (nr + S::TH - 1) / S::TH, g.nb);
-  static const bool pdl = getenv("MSA_NO_PDL") == nullptr;  // A/B hook
+  static const bool pdl = MSA_HOOK("MSA_NO_PDL") == nullptr;  // A/B hook
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grd;
   cfg.blockDim = dim3(NT);
@@ -521,7 +521,7 @@ cudaError_t launch_cr(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
   }
   // P = 4 rows per thread (C <= 3); C = 4 takes P = 2 (the P = 4 tiles would need 145 KB of shared
   // memory, one CTA per SM). MSA_K1_P=2 / 4 forces the choice for C <= 3 (A/B hook).
-  static const int rows_per_thread = getenv("MSA_K1_P") ? atoi(getenv("MSA_K1_P")) : 0;
+  static const int rows_per_thread = MSA_HOOK("MSA_K1_P") ? atoi(MSA_HOOK("MSA_K1_P")) : 0;
   if constexpr (C == 4) {
     return launch_rp<C, R, 2, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
   } else {
@@ -546,7 +546,7 @@ cudaError_t launch_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffse
                         float* cb_out, float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
   // test hook: MSA_FORCE_GENERIC=1 selects the generic kernel (bitwise-identical results)
-  static const bool force_generic = getenv("MSA_FORCE_GENERIC") != nullptr;
+  static const bool force_generic = MSA_HOOK("MSA_FORCE_GENERIC") != nullptr;
   if (g.C < 1 || g.C > 4 || force_generic || !K.scaled) return cudaErrorNotSupported;  // scaled form only
   // every active offset must lie in the interior disc (true for eps_x >= the default)
   for (int o = 0; o < T.n; ++o)

@@ -45,20 +45,12 @@ using namespace msa_f32x2;
 
 constexpr int C = 3;
 constexpr int P = 4;       // rows per chunk
+constexpr int NR = 2 * P;  // register ring rows: chunk j-1 (0..P-1) and chunk j (P..2P-1)
 #ifndef MSA_SWEEP_NW
 #define MSA_SWEEP_NW 8
 #endif
 #ifndef MSA_SWEEP_OCC
 #define MSA_SWEEP_OCC 1
-#endif
-#ifndef MSA_SWEEP_NOFIN
-#define MSA_SWEEP_NOFIN 0
-#endif
-#ifndef MSA_SWEEP_STAGGER
-#define MSA_SWEEP_STAGGER 0
-#endif
-#ifndef MSA_SWEEP_LOCKSTEP
-#define MSA_SWEEP_LOCKSTEP 0
 #endif
 constexpr int NW = MSA_SWEEP_NW;  // warps (independent sweep units) per CTA
 // Box x starts are rounded down to a multiple of 4 floats (16 bytes, which the TMA unit needs):
@@ -66,26 +58,25 @@ constexpr int NW = MSA_SWEEP_NW;  // warps (independent sweep units) per CTA
 constexpr int RW = 40;     // c / cbar box width: 32 lanes + up to 4 right neighbours + cofs
 constexpr int LW = 36;     // p, mu, I box width: 32 lanes + cofs
 constexpr int OW = 28;     // output columns per band (a multiple of 4: the output boxes start 16-byte aligned)
-constexpr int OUT_CB = 352, OUT_P = 704;  // staged-output sub-buffers, 128-byte aligned (TMA store sources)
+constexpr int OUT_CB = 352, OUT_P = 704;  // staged outputs inside the dead p/mu slot, 128-byte aligned
 static_assert(OUT_CB >= C * P * OW && OUT_P - OUT_CB >= C * P * OW && OUT_CB % 32 == 0 && OUT_P % 32 == 0, "staging");
+constexpr int NSLOT = 3;   // c ring: chunks j-1, j (read at step j) and j+1 (in flight)
 constexpr int OCC = MSA_SWEEP_OCC;  // CTAs per SM the register budget is sized for
 constexpr float SENT = 1e18f;
 constexpr unsigned FULL = 0xffffffffu;
 
 struct __align__(128) WarpSmem {
-  float cring[4][C * P * RW];  // [slot][C][P][RW], chunk q in slot q & 3
-  float cb[608];               // [C][P+1][RW] (600 used)
-  float p[2 * C * P * LW];     // [2C][P][LW]
-  float mu[2 * C * P * LW];    // [2C][P][LW]
-  float I[448];                // [C][P][LW] (432 used)
-  float out[OUT_P + 2 * C * P * OW];  // staged outputs of one chunk: c+ [C][P][OW] at 0, cbar+ at OUT_CB, p+ [2C][P][OW] at OUT_P
-  unsigned long long bar[16];  // 0..3 c slots, 4 step-2/3 slot
+  float cring[NSLOT][C * P * RW];  // [slot][C][P][RW], chunk q in slot (q + 3) % 3
+  float cb[608];                   // [C][P+1][RW] (600 used)
+  float pm[2 * 2 * C * P * LW];    // p [2C][P][LW], mu [2C][P][LW]; after the dual step the output staging
+  float I[448];                    // [C][P][LW] (432 used)
+  unsigned long long bar[8];       // 0..2 c slots, 3 step-2/3 slot
 };
 static_assert(sizeof(WarpSmem) % 128 == 0, "warp smem must stay 128-byte aligned");
 static_assert(sizeof(float) * C * P * RW % 128 == 0, "ring slots must stay 128-byte aligned");
-static_assert(offsetof(WarpSmem, out) % 128 == 0 && offsetof(WarpSmem, cb) % 128 == 0 && offsetof(WarpSmem, p) % 128 == 0 &&
-                  offsetof(WarpSmem, mu) % 128 == 0 && offsetof(WarpSmem, I) % 128 == 0,
+static_assert(offsetof(WarpSmem, cb) % 128 == 0 && offsetof(WarpSmem, pm) % 128 == 0 && offsetof(WarpSmem, I) % 128 == 0,
               "TMA destinations must be 128-byte aligned");
+static_assert(OUT_P + 2 * C * P * OW <= 2 * 2 * C * P * LW, "staging fits the p/mu slot");
 constexpr unsigned C_BYTES = C * P * RW * 4;
 constexpr unsigned PD_BYTES = (C * (P + 1) * RW + 2 * (2 * C * P * LW) + C * P * LW) * 4;
 static_assert(C * (P + 1) * RW <= 608 && C * P * LW <= 448, "step-2/3 slot sizes");
@@ -105,8 +96,35 @@ __host__ __device__ constexpr int om_index(int R, int dx, int dy) {
   return n + (dx == 0 ? dy - 1 : dy + col_m(R, dx));
 }
 
+// Evaluation lists. A packed evaluation pairs one own row ya (0..7 of the two-chunk ring, a scalar
+// broadcast operand) with one aligned partner row pair (2q, 2q+1); a half whose pair is not to be
+// evaluated at this step (|dy| > m, or both rows in the older chunk, or dy <= 0 in the own column)
+// carries nom = 0, which gives t = max(-|d|^2, 0) = 0 and w = 0 exactly.
+__host__ __device__ constexpr bool half_valid(int M, bool own_col, int ya, int yb) {
+  return own_col ? (yb - ya >= 1 && yb - ya <= M && yb >= P)
+                 : (yb - ya <= M && ya - yb <= M && (ya >= P || yb >= P));
+}
+__host__ __device__ constexpr int n_evals(int M, bool own_col) {
+  int n = 0;
+  for (int ya = 0; ya < NR; ++ya)
+    for (int q = 0; q < P; ++q)
+      if (half_valid(M, own_col, ya, 2 * q) || half_valid(M, own_col, ya, 2 * q + 1)) ++n;
+  return n;
+}
+// e-th evaluation of a shape: ya * 4 + q
+__host__ __device__ constexpr int eval_at(int M, bool own_col, int e) {
+  int n = 0;
+  for (int ya = 0; ya < NR; ++ya)
+    for (int q = 0; q < P; ++q)
+      if (half_valid(M, own_col, ya, 2 * q) || half_valid(M, own_col, ya, 2 * q + 1)) {
+        if (n == e) return ya * 4 + q;
+        ++n;
+      }
+  return -1;
+}
+constexpr int MAX_EV = 24;  // evaluations per column offset (shape M = 4: 20)
 struct SweepOm {
-  float v[64];  // 1 - a_delta for the half-disc H+ in the kernel's order
+  float2 v[5][MAX_EV];  // per column offset k = 0..4: (nom of the lo half, nom of the hi half) per evaluation
 };
 struct SweepPlan {
   int nbands, nsegs, seg_chunks, jfirst, jend, units;
@@ -116,9 +134,103 @@ struct SweepMaps {
   CUtensorMap co, cbo, po;  // outputs: owned rows only, row 0 = the slab's first owned row
 };
 
+// One packed evaluation = two unordered pairs {(x, ya), (x + k, 2q)} and {(x, ya), (x + k, 2q + 1)}:
+// the weights w = phi(r) (scaled form, msa_common.cuh msa_agent_term_s) are evaluated once per pair
+// and both terms of each pair are formed from them. With d = c_own - c_partner, the own pixel gets
+// w (c_partner - c_own) = -(w d) and the partner gets w (c_own - c_partner) = w d: the values a
+// separate evaluation at either pixel would give (fsub is antisymmetric, (-d)^2 = d^2 bitwise).
+// The own row is a broadcast scalar operand, the partner rows an aligned register pair.
+__device__ __forceinline__ void pair_eval(const float (&own)[C], const f2 (&pp)[C], f2 nom, f2 M4, f2 QC,
+                                          f2 (&acc_own)[C], f2 (&acc_p)[C]) {
+  f2 d[C];
+#pragma unroll
+  for (int k = 0; k < C; ++k) d[k] = sub2(pk(own[k], own[k]), pp[k]);
+  f2 s = fma2(d[0], d[0], nom);  // |d|^2 - om/e_c per half
+#pragma unroll
+  for (int k = 1; k < C; ++k) s = fma2(d[k], d[k], s);
+  const f2 t = relu2n(s);
+  const f2 t2 = mul2(t, t);
+  const f2 t4 = mul2(t2, t2);
+  const f2 w = mul2(t4, fma2(M4, t, QC));
+#pragma unroll
+  for (int k = 0; k < C; ++k) {
+    acc_own[k] = fma2(w, d[k], acc_own[k]);  // the NEGATED own-role sum, one partial per half
+    acc_p[k] = fma2(w, d[k], acc_p[k]);
+  }
+}
+
+// dx = 0: pairs (ya, yb) of the own column with ya < yb <= ya + M0, yb in chunk j; both terms stay
+// in this thread (partner role into the pair-aligned accumulator accp)
+template <int M0>
+__device__ __forceinline__ void pass_own(const SweepOm& om, const float (&cc)[NR][C], f2 (&acc)[NR][C],
+                                         f2 (&accp)[P][C], f2 M4, f2 QC) {
+  constexpr int NE = n_evals(M0, true);
+  static_assert(NE <= MAX_EV, "evaluation list");
+#pragma unroll
+  for (int e = 0; e < NE; ++e) {
+    const int ya = eval_at(M0, true, e) >> 2, q = eval_at(M0, true, e) & 3;
+    f2 pp[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) pp[c] = pk(cc[2 * q][c], cc[2 * q + 1][c]);
+    const float2 nm = om.v[0][e];
+    pair_eval(cc[ya], pp, pk(nm.x, nm.y), M4, QC, acc[ya], accp[q]);
+  }
+}
+
+// dx = k in [k_lo, k_hi] (a rolled loop over one evaluation shape M): pairs (x, ya) - (x + k, yb),
+// |yb - ya| <= m_k, max(ya, yb) in chunk j. The partner terms are summed per partner row and handed to
+// lane + k with one shuffle per row and channel (lanes < k are halo columns: what they receive is
+// discarded).
+template <int M>
+__device__ __forceinline__ void pass_cols(int k_lo, int k_hi, const float* __restrict__ r0,
+                                          const float* __restrict__ r1, int cl, const SweepOm& om,
+                                          const float (&cc)[NR][C], f2 (&acc)[NR][C], f2 (&accp)[P][C],
+                                          f2 M4, f2 QC) {
+  constexpr int NE = n_evals(M, false);
+  static_assert(NE <= MAX_EV, "evaluation list");
+  auto load_col = [&](int k, f2 (&pc)[P][C]) {
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        const float* r = (q < 2 ? r0 : r1) + (c * P + 2 * (q & 1)) * RW + cl + k;
+        pc[q][c] = pk(r[0], r[RW]);
+      }
+  };
+  f2 pc[P][C];
+  load_col(k_lo, pc);
+#pragma unroll 1
+  for (int k = k_lo; k <= k_hi; ++k) {
+    f2 pn[P][C], ar[P][C];
+    load_col(k < k_hi ? k + 1 : k, pn);  // the next column lands while this one is evaluated
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+      for (int c = 0; c < C; ++c) ar[q][c] = pk(0.0f, 0.0f);
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int ya = eval_at(M, false, e) >> 2, q = eval_at(M, false, e) & 3;
+      const float2 nm = om.v[k][e];
+      pair_eval(cc[ya], pc[q], pk(nm.x, nm.y), M4, QC, acc[ya], ar[q]);
+    }
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        float l, h;
+        upk(ar[q][c], l, h);
+        l = __shfl_up_sync(FULL, l, k);
+        h = __shfl_up_sync(FULL, h, k);
+        accp[q][c] = add2(accp[q][c], pk(l, h));
+        pc[q][c] = pn[q][c];
+      }
+  }
+}
+
 template <int R>
 __global__ void __launch_bounds__(NW * 32, OCC)
-    k_iter_sweep_c3(MsaGeom g, MsaIterConsts K, SweepOm om, SweepPlan pl, const __grid_constant__ SweepMaps tm) {
+    k_iter_sweep_c3(MsaGeom g, MsaIterConsts K, const __grid_constant__ SweepOm om, SweepPlan pl,
+                    const __grid_constant__ SweepMaps tm) {
   constexpr int HL = R - 1;    // halo lanes = largest |dx| in the interior disc
   constexpr int BS = OW;       // output columns per band: lanes HL .. HL+27 (lanes past that idle for R < 5)
   static_assert(HL + OW <= 32, "band too wide");
@@ -147,45 +259,43 @@ __global__ void __launch_bounds__(NW * 32, OCC)
 
   if (lane == 0) {
 #pragma unroll
-    for (int i = 0; i < 5; ++i) mbar_init(&sm.bar[i], 1);
+    for (int i = 0; i < 4; ++i) mbar_init(&sm.bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
   unsigned ph = 0;  // expected parity per barrier
-#if MSA_SWEEP_STAGGER
-  if (warp & 1) __nanosleep(MSA_SWEEP_STAGGER);  // A/B: odd warps start half a step late
-#endif
+  auto slot = [](int q) { return (q + NSLOT) % NSLOT; };  // q >= -1
 
   auto load_c = [&](int q) {
-    unsigned long long* bar = &sm.bar[q & 3];
+    unsigned long long* bar = &sm.bar[slot(q)];
     mbar_expect_tx(bar, C_BYTES);
-    tma_load3(sm.cring[q & 3], &tm.c, xa, 4 * q + so, b * C, bar);
+    tma_load3(sm.cring[slot(q)], &tm.c, xa, 4 * q + so, b * C, bar);
   };
   auto load_pd = [&](int q) {
-    unsigned long long* bar = &sm.bar[4];
+    unsigned long long* bar = &sm.bar[3];
     mbar_expect_tx(bar, PD_BYTES);
     tma_load3(sm.cb, &tm.cb, xa, 4 * q + so, b * C, bar);
-    tma_load3(sm.p, &tm.p, xa, 4 * q + so, b * 2 * C, bar);
-    tma_load3(sm.mu, &tm.mu, xa, 4 * q + so, b * 2 * C, bar);
+    tma_load3(sm.pm, &tm.p, xa, 4 * q + so, b * 2 * C, bar);
+    tma_load3(sm.pm + 2 * C * P * LW, &tm.mu, xa, 4 * q + so, b * 2 * C, bar);
     tma_load3(sm.I, &tm.I, xa, 4 * q + so, b * C, bar);
   };
   auto wait_c = [&](int q) {
-    const int s = q & 3;
+    const int s = slot(q);
     mbar_wait(&sm.bar[s], (ph >> s) & 1u);
     ph ^= 1u << s;
   };
   auto wait_pd = [&]() {
-    mbar_wait(&sm.bar[4], (ph >> 4) & 1u);
-    ph ^= 16u;
+    mbar_wait(&sm.bar[3], (ph >> 3) & 1u);
+    ph ^= 8u;
     __syncwarp();  // reconverge after the spin (the shuffles that follow need it)
   };
-  // sentinel colour for ring entries outside the image / the stored slab (all: whole chunk)
-  auto fix_c = [&](int q, bool all) {
-    float* s = sm.cring[q & 3];
+  // sentinel colour for ring entries outside the image / the stored slab
+  auto fix_c = [&](int q) {
+    float* s = sm.cring[slot(q)];
 #pragma unroll
     for (int r = 0; r < P; ++r) {
       const int y = 4 * q + r;
-      const bool row_bad = all || y < yv0 || y >= yv1;
+      const bool row_bad = y < yv0 || y >= yv1;
 #pragma unroll
       for (int k = 0; k < C; ++k) {
         float* row = s + (k * P + r) * RW;
@@ -197,28 +307,6 @@ __global__ void __launch_bounds__(NW * 32, OCC)
   };
   auto needs_fix = [&](int q) { return col_edge || 4 * q < yv0 || 4 * q + P > yv1; };
 
-  // prologue: chunk jlo-2 only feeds discarded accumulators -> sentinel; chunks jlo-1, jlo by TMA;
-  // step-2/3 inputs of chunk jlo-1 for p+ of the row below the first output row
-  const bool prow = 4 * jlo > 0;
-  fix_c(jlo - 2, true);
-  if (lane == 0) {
-    load_c(jlo - 1);
-    load_c(jlo);
-    if (prow) load_pd(jlo - 1);
-  }
-  wait_c(jlo - 1);
-  if (needs_fix(jlo - 1)) fix_c(jlo - 1, false);
-
-  f2 S[6][C];  // accumulators of rows 4j-4 .. 4j+7 (chunks j-1, j, j+1) at step j, pairs (2i, 2i+1)
-#pragma unroll
-  for (int i = 0; i < 6; ++i)
-#pragma unroll
-    for (int k = 0; k < C; ++k) S[i][k] = pk(0.0f, 0.0f);
-  float qyp[C] = {0.0f, 0.0f, 0.0f};  // p+_y of the row below the next row to finalise
-  const f2 M4 = pk(K.m4, K.m4);  // scaled form (msa_agent_term_s)
-  const float qcs = K.kernel == 0 ? 5.0f : 3.0f;
-  const f2 QC = pk(qcs, qcs);
-
   // step 2 for row r of the step-2/3 slot: p+ = Pi_beta((rho (p + sigma grad cbar) - sigma mu)/(rho + sigma))
   auto dual_row = [&](int r, int y, float (&qx)[C], float (&qy)[C]) {
     float gx[C], gy[C], px[C], py[C], mx[C], my[C];
@@ -228,152 +316,103 @@ __global__ void __launch_bounds__(NW * 32, OCC)
       const float c0 = cbr[0];
       gx[k] = x < W - 1 ? __fmul_rn(__fsub_rn(cbr[1], c0), K.inv_hx) : 0.0f;
       gy[k] = y < H - 1 ? __fmul_rn(__fsub_rn(cbr[RW], c0), K.inv_hy) : 0.0f;
-      px[k] = sm.p[(k * P + r) * LW + cl];
-      py[k] = sm.p[((C + k) * P + r) * LW + cl];
-      mx[k] = sm.mu[(k * P + r) * LW + cl];
-      my[k] = sm.mu[((C + k) * P + r) * LW + cl];
+      px[k] = sm.pm[(k * P + r) * LW + cl];
+      py[k] = sm.pm[((C + k) * P + r) * LW + cl];
+      mx[k] = sm.pm[2 * C * P * LW + (k * P + r) * LW + cl];
+      my[k] = sm.pm[2 * C * P * LW + ((C + k) * P + r) * LW + cl];
     }
     msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
   };
 
-  // Every warp of a CTA runs the same number of steps (a shorter last segment idles through the
-  // tail) so that, with MSA_SWEEP_LOCKSTEP, a CTA barrier per step keeps the warps on the same
-  // stretch of the (long, fully unrolled) step code: they then share the instruction cache.
+  // prologue: chunks jlo-1 (older partners of chunk jlo) and jlo by TMA; step-2/3 inputs of chunk
+  // jlo-1 for p+_y of the row below the first output row
+  const bool prow = 4 * jlo > 0;
+  if (lane == 0) {
+    load_c(jlo - 1);
+    load_c(jlo);
+    if (prow) load_pd(jlo - 1);
+  }
+  wait_c(jlo - 1);
+  if (needs_fix(jlo - 1)) fix_c(jlo - 1);
+  __syncwarp();
+  // own colours / own-role interaction sums of rows 4j-4 .. 4j+3 at step j; partner-role sums of
+  // the same rows as aligned pairs (rows 2q, 2q+1)
+  float cc[NR][C];
+  f2 acc[NR][C], accp[P][C];
+#pragma unroll
+  for (int r = 0; r < P; ++r)
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      cc[P + r][k] = sm.cring[slot(jlo - 1)][(k * P + r) * RW + cl];
+      acc[P + r][k] = pk(0.0f, 0.0f);
+    }
+#pragma unroll
+  for (int q = 0; q < P; ++q)
+#pragma unroll
+    for (int k = 0; k < C; ++k) accp[q][k] = pk(0.0f, 0.0f);
+  float qyp[C] = {0.0f, 0.0f, 0.0f};  // p+_y of the row below the next row to finalise
+  // m4 in an ordinary register (msa_iter_fast.cu agent_phase: otherwise reloaded from the constant bank)
+  const float m4 = __fmaf_rn(0.0f, (float)lane, K.m4);
+  const float qc = K.kernel == 0 ? 5.0f : 3.0f;
+  const f2 M4 = pk(m4, m4), QC = pk(qc, qc);
+
+  // Step j evaluates every unordered pair whose newer (upper) element lies in chunk j; the older
+  // element is then in chunk j or j-1, so both of its terms land in the two-chunk register ring, and
+  // chunk j-1 is complete at the end of the step. Per pixel the terms arrive in a fixed order that
+  // depends only on (y mod 4) and the offset, so results do not depend on band or segment bounds.
 #pragma unroll 1
-  for (int t = 0; t < pl.seg_chunks + 2; ++t) {
-    const int j = jlo - 1 + t;
-    if (j <= jhi + 1) {
-    // (a) prefetch chunk j+2 into the slot chunk j-2 used (last read in the previous step)
-    __syncwarp();
-    if (lane == 0 && j + 2 <= jhi + 1) load_c(j + 2);
-    // (b) chunk j+1: wait for it, or sentinel past the segment's upper halo chunk
-    if (j + 1 <= jhi + 1) {
-      wait_c(j + 1);
-      if (needs_fix(j + 1)) fix_c(j + 1, false);
-    } else {
-      fix_c(j + 1, true);
-    }
-    __syncwarp();
-
-    // (c) source pass over chunk j (step 1 on the half-disc H+). Rows are held in register pairs
-    // (2i, 2i+1); a column is done in two parity passes so that every neighbour pair the packed
-    // arithmetic needs is loaded straight into a pair (no repacking).
-    {
-      const float* rm = sm.cring[(j - 1) & 3];
-      const float* r0 = sm.cring[j & 3];
-      const float* rp = sm.cring[(j + 1) & 3];
-#define CV(r, k, dx) (((r) < 0 ? rm : (r) < P ? r0 : rp)[((k) * P + (((r) + 4) & 3)) * RW + cl + (dx)])
-      f2 ci[2][C];
+  for (int j = jlo; j <= jhi + 1; ++j) {
 #pragma unroll
-      for (int jj = 0; jj < 2; ++jj)
+    for (int r = 0; r < P; ++r)
 #pragma unroll
-        for (int k = 0; k < C; ++k) ci[jj][k] = pk(CV(2 * jj, k, 0), CV(2 * jj + 1, k, 0));
-#pragma unroll
-      for (int dx = 0; dx <= HL; ++dx) {
-        const int m = col_m(R, dx);
-        f2 pa[6][C];  // partner sums of column x + dx, ring rows (2i, 2i+1) (relative rows 2i-4, 2i-3)
-#pragma unroll
-        for (int i = 0; i < 6; ++i)
-#pragma unroll
-          for (int k = 0; k < C; ++k) pa[i][k] = pk(0.0f, 0.0f);
-#pragma unroll
-        for (int par = 0; par < 2; ++par) {
-          f2 np[12][C];  // neighbour pairs (a, a+1) of column x + dx, a = par (mod 2), index a + 4
-#pragma unroll
-          for (int a = -4; a <= P + 2; ++a) {
-            if (((a + 4) & 1) != par || a < (dx == 0 ? 1 : -m) || a > P - 2 + m) continue;
-#pragma unroll
-            for (int k = 0; k < C; ++k) np[a + 4][k] = pk(CV(a, k, dx), CV(a + 1, k, dx));
-          }
-#pragma unroll
-          for (int dy = -4; dy <= 4; ++dy) {
-            if (dy < -m || dy > m || (dx == 0 && dy <= 0) || ((dy + 4) & 1) != par) continue;
-            const float omv = om.v[om_index(R, dx, dy)];
-            const f2 OM = pk(omv, omv);
-#pragma unroll
-            for (int jj = 0; jj < 2; ++jj) {
-              const int a = 2 * jj + dy;  // partner rows a, a+1 of own rows 2jj, 2jj+1
-              f2 d[C];
-#pragma unroll
-              for (int k = 0; k < C; ++k) d[k] = sub2(np[a + 4][k], ci[jj][k]);
-              f2 sq = fma2(d[0], d[0], OM);  // |d|^2 - om/e_c
-#pragma unroll
-              for (int k = 1; k < C; ++k) sq = fma2(d[k], d[k], sq);
-              const f2 t = relu2n(sq);
-              const f2 t2 = mul2(t, t);
-              const f2 t4 = mul2(t2, t2);
-              const f2 w = mul2(t4, fma2(M4, t, QC));
-#pragma unroll
-              for (int k = 0; k < C; ++k) S[jj + 2][k] = fma2(w, d[k], S[jj + 2][k]);  // own: + w d
-              if (par == 0) {  // partner pair aligned with the ring pairs
-#pragma unroll
-                for (int k = 0; k < C; ++k) pa[(a + 4) >> 1][k] = fma2(w, d[k], pa[(a + 4) >> 1][k]);
-              } else {         // partner rows straddle two ring pairs: hi half of one, lo half of the next
-                float wl, wh;
-                upk(w, wl, wh);
-#pragma unroll
-                for (int k = 0; k < C; ++k) {
-                  float dl, dh, p0l, p0h, p1l, p1h;
-                  upk(d[k], dl, dh);
-                  upk(pa[(a + 3) >> 1][k], p0l, p0h);
-                  upk(pa[(a + 5) >> 1][k], p1l, p1h);
-                  p0h = __fmaf_rn(wl, dl, p0h);
-                  p1l = __fmaf_rn(wh, dh, p1l);
-                  pa[(a + 3) >> 1][k] = pk(p0l, p0h);
-                  pa[(a + 5) >> 1][k] = pk(p1l, p1h);
-                }
-              }
-            }
-          }
-        }
-        // partner terms (- w d): same lane for dx = 0, else handed to lane + dx (lanes < dx are halo)
-#pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          const int r0i = 2 * i - 4;  // relative rows r0i, r0i + 1
-          if (r0i + 1 < (dx == 0 ? 1 : -m) || r0i > P - 1 + m) continue;
-#pragma unroll
-          for (int k = 0; k < C; ++k) {
-            if (dx == 0) {
-              S[i][k] = sub2(S[i][k], pa[i][k]);
-            } else {
-              float l, h, sl, sh;
-              upk(pa[i][k], l, h);
-              l = __shfl_up_sync(FULL, l, dx);
-              h = __shfl_up_sync(FULL, h, dx);
-              upk(S[i][k], sl, sh);
-              S[i][k] = pk(__fsub_rn(sl, l), __fsub_rn(sh, h));
-            }
-          }
-        }
+      for (int k = 0; k < C; ++k) {
+        cc[r][k] = cc[P + r][k];
+        acc[r][k] = acc[P + r][k];
+        acc[P + r][k] = pk(0.0f, 0.0f);
       }
-#undef CV
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      accp[0][k] = accp[2][k];
+      accp[1][k] = accp[3][k];
+      accp[2][k] = pk(0.0f, 0.0f);
+      accp[3][k] = pk(0.0f, 0.0f);
+    }
+    __syncwarp();  // every lane is done with chunk j-2's slot (chunk j+1 goes there)
+    if (lane == 0 && j + 1 <= jhi + 1) load_c(j + 1);
+    wait_c(j);
+    if (needs_fix(j)) fix_c(j);
+    __syncwarp();
+    const float* r0 = sm.cring[slot(j - 1)];
+    const float* r1 = sm.cring[slot(j)];
+#pragma unroll
+    for (int r = 0; r < P; ++r)
+#pragma unroll
+      for (int k = 0; k < C; ++k) cc[P + r][k] = r1[(k * P + r) * RW + cl];
+
+    pass_own<col_m(R, 0)>(om, cc, acc, accp, M4, QC);
+    if constexpr (R == 5) {
+      pass_cols<4>(1, 2, r0, r1, cl, om, cc, acc, accp, M4, QC);
+      pass_cols<3>(3, 4, r0, r1, cl, om, cc, acc, accp, M4, QC);
+    } else {
+      pass_cols<col_m(R, 1)>(1, HL, r0, r1, cl, om, cc, acc, accp, M4, QC);
     }
 
-    // (d) finalise chunk j-1 (its sums are complete): c_half, steps 2-3, outputs staged in smem
-    // and written by three TMA tensor stores (clipped at the image edge and the slab's rows)
+    // finalise chunk j-1 (its sums are complete): c_half, steps 2-3, outputs staged over the dead
+    // p/mu slot and written by three TMA tensor stores (clipped at the image edge and the slab's rows)
     if (j - 1 >= jlo) {
       wait_pd();
-      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging free
-      __syncwarp();
       const int q = j - 1;
-      const float* cr = sm.cring[q & 3];
       const bool st = lane >= HL && lane < HL + OW;
-      float* oc = sm.out + (lane - HL);
       // the four rows' dual steps are independent: all first (latency overlaps), then div + prox
       float qx[P][C], qy[P][C], qxl[P][C];
-#if MSA_SWEEP_NOFIN  // timing experiment only: wrong results
-#pragma unroll
-      for (int r = 0; r < P; ++r)
-#pragma unroll
-        for (int k = 0; k < C; ++k) { qx[r][k] = sm.p[(k * P + r) * LW + cl]; qy[r][k] = sm.mu[(k * P + r) * LW + cl]; }
-#else
 #pragma unroll
       for (int r = 0; r < P; ++r) dual_row(r, 4 * q + r, qx[r], qy[r]);
-#endif
 #pragma unroll
       for (int r = 0; r < P; ++r)
 #pragma unroll
         for (int k = 0; k < C; ++k) qxl[r][k] = __shfl_up_sync(FULL, qx[r][k], 1);
+      __syncwarp();  // p and mu are read: the slot becomes the output staging
+      float* oc = sm.pm + (lane - HL);
 #pragma unroll
       for (int r = 0; r < P; ++r) {
         const int y = 4 * q + r;
@@ -384,9 +423,12 @@ __global__ void __launch_bounds__(NW * 32, OCC)
           float ay = y < H - 1 ? qy[r][k] : 0.0f;
           if (y > 0) ay = __fsub_rn(ay, r == 0 ? qyp[k] : qy[r - 1][k]);
           const float dv = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
-          float s0, s1;
-          upk(S[r >> 1][k], s0, s1);
-          const float chalf = __fmaf_rn(K.dt_s, (r & 1) ? s1 : s0, cr[(k * P + r) * RW + cl]);
+          float apl, aph, anl, anh;
+          upk(accp[r >> 1][k], apl, aph);
+          upk(acc[r][k], anl, anh);
+          const float own = -__fadd_rn(anl, anh);                     // own-role sum (negated partials)
+          const float a = __fadd_rn(own, (r & 1) ? aph : apl);        // + partner-role sum
+          const float chalf = __fmaf_rn(K.dt_s, a, cc[r][k]);
           float cp, cbp;
           msa_prox_extrap(K, chalf, dv, sm.I[(k * P + r) * LW + cl], cp, cbp);
           if (st) {
@@ -403,34 +445,24 @@ __global__ void __launch_bounds__(NW * 32, OCC)
       __syncwarp();
       if (lane == 0 && active) {
         const int xo = band * BS, yo = 4 * q - g.row0;
-        tma_store3(&tm.co, xo, yo, b * C, sm.out);
-        tma_store3(&tm.cbo, xo, yo, b * C, sm.out + OUT_CB);
-        tma_store3(&tm.po, xo, yo, b * 2 * C, sm.out + OUT_P);
+        tma_store3(&tm.co, xo, yo, b * C, sm.pm);
+        tma_store3(&tm.cbo, xo, yo, b * C, sm.pm + OUT_CB);
+        tma_store3(&tm.po, xo, yo, b * 2 * C, sm.pm + OUT_P);
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-    } else if (j == jlo - 1 && prow) {  // halo step: p+_y of row 4 jlo - 1 only
+    } else if (prow) {  // first step: p+_y of row 4 jlo - 1 only
       wait_pd();
       float qx[C], qy[C];
       dual_row(P - 1, 4 * jlo - 1, qx, qy);
 #pragma unroll
       for (int k = 0; k < C; ++k) qyp[k] = qy[k];
     }
-    // (e) step-2/3 inputs of chunk j (finalised in the next step)
+    // step-2/3 inputs of chunk j (finalised in the next step); the staging must have been read
     __syncwarp();
-    if (lane == 0 && j >= jlo && j <= jhi) load_pd(j);
-    // (f) rotate the accumulator ring
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int k = 0; k < C; ++k) S[i][k] = S[i + 2][k];
-#pragma unroll
-    for (int i = 4; i < 6; ++i)
-#pragma unroll
-      for (int k = 0; k < C; ++k) S[i][k] = pk(0.0f, 0.0f);
+    if (lane == 0 && j <= jhi) {
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      load_pd(j);
     }
-#if MSA_SWEEP_LOCKSTEP
-    __syncthreads();
-#endif
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // smem must outlive the reads
 }
@@ -476,7 +508,7 @@ SweepPlan make_plan(const MsaGeom& g, int BS, int slots) {
   pl.jfirst = g.row0 / P;
   pl.jend = (g.row0 + g.nrows - 1) / P + 1;
   const int nch = pl.jend - pl.jfirst;
-  static const int force_seg = getenv("MSA_SWEEP_SEG") ? atoi(getenv("MSA_SWEEP_SEG")) : 0;  // test hook (chunks)
+  static const int force_seg = MSA_HOOK("MSA_SWEEP_SEG") ? atoi(MSA_HOOK("MSA_SWEEP_SEG")) : 0;  // test hook (chunks)
   long long best = -1;
   int best_s = 1;
   for (int s = 1; s <= nch; ++s) {
@@ -525,8 +557,10 @@ cudaError_t launch_r(const MsaGeom& g, const MsaIterConsts& K, const SweepOm& om
   return cudaGetLastError();
 }
 
-// om for the half-disc H+ in the kernel's order (dx = 0: dy = 1..m; dx = 1..R-1: dy = -m..m).
-// Offsets absent from the driver's active table have phi = 0 exactly in fp32 and get om = 0.
+// Packed nom table (SweepOm): for column offset k, evaluation e of its shape (pass_own: M = m_0;
+// pass_cols: the shape of its group), the (lo, hi) halves hold -om/e_c of offsets (k, 2q - ya) and
+// (k, 2q + 1 - ya) when that pair is evaluated at this step under the offset's own half-height m_k,
+// else 0 (w = 0). Offsets absent from the driver's active table have phi = 0 in fp32 and get 0.
 template <int R>
 bool build_om(const MsaOffsetTable& T, SweepOm* om) {
   memset(om, 0, sizeof(*om));
@@ -535,21 +569,32 @@ bool build_om(const MsaOffsetTable& T, SweepOm* om) {
       if (T.dx[o] == dx && T.dy[o] == dy) return o;
     return -1;
   };
-  int n = 0;
-  for (int dx = 0; dx <= R - 1; ++dx) {
-    const int m = col_m(R, dx);
-    for (int dy = -m; dy <= m; ++dy) {
-      if (dx == 0 && dy <= 0) continue;
-      const int a = find(dx, dy), b = find(-dx, -dy);
-      if ((a < 0) != (b < 0)) return false;  // the window must be symmetric
-      if (a >= 0) {
-        if (T.oms[a] != T.oms[b]) return false;
-        om->v[n] = T.oms[a];
+  // the window must be symmetric (w_ij = w_ji needs om(delta) = om(-delta))
+  for (int o = 0; o < T.n; ++o) {
+    const int b = find(-T.dx[o], -T.dy[o]);
+    if (b < 0 || T.oms[b] != T.oms[o]) return false;
+  }
+  auto nom = [&](int dx, int dy) -> float {
+    const int a = find(dx, dy);
+    return a < 0 ? 0.0f : T.oms[a];
+  };
+  for (int k = 0; k <= R - 1; ++k) {
+    const int mk = col_m(R, k);
+    const bool own = k == 0;
+    const int M = own ? col_m(R, 0) : (R == 5 ? (k <= 2 ? 4 : 3) : col_m(R, 1));
+    const int ne = n_evals(M, own);
+    if (ne > MAX_EV) return false;
+    for (int e = 0; e < ne; ++e) {
+      const int ya = eval_at(M, own, e) >> 2, q = eval_at(M, own, e) & 3;
+      float h[2];
+      for (int s = 0; s < 2; ++s) {
+        const int yb = 2 * q + s;
+        h[s] = half_valid(mk, own, ya, yb) ? nom(k, yb - ya) : 0.0f;
       }
-      ++n;
+      om->v[k][e] = make_float2(h[0], h[1]);
     }
   }
-  return n <= 64;
+  return true;
 }
 
 template <int R>

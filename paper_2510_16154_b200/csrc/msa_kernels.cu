@@ -10,6 +10,8 @@
 // (readings in DESIGN.md §2; the per-function contract in include/msa.h).
 #include <math.h>
 
+#include <algorithm>
+
 #include "../../include/msa.h"
 #include "msa_internal.h"
 
@@ -465,4 +467,29 @@ int msa_sm_count() {
     return sms > 0 ? sms : 1;
   }();
   return n;
+}
+
+// ---------------------------------------------------------------- packed halo exchange (§8(e))
+// One launch moves every plane row-run of one exchange between the field ghost rows / edge rows and
+// the staging buffer, so each neighbour gets one ncclSend / ncclRecv per direction instead of one per
+// component plane and field. blockIdx.y = segment; float4 copies (row runs are 128-byte aligned).
+__global__ void k_halo_pack(const MsaHaloSeg* __restrict__ segs, float* __restrict__ buf, int to_buf) {
+  const MsaHaloSeg sg = segs[blockIdx.y];
+  float4* a = reinterpret_cast<float4*>(sg.ptr);
+  float4* b = reinterpret_cast<float4*>(buf + sg.off);
+  const long long n4 = sg.n >> 2;
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    if (to_buf)
+      b[i] = a[i];
+    else
+      a[i] = b[i];
+  }
+}
+
+cudaError_t msa_launch_halo_pack(const MsaHaloSeg* d_segs, int nseg, long long max_n, float* buf, int to_buf,
+                                 cudaStream_t s) {
+  if (nseg <= 0) return cudaSuccess;
+  const long long blocks = std::min<long long>(64, ((max_n >> 2) + 255) / 256);
+  k_halo_pack<<<dim3((unsigned)std::max<long long>(blocks, 1), (unsigned)nseg), 256, 0, s>>>(d_segs, buf, to_buf);
+  return cudaGetLastError();
 }

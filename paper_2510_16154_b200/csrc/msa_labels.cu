@@ -575,7 +575,7 @@ cudaError_t stage23(int n, int C, float delta, int32_t* count_dev, float* palett
   k_seg_mean<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_sum, S->seg_cnt, S->seg_mean, S->seg_parent, S->dscal);
   cudaMemsetAsync(S->cell_count, 0, sizeof(int32_t) * (NCELL_MAX + 1), st);
   cudaMemsetAsync(S->cell_fill, 0, sizeof(int32_t) * NCELL_MAX, st);
-  static const bool no_shortcut = getenv("MSA_LABELS_NO_SHORTCUT") != nullptr;  // debug hook
+  static const bool no_shortcut = MSA_HOOK("MSA_LABELS_NO_SHORTCUT") != nullptr;  // debug hook
   k_cell_setup<<<1, 32, 0, st>>>(S->dscal, C, (double)delta, no_shortcut ? 0 : 1, (CellGrid*)S->grid);
   k_seg_cell<<<nbN, T, 0, st>>>(S->scalars, C, S->seg_mean, (const CellGrid*)S->grid, S->seg_cell, S->cell_count);
   *launches += 3;
@@ -642,7 +642,7 @@ cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delt
   if ((e = stage23(N, C, delta, count_dev, palette_dev, max_k, S, st, launches))) return e;
   k_write_labels<<<nbN, T, 0, st>>>(N, S->parent, S->flag, S->seg_parent, S->seg_flag, labels_dev);
   ++*launches;
-  if (getenv("MSA_LABELS_DEBUG")) {  // debug hook: segment / cluster counts and the cell grid
+  if (MSA_HOOK("MSA_LABELS_DEBUG")) {  // debug hook: segment / cluster counts and the cell grid
     int32_t sc[2];
     double g[8];
     cudaMemcpyAsync(sc, S->scalars, sizeof(sc), cudaMemcpyDeviceToHost, st);

@@ -2,6 +2,8 @@
 same seeded inputs, and the parity metric of SURVEY.md §8(c) R17."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 import oracle
@@ -52,3 +54,16 @@ def config_case(name: str, H: int | None = None, W: int | None = None, B: int | 
                             iters_per_round=iters_per_round)
     img = synth.generate(cfg.recipe)
     return cfg, img, synth.solver_params(cfg)
+
+
+TESTING_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2510_16154_b200",
+                           "libmsa_testing.so")
+
+
+def testing_env(**hooks) -> dict:
+    """Environment of a subprocess that runs the testing build of the library (the same kernels plus the
+    environment test hooks, the experimental sweep K1 and the in-process NCCL transport):
+    the product libmsa.so reads no environment variable, so hook-driven cases must load this one."""
+    env = dict(os.environ, MSA_LIB=TESTING_LIB)
+    env.update({k: str(v) for k, v in hooks.items()})
+    return env

@@ -38,7 +38,7 @@ def test_library_is_sm100a():
 
 
 def test_abi_version(lib):
-    assert lib.msa_abi_version() == 2
+    assert lib.msa_abi_version() == 3
 
 
 def _params(**kw):
@@ -131,3 +131,20 @@ def test_binding_rejects_wrong_buffers():
     with pytest.raises(ValueError):
         f(torch.zeros(7), 6, "x")
     assert f(torch.zeros(6), 6, "x")[1] == 0
+
+
+def test_product_library_reads_no_environment_hook():
+    """no environment variable affects numerics. The A/B and test hooks (kernel variant,
+    summation order, scaled form, in-process NCCL transport, ...) are compiled only into the testing
+    build (-DMSA_TESTING); the product library contains none of their names and neither the
+    experimental sweep kernel nor the loopback transport."""
+    msa.build()
+    prod = open(os.path.join(ROOT, "paper_2510_16154_b200", "libmsa.so"), "rb").read()
+    test = open(os.path.join(ROOT, "paper_2510_16154_b200", "libmsa_testing.so"), "rb").read()
+    hooks = [b"MSA_K1", b"MSA_NO_SCALED", b"MSA_NCCL_LOOPBACK", b"MSA_LARGE_FROM", b"MSA_LARGE_NOSPLIT",
+             b"MSA_DAL_GENERIC", b"MSA_FORCE_GENERIC", b"MSA_LABELS_PARTS", b"MSA_DAL_CHECKPOINT", b"MSA_NO_GRAPH"]
+    for h in hooks:
+        assert h not in prod, h
+        assert h in test, h
+    assert b"k_iter_sweep" not in prod and b"k_iter_sweep" in test
+    assert b"loopback" not in prod

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import oracle
+from _harness import testing_env
 
 pytestmark = pytest.mark.gpu
 msa = pytest.importorskip("paper_2510_16154_b200")
@@ -103,7 +104,7 @@ np.savez(sys.argv[2], J=np.array([J]), g=g)
     spec = dict(seed=R + C, H=29, W=37, C=C, R=R, M=6, kernel=kernel)
     outs = []
     for variant in ("large", "generic", "large_split"):
-        env = dict(os.environ)
+        env = testing_env()
         env.pop("MSA_DAL_GENERIC", None)
         env.pop("MSA_LARGE_NOSPLIT", None)
         if variant == "generic":
@@ -152,7 +153,7 @@ np.savez(sys.argv[2], J=np.array([J]), g=g)
     spec = dict(seed=S + R, R=R, cost=cost)
     outs = []
     for ck in (None, S):
-        env = dict(_os.environ)
+        env = testing_env()
         env.pop("MSA_DAL_CHECKPOINT", None)
         if ck is not None:
             env["MSA_DAL_CHECKPOINT"] = str(ck)

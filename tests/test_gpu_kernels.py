@@ -15,15 +15,19 @@ import sys
 
 import numpy as np
 import pytest
+from _harness import testing_env
 
 pytestmark = pytest.mark.gpu
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 
-def _run(spec, variant: str, tmp_path, seg: int = 0, split: bool = False, direct: bool = False):
-    out = str(tmp_path / f"{variant}_{seg}_{int(split)}_{int(direct)}.npz")
-    env = dict(os.environ)
+def _run(spec, variant: str, tmp_path, seg: int = 0, split: bool = False, direct: bool = False, rows_per_thread: int = 0):
+    out = str(tmp_path / f"{variant}_{seg}_{int(split)}_{int(direct)}_{rows_per_thread}.npz")
+    env = testing_env()
+    env.pop("MSA_K1_P", None)
+    if rows_per_thread:
+        env["MSA_K1_P"] = str(rows_per_thread)
     env.pop("MSA_FORCE_GENERIC", None)
     env.pop("MSA_NO_SCALED", None)
     if direct:
@@ -67,6 +71,23 @@ def test_tile_equals_generic_bitwise(shape, R, ker, tmp_path):
     spec = _spec(shape, R, ker)
     a = _run(spec, "generic", tmp_path)
     b = _run(spec, "tile", tmp_path)
+    for k in ("c", "cbar", "p", "mu"):
+        assert np.array_equal(a[k], b[k]), (k, float(np.max(np.abs(a[k] - b[k]))))
+
+
+# The bench configuration (cfg4, 4096^2) runs the tiled kernel with P = 4 rows per thread (32 x 32
+# tiles), which the launcher picks only when the image has at least 2 x 148 tiles; small test images
+# pick P = 2. MSA_K1_P=4 forces the bench's P = 4 tiles on small shapes: bitwise equal to the generic
+# kernel across two multiplier rounds (5 iterations, K = 2), ragged and tile-aligned.
+P4_CASES = [((1, 100, 70, 3), 5, 0), ((1, 64, 64, 3), 5, 1), ((2, 45, 61, 3), 3, 0), ((1, 130, 33, 3), 4, 0),
+            ((1, 70, 97, 1), 5, 0), ((1, 41, 40, 2), 2, 1), ((1, 7, 300, 3), 5, 0)]
+
+
+@pytest.mark.parametrize("shape,R,ker", P4_CASES)
+def test_tile_p4_equals_generic_bitwise_across_rounds(shape, R, ker, tmp_path):
+    spec = _spec(shape, R, ker, iters=5)
+    a = _run(spec, "generic", tmp_path)
+    b = _run(spec, "tile", tmp_path, rows_per_thread=4)
     for k in ("c", "cbar", "p", "mu"):
         assert np.array_equal(a[k], b[k]), (k, float(np.max(np.abs(a[k] - b[k]))))
 

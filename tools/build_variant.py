@@ -7,7 +7,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2510_16154_b200 import _build  # noqa: E402
 
 tag = sys.argv[1]
-defs = tuple(a for a in sys.argv[2:] if not a.startswith("-"))
+defs = ("MSA_TESTING",) + tuple(a for a in sys.argv[2:] if not a.startswith("-"))
 flags = tuple(a for a in sys.argv[2:] if a.startswith("-"))  # raw nvcc flags, e.g. -Xptxas=...
 out_dir = os.path.join(_build.PKG, "variants")
 lib = os.path.join(out_dir, f"libmsa_{tag}.so")
