@@ -60,7 +60,7 @@ TESTING_LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__fil
                            "libmsa_testing.so")
 
 
-def testing_env(**hooks) -> dict:
+def hook_env(**hooks) -> dict:
     """Environment of a subprocess that runs the testing build of the library (the same kernels plus the
     environment test hooks, the experimental sweep K1 and the in-process NCCL transport):
     the product libmsa.so reads no environment variable, so hook-driven cases must load this one."""

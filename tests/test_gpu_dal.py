@@ -6,7 +6,7 @@ import numpy as np
 import pytest
 
 import oracle
-from _harness import testing_env
+from _harness import hook_env
 
 pytestmark = pytest.mark.gpu
 msa = pytest.importorskip("paper_2510_16154_b200")
@@ -104,7 +104,7 @@ np.savez(sys.argv[2], J=np.array([J]), g=g)
     spec = dict(seed=R + C, H=29, W=37, C=C, R=R, M=6, kernel=kernel)
     outs = []
     for variant in ("large", "generic", "large_split"):
-        env = testing_env()
+        env = hook_env()
         env.pop("MSA_DAL_GENERIC", None)
         env.pop("MSA_LARGE_NOSPLIT", None)
         if variant == "generic":
@@ -153,7 +153,7 @@ np.savez(sys.argv[2], J=np.array([J]), g=g)
     spec = dict(seed=S + R, R=R, cost=cost)
     outs = []
     for ck in (None, S):
-        env = testing_env()
+        env = hook_env()
         env.pop("MSA_DAL_CHECKPOINT", None)
         if ck is not None:
             env["MSA_DAL_CHECKPOINT"] = str(ck)
@@ -181,4 +181,43 @@ def test_dal_admm_matches_oracle(R, C):
     assert len(recs) == outer
     np.testing.assert_allclose(Jh, Jho, rtol=1e-4)
     np.testing.assert_allclose(e, eo, rtol=2e-3, atol=1e-6)
+    np.testing.assert_allclose(mu, muo, rtol=0, atol=2e-4 * max(1.0, float(np.max(np.abs(muo)))))
+
+
+def test_dal_stopping_rules_match_oracle():
+    """Remark 3.4 on the GPU: with the paper's eta = 1e-10 the run ends at the same
+    iteration as the oracle's (cost stationarity), and a one-point box stops it before any step
+    (projected gradient, criterion 2)."""
+    rng, I, sp, eps = _case(H=16, W=16, C=3, R=15, M=6, seed=21)
+    H, W, C = I.shape
+    kw = dict(iters=12, max_ls=20, sigma0=1e3, b=0.5, c=1e-4, eta=1e-10)
+    with msa.Solver(msa.Params.from_solver(1, H, W, C, sp), I[None]) as s:
+        e, Jh, sh, stop = s.dal(msa.DalParams(steps=6, **kw), eps, return_stop=True)
+        e2, Jh2, sh2, stop2 = s.dal(msa.DalParams(steps=6, iters=5, ex_lo=40.0, ex_hi=40.0, ec_lo=10.0, ec_hi=10.0,
+                                                  eta_grad=1e-30), eps, return_stop=True)
+    eo, Jho, sho, stopo = oracle.dal(_oracle_params(I, sp), oracle.DalParams(M=6, **kw), eps, I.astype(np.float64),
+                                     return_stop=True)
+    assert stop == stopo, (stop, stopo)
+    np.testing.assert_allclose(Jh, Jho, rtol=1e-4)
+    assert stop2 == (0, 2) and np.all(e2[:, 0] == 40.0) and np.all(e2[:, 1] == 10.0)
+
+
+def test_dal_admm_gamma_search_matches_oracle():
+    """The remark after Algorithm 2: the ascent step gamma^(j) chosen by the two-way
+    Armijo search on Phi(mu) = min_v L(c(mu), v, mu). The GPU (fp32 states, host search) takes the same
+    steps as oracle.dal_admm(gamma_search=True) (pinned by tests/test_oracle_dal.py::test_D7) and ends
+    at the same multiplier."""
+    rng, I, sp, eps = _case(H=16, W=16, C=2, R=12, M=4, seed=33)
+    sp = dict(sp, rho=0.4, gamma=0.05)
+    H, W, C = I.shape
+    kw = dict(iters=2, max_ls=8, sigma0=1e3, b=0.5, c=1e-4, ex_lo=8.0, ex_hi=1100.0, ec_lo=2.0, ec_hi=1100.0)
+    outer = 2
+    with msa.Solver(msa.Params.from_solver(1, H, W, C, sp), I[None]) as s:
+        e, Jh, recs, gh = s.dal_admm(msa.DalParams(steps=4, cost=1, gamma_ls=1, **kw), eps, outer, return_gamma=True)
+        mu = s.get_field(msa.FIELD_MU)[0]
+    eo, Jho, co, vo, muo, gho = oracle.dal_admm(_oracle_params(I, sp), oracle.DalParams(M=4, cost=1, **kw), eps,
+                                                I.astype(np.float64), outer, gamma_search=True)
+    np.testing.assert_array_equal(gh, gho)
+    assert np.all(gh > 0)
+    np.testing.assert_allclose(Jh, Jho, rtol=1e-4)
     np.testing.assert_allclose(mu, muo, rtol=0, atol=2e-4 * max(1.0, float(np.max(np.abs(muo)))))

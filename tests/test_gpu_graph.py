@@ -10,7 +10,7 @@ import sys
 
 import numpy as np
 import pytest
-from _harness import testing_env
+from _harness import hook_env
 
 pytestmark = pytest.mark.gpu
 msa = pytest.importorskip("paper_2510_16154_b200")
@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 def _run(spec, graph, tmp_path):
     out = str(tmp_path / f"g{int(graph)}.npz")
-    env = testing_env()
+    env = hook_env()
     for k in ("MSA_NO_GRAPH", "MSA_K1", "MSA_FORCE_GENERIC"):
         env.pop(k, None)
     if not graph:

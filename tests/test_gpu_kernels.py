@@ -15,7 +15,7 @@ import sys
 
 import numpy as np
 import pytest
-from _harness import testing_env
+from _harness import hook_env
 
 pytestmark = pytest.mark.gpu
 
@@ -24,7 +24,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 def _run(spec, variant: str, tmp_path, seg: int = 0, split: bool = False, direct: bool = False, rows_per_thread: int = 0):
     out = str(tmp_path / f"{variant}_{seg}_{int(split)}_{int(direct)}_{rows_per_thread}.npz")
-    env = testing_env()
+    env = hook_env()
     env.pop("MSA_K1_P", None)
     if rows_per_thread:
         env["MSA_K1_P"] = str(rows_per_thread)

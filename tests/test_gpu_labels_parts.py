@@ -10,7 +10,7 @@ import sys
 
 import numpy as np
 import pytest
-from _harness import testing_env
+from _harness import hook_env
 
 pytestmark = pytest.mark.gpu
 
@@ -19,7 +19,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 def _run(spec, parts, tmp_path):
     out = str(tmp_path / f"lab_{parts}.npz")
-    env = testing_env()
+    env = hook_env()
     if parts:
         env["MSA_LABELS_PARTS"] = str(parts)
     else:

@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 import oracle
-from _harness import rel_err_per_pixel, testing_env
+from _harness import rel_err_per_pixel, hook_env
 
 pytestmark = pytest.mark.gpu
 msa = pytest.importorskip("paper_2510_16154_b200")
@@ -23,7 +23,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 def _run(spec, variant, tmp_path):
     out = str(tmp_path / f"{variant}.npz")
-    env = testing_env(MSA_K1=variant)
+    env = hook_env(MSA_K1=variant)
     env.pop("MSA_FORCE_GENERIC", None)
     subprocess.run([sys.executable, os.path.join(HERE, "_run_case.py"), json.dumps(spec), out], check=True, env=env)
     return np.load(out)

@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 import oracle
-from _harness import config_case, rel_err_per_pixel, run_oracle, testing_env
+from _harness import config_case, rel_err_per_pixel, run_oracle, hook_env
 
 pytestmark = pytest.mark.gpu
 
@@ -95,7 +95,7 @@ def test_lin_split_bitwise(tmp_path):
                             gamma=2.5 / 69, iters_per_round=2, rounds=1, scheme=LIN))
     outs = []
     for split in (False, True):
-        env = testing_env()
+        env = hook_env()
         env.pop("MSA_K1_SPLIT", None)
         if split:
             env["MSA_K1_SPLIT"] = "1"
@@ -121,7 +121,7 @@ def test_lin_tile_equals_generic_bitwise(shape, R, tmp_path):
                             gamma=2.5 * h, iters_per_round=2, rounds=1, scheme=LIN))
     outs = []
     for variant in ("generic", "tile"):
-        env = testing_env(MSA_K1=variant)
+        env = hook_env(MSA_K1=variant)
         env.pop("MSA_FORCE_GENERIC", None)
         out = str(tmp_path / f"{variant}.npz")
         subprocess.run([sys.executable, os.path.join(HERE, "_run_case.py"), json.dumps(spec), out], check=True,

@@ -12,7 +12,7 @@ import subprocess
 import sys
 
 import pytest
-from _harness import testing_env
+from _harness import hook_env
 
 pytestmark = pytest.mark.gpu
 msa = pytest.importorskip("paper_2510_16154_b200")
@@ -20,7 +20,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 
 
 def _run(spec, **env_extra):
-    env = testing_env(MSA_NCCL_LOOPBACK="1")
+    env = hook_env(MSA_NCCL_LOOPBACK="1")
     for k in ("MSA_NO_OVERLAP", "MSA_K1", "MSA_FORCE_GENERIC", "MSA_K1_SPLIT", "MSA_LABELS_PARTS"):
         env.pop(k, None)
     env.update(env_extra)
