@@ -38,6 +38,7 @@ METRIC = "pixel-iterations/sec (solver iterations x pixels) at 1/2/4/8 B200; % H
 UNIT = "pixel-iterations/s"
 WORKLOAD = "cfg4"
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+FP32_LANE_OPS_PER_CLK = 126.6  # measured packed FFMA2 rate per SM (tools/fp32_microbench.cu, round 1)
 
 
 def _env_int(name, default):
@@ -117,6 +118,17 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
+def _cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def _cpu_threads():
     n = os.environ.get("OMP_NUM_THREADS")
     return int(n) if n else (os.cpu_count() or 1)
@@ -181,7 +193,7 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": _config(cfg, args.gpus),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle",
-                             "sample": sample},
+                             "sample": sample, "cpu_model": _cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -258,9 +270,9 @@ def main():
     for _ in range(max(args.warmup, 0)):
         step()
     barrier()
+    # timed region: the production path (msa_solve replays its CUDA graph; no per-launch events)
     clocks = ClockSampler(local)
     clocks.start()
-    solver.set_timing(True)
     launches0 = solver.query().launches
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
@@ -270,9 +282,25 @@ def main():
     barrier()
     ms_local = e0.elapsed_time(e1)
     launches = solver.query().launches - launches0
-    tim = solver.get_timing()
-    solver.set_timing(False)
     clk = clocks.stop()
+    # separate instrumented pass (msa_set_timing: CUDA events around every K1 batch, round and halo
+    # exchange, direct launches) for the kernel-level roofline and the halo time per rank
+    barrier()
+    solver.set_timing(True)
+    i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    i0.record(stream)
+    step()
+    i1.record(stream)
+    barrier()
+    inst_ms = i0.elapsed_time(i1)
+    tim = solver.get_timing()
+    qi = solver.query()
+    halo = {"ms_per_step": qi.halo_ms, "exchanges": int(qi.halo_exchanges)}
+    solver.set_timing(False)
+    halo_all = [halo]
+    if dist:
+        halo_all = [None] * world
+        dist.all_gather_object(halo_all, halo)
     ms = ms_local
     if dist:
         t = torch.tensor([ms_local], device="cuda")
@@ -292,15 +320,17 @@ def main():
     achieved = alg_bytes / (k1_avg_ms * 1e-3) / 1e9
     peak, peak_src = _hbm_peak()
     traffic, _tr = _k1_traffic()
-    k1_share = tim["iter_ms"] / ms_local if ms_local > 0 else None
+    k1_share = tim["iter_ms"] / inst_ms if inst_ms > 0 else None
     n_off = info.active_offsets
     alg_ops = (n_off * (3 * C + 4) + 27 * C + 2) * own_px
     sm_count = torch.cuda.get_device_properties(local).multi_processor_count
-    alu_peak = sm_count * 128 * 1965e6 / 1e12  # T FP32 lane-ops/s at clocks.max.sm
+    # FP32 peak at this run's median SM clock with the measured packed-FFMA rate per SM
+    # (tools/fp32_microbench.cu: 126.6 lane-ops/clk/SM of the nominal 128)
+    sm_mhz = clk.get("sm_mhz") or 1965.0
+    alu_peak = sm_count * FP32_LANE_OPS_PER_CLK * sm_mhz * 1e6 / 1e12
     alu_achieved = alg_ops / (k1_avg_ms * 1e-3) / 1e12
     hbm_time = alg_bytes / (peak * 1e9)
     alu_time = alg_ops / (alu_peak * 1e12)
-    bound = "alu" if alu_time > hbm_time else "hbm"
 
     # end to end through the public API with host buffers (pinned), H2D + D2H inside the timed region
     e2e = None
@@ -342,7 +372,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, sample = cpu_oracle_rate(img, sp)
-        cpu = {"value": rate, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle", "sample": sample}
+        cpu = {"value": rate, "unit": UNIT, "cores": _cpu_threads(), "kind": "oracle", "sample": sample,
+               "cpu_model": _cpu_model()}
 
     if rank == 0:
         line = {
@@ -351,20 +382,23 @@ def main():
             "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded generator synth/, BASELINE config 4 recipe)",
             "config": _config(cfg, world),
-            "roofline": ({"bound": "alu", "achieved": alu_achieved, "peak": alu_peak,
-                          "unit": "T FP32 lane-ops/s", "frac": alu_achieved / alu_peak,
-                          "peak_source": f"derived: {sm_count} SMs x 128 FP32 lanes x 1965 MHz clocks.max.sm"}
-                         if bound == "alu" else
-                         {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                          "peak_source": peak_src}) | {
-                "kernel": "K1 msa_iter (fused agent + primal-dual iteration)", "traffic": traffic,
-                "alg_bytes_per_launch": alg_bytes, "alg_ops_per_launch": alg_ops, "k1_avg_ms": k1_avg_ms,
-                "k1_launches": tim["iter_launches"], "k1_share_of_step": k1_share,
-                "hbm": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                        "frac_of_8TBs_spec": achieved / 8000.0, "peak_source": peak_src},
-                "alu": {"achieved": alu_achieved, "peak": alu_peak, "unit": "T FP32 lane-ops/s",
-                        "frac": alu_achieved / alu_peak},
-                "floor_ms": {"hbm": hbm_time * 1e3, "alu": alu_time * 1e3}},
+            # north_star's metric: the fraction of measured HBM bandwidth (algorithmic bytes); the FP32
+            # pipe is what binds K1 at R = 5 RGB (see "alu" and floor_ms)
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src,
+                         "kernel": "K1 msa_iter (fused agent + primal-dual iteration)", "traffic": traffic,
+                         "alg_bytes_per_launch": alg_bytes, "alg_ops_per_launch": alg_ops, "k1_avg_ms": k1_avg_ms,
+                         "k1_launches": tim["iter_launches"], "k1_share_of_step": k1_share,
+                         "k1_timing": "separate instrumented step after the timed region (CUDA events per K1 batch)",
+                         "frac_of_8TBs_spec": achieved / 8000.0,
+                         "alu": {"achieved": alu_achieved, "peak": alu_peak, "unit": "T FP32 lane-ops/s",
+                                 "frac": alu_achieved / alu_peak,
+                                 "peak_source": f"measured FFMA2 rate {FP32_LANE_OPS_PER_CLK} lane-ops/clk/SM "
+                                                f"(tools/fp32_microbench.cu) x {sm_count} SMs x median SM clock "
+                                                f"{sm_mhz:.0f} MHz of this run"},
+                         "floor_ms": {"hbm": hbm_time * 1e3, "alu": alu_time * 1e3},
+                         "binding": "alu" if alu_time > hbm_time else "hbm"},
+            "halo": halo_all if world > 1 else None,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(launches),

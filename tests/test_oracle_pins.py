@@ -578,3 +578,26 @@ def test_crop_locality_exact():
                                       **base), I[cj0:cj1, ci0:ci1])
     crop.run(n)
     assert np.array_equal(crop.c[j0 - cj0:j1 - cj0, i0 - ci0:i1 - ci0], full.c[j0:j1, i0:i1])
+
+
+def test_golden_generator_reproduces_stored_vectors():
+    """Provenance of G1/G2: the committed independent NumPy transcription of the §8(c) block
+    (tools/golden_numpy.py, which imports neither oracle/ nor the CUDA package) regenerates every stored
+    value to 1e-12."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(GOLDEN), "..", "tools"))
+    import golden_numpy as gn
+    g1 = json.load(open(os.path.join(GOLDEN, "G1_grey_nonsquare.json")))
+    g2 = json.load(open(os.path.join(GOLDEN, "G2_rgb_coupled.json")))
+    a, b = gn.G1(), gn.G2()
+    for k in ("c_after_iteration_1", "c_after_2_rounds", "mu_x_after_2_rounds", "mu_y_after_2_rounds"):
+        np.testing.assert_allclose(np.array(a[k], float), np.array(g1[k], float), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(np.array(b["c_rows_0_and_2"]), np.array(g2["c_rows_0_and_2"]), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(np.array(b["c_row_2"]), np.array(g2["c_rows_0_and_2"]), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(np.array(b["c_row_1"]), np.array(g2["c_row_1"]), rtol=0, atol=1e-12)
+    for got, want in ((a["round_stats"], g1["round_stats"]), (b["round_stats"], g2["round_stats"])):
+        for r, rec in enumerate(want):
+            for k, v in rec.items():
+                assert abs(got[r][k] - v) <= 1e-12 * max(1.0, abs(v)), (r, k)
+    assert a["expect_tau"] == pytest.approx(g1["params"]["expect_tau"], rel=1e-15)
+    assert b["expect_tau"] == pytest.approx(g2["params"]["expect_tau"], rel=1e-15)
