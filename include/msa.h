@@ -214,6 +214,13 @@ int msa_solve_until(msa_ctx* ctx, double tol_residual, double tol_gap, int32_t m
 int msa_labels(msa_ctx* ctx, float delta, int32_t* labels, int32_t* n_clusters, float* palette, int32_t max_k,
                int out_on_device);
 
+/* Decision margin of the quantisation rule's stage (i) on the current c (reading R17): per image,
+ * min over the 4-neighbour pairs of | ||c_a - c_b||_inf - delta | in fp32, the distance of the closest
+ * comparison from flipping; labels that differ between two fields closer than margin/2 cannot come
+ * from stage (i). margin: host float [nimages] (this rank's images; rows mode: over the whole image,
+ * all-reduced). Synchronises. (ABI 3) */
+int msa_label_margin(msa_ctx* ctx, float delta, float* margin);
+
 /* Copies a field of this rank's rows/images out in the ABI layout ([nimages][nrows][W][C]
  * or [..][2C] for p, mu). row0/nrows may be NULL. Synchronises. */
 int msa_get_field(msa_ctx* ctx, int32_t which, float* out, int out_on_device, int32_t* row0, int32_t* nrows);

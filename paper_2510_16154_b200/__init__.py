@@ -27,7 +27,7 @@ SCHEME_CP_ROUNDS, SCHEME_LINEARISED_ADMM = 0, 1
 # every symbol include/msa.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["msa_abi_version", "msa_last_error", "msa_workspace_bytes", "msa_partition_rows",
                "msa_nccl_unique_id", "msa_halo_plan", "msa_init", "msa_reset", "msa_step", "msa_solve",
-               "msa_solve_until", "msa_labels",
+               "msa_solve_until", "msa_labels", "msa_label_margin",
                "msa_get_field", "msa_set_field", "msa_get_stats", "msa_state_bytes", "msa_get_state",
                "msa_set_state", "msa_query", "msa_set_timing", "msa_get_timing", "msa_dal", "msa_dal_gradient", "msa_dal_admm",
                "msa_sync", "msa_free"]
@@ -183,6 +183,7 @@ def lib():
             "msa_solve": ([P, V], ctypes.c_int),
             "msa_solve_until": ([P, ctypes.c_double, ctypes.c_double, I32, V, PI32, PI32], ctypes.c_int),
             "msa_labels": ([P, ctypes.c_float, V, V, V, I32, ctypes.c_int], ctypes.c_int),
+            "msa_label_margin": ([P, ctypes.c_float, V], ctypes.c_int),
             "msa_get_field": ([P, I32, V, ctypes.c_int, PI32, PI32], ctypes.c_int),
             "msa_set_field": ([P, I32, V, ctypes.c_int], ctypes.c_int),
             "msa_get_stats": ([P, V, I32, PI32], ctypes.c_int),
@@ -385,6 +386,12 @@ class Solver:
         return lab, cnt, pal
 
     # -- fields and state
+    def label_margin(self, delta: float = 0.1) -> np.ndarray:
+        """Stage-(i) decision margin of Q(c; delta) per image (reading R17; msa_label_margin)."""
+        out = np.zeros(self.query().nimages, dtype=np.float32)
+        _check(lib().msa_label_margin(self._ctx, ctypes.c_float(delta), out.ctypes.data))
+        return out
+
     def get_field(self, which: int = FIELD_C, out=None) -> np.ndarray:
         info = self.query()
         C = self.params.channels

@@ -1321,6 +1321,37 @@ int labels_parts(msa_ctx* x, int b, float delta, int nparts, int32_t* labels_dev
   return MSA_OK;
 }
 
+int msa_label_margin(msa_ctx* x, float delta, float* margin) {
+  if (!x || !margin) return set_err(MSA_EINVAL, "NULL argument");
+  if (!(delta >= 0) || !isfinite(delta)) return set_err(MSA_EINVAL, "delta must be finite and >= 0");
+  const bool dist = x->prm.world > 1 && x->prm.shard == MSA_SHARD_ROWS;
+  const MsaGeom& g = x->g;
+  int rc;
+  if (dist && (rc = halo_exchange(x, MSA_HALO_ROUND)) != MSA_OK) return rc;  // the c row above the slab
+  unsigned int* d = nullptr;
+  CUDA_TRY(cudaMallocAsync((void**)&d, sizeof(unsigned int) * g.nb, x->stream));
+  std::vector<unsigned int> h(g.nb, 0x7f800000u);  // +inf
+  cudaError_t e = cudaMemcpyAsync(d, h.data(), sizeof(unsigned int) * g.nb, cudaMemcpyHostToDevice, x->stream);
+  const int up_rows = g.nrows + (dist && g.row0 + g.nrows < g.H ? 1 : 0);
+  for (int b = 0; e == cudaSuccess && b < g.nb; ++b)
+    e = msa_launch_label_margin(g, x->c[x->cur], b, g.row0, g.nrows, up_rows, delta, d + b, x->stream);
+  if (e == cudaSuccess && dist) {
+    // min over slabs: the float bits of non-negative values order like unsigned integers
+    ncclResult_t r = g_nccl.AllReduce(d, d, g.nb, ncclUint32, ncclMin, x->comm, x->stream);
+    if (r != ncclSuccess) {
+      cudaFreeAsync(d, x->stream);
+      return set_err(MSA_ENCCL, "margin all-reduce: %s", g_nccl.GetErrorString(r));
+    }
+  }
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h.data(), d, sizeof(unsigned int) * g.nb, cudaMemcpyDeviceToHost, x->stream);
+  cudaFreeAsync(d, x->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
+  if (e != cudaSuccess) return set_err(MSA_ECUDA, "label margin: %s", cudaGetErrorString(e));
+  x->launches += g.nb;
+  for (int b = 0; b < g.nb; ++b) memcpy(&margin[b], &h[b], sizeof(float));
+  return MSA_OK;
+}
+
 int msa_labels(msa_ctx* x, float delta, int32_t* labels, int32_t* n_clusters, float* palette, int32_t max_k,
                int out_on_device) {
   if (!x) return set_err(MSA_EINVAL, "ctx is NULL");

@@ -117,6 +117,10 @@ cudaError_t msa_launch_halo_pack(const MsaHaloSeg* d_segs, int nseg, long long m
                                  cudaStream_t s);
 
 // Labels (msa_labels.cu): Q(c; delta) of reading R16 on image b of the planar field c.
+// Stage (i) decision margin (R17): min | ||c_a - c_b||_inf - delta | over the 4-neighbour pairs whose
+// lower / left pixel lies in rows [r0, r0 + nr); min-reduced into *out as float bits (init 0x7f800000).
+cudaError_t msa_launch_label_margin(const MsaGeom& g, const float* c, int b, int r0, int nr, int up_rows, float delta,
+                                    unsigned int* out, cudaStream_t s);
 struct MsaLabelScratch;
 cudaError_t msa_labels_image(const MsaGeom& g, const float* c, int b, float delta, int32_t* labels_dev,
                              int32_t* count_dev, float* palette_dev, int max_k, MsaLabelScratch** scratch,

@@ -722,3 +722,37 @@ cudaError_t msa_labels_relabel(int npix, const int32_t* seg_of_pix, int seg_off,
   k_relabel<<<(npix + 255) / 256, 256, 0, st>>>(npix, seg_of_pix, seg_off, cl_of_seg, labels);
   return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------- decision margin of stage (i) (R17)
+// min over the 4-neighbour pairs (right, up) with the lower / left pixel in rows [r0, r0 + nr) of
+// | ||c_a - c_b||_inf - delta | in fp32 (the comparison stage (i) makes, k_edges), as the bits of a
+// non-negative float (unsigned order = float order) min-reduced into *out. up_rows = rows above r0 that
+// may be read (nr, or nr + 1 when the row above the slab is valid: rows mode after the halo exchange).
+__global__ void k_margin(MsaGeom g, const float* __restrict__ c, int b, int r0, int nr, int up_rows, float delta,
+                         unsigned int* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  float m = INFINITY;
+  if (i < g.W && jl < nr) {
+    const int j = r0 + jl;
+    const bool right = i + 1 < g.W, up = jl + 1 < up_rows;
+    float dr = 0.0f, du = 0.0f;
+    for (int k = 0; k < g.C; ++k) {
+      const float a = c[msa_idx(g, b, k, g.C, j, i)];
+      if (right) dr = fmaxf(dr, fabsf(__fsub_rn(a, c[msa_idx(g, b, k, g.C, j, i + 1)])));
+      if (up) du = fmaxf(du, fabsf(__fsub_rn(a, c[msa_idx(g, b, k, g.C, j + 1, i)])));
+    }
+    if (right) m = fminf(m, fabsf(__fsub_rn(dr, delta)));
+    if (up) m = fminf(m, fabsf(__fsub_rn(du, delta)));
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fminf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m < INFINITY) atomicMin(out, __float_as_uint(m));
+}
+
+cudaError_t msa_launch_label_margin(const MsaGeom& g, const float* c, int b, int r0, int nr, int up_rows, float delta,
+                                    unsigned int* out, cudaStream_t s) {
+  if (nr <= 0) return cudaSuccess;
+  dim3 blk(32, 8), grd((g.W + 31) / 32, (nr + 7) / 8);
+  k_margin<<<grd, blk, 0, s>>>(g, c, b, r0, nr, up_rows, delta, out);
+  return cudaGetLastError();
+}

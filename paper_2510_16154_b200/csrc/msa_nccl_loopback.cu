@@ -18,6 +18,7 @@
 #include <memory>
 #include <mutex>
 #include <random>
+#include <algorithm>
 #include <vector>
 
 #include "msa_internal.h"
@@ -201,9 +202,18 @@ void sum_into(const std::vector<std::vector<char>>& in, std::vector<char>& out, 
 
 ncclResult_t lb_all_reduce(const void* send, void* recv, size_t count, ncclDataType_t t, ncclRedOp_t op,
                            ncclComm_t comm, cudaStream_t st) {
-  if (op != ncclSum) return ncclInvalidArgument;
+  if (op != ncclSum && !(op == ncclMin && t == ncclUint32)) return ncclInvalidArgument;
   const size_t b = count * type_size(t);
   if (!b && count) return ncclInvalidArgument;
+  if (op == ncclMin)  // msa_label_margin: min of float bits as uint32
+    return collective(reinterpret_cast<Comm*>(comm), send, b, recv, b, st,
+                      [&](const std::vector<std::vector<char>>& in, std::vector<char>& out) {
+                        for (size_t k = 0; k < count; ++k) {
+                          uint32_t m = 0xffffffffu;
+                          for (const auto& r : in) m = std::min(m, reinterpret_cast<const uint32_t*>(r.data())[k]);
+                          reinterpret_cast<uint32_t*>(out.data())[k] = m;
+                        }
+                      });
   return collective(reinterpret_cast<Comm*>(comm), send, b, recv, b, st,
                     [&](const std::vector<std::vector<char>>& in, std::vector<char>& out) {
                       switch (t) {
