@@ -9,10 +9,11 @@ Per image it stores (tests/golden/full_<case>.npz):
   input_sha256   hash of the float32 input [B][H][W][C] the generator drew (so the GPU test knows it
                  runs on the same image)
   idx            sampled pixel indices (j, i): the four corners, points on each border, 4096 uniform
-  c              the oracle's final colour field at those pixels (fp64) [B][n][C]
+  c              the oracle's final colour field at those pixels (fp64; fp32 for batches) [B][n][C]
   stats          the round records (pre-update mu) [B][rounds][8 + C]
   labels         Q(c; delta) of the oracle's final field rounded to fp32 (reading R16), full map
-                 [B][H][W] (uint16 when the count allows it)
+                 [min(B, 4)][H][W] (uint16 when the count allows it)
+  labels_sampled (batches) the labels at idx for every image [B][n]
   count          cluster counts [B]
   margin         R17's decision margin of Q on the oracle field: min |d - delta| over the
                  neighbour comparisons of stage (i) [B]
@@ -39,6 +40,7 @@ import synth  # noqa: E402
 
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 N_UNIFORM = 4096
+FULL_MAPS = 4  # full label maps stored per case (the rest sampled: keeps the files small)
 
 
 def cases() -> dict:
@@ -93,9 +95,14 @@ def make(name: str, cfg) -> dict:
     lab = np.stack(labs)
     lab = lab.astype(np.uint16) if lab.max() < 65535 else lab
     path = os.path.join(GOLDEN, f"full_{name}.npz")
+    extra = {}
+    if B > FULL_MAPS:  # batches: full label maps of the first FULL_MAPS images, sampled labels of all
+        extra["labels_sampled"] = np.stack([lab[b][idx[:, 0], idx[:, 1]] for b in range(B)])
+        lab = lab[:FULL_MAPS]
+        out_c = out_c.astype(np.float32)  # 6e-8 relative rounding against the 1e-4 gate; 4x smaller
     np.savez_compressed(path, input_sha256=np.frombuffer(hashlib.sha256(img.tobytes()).digest(), np.uint8),
                         idx=idx, c=out_c, stats=out_stats, labels=lab, count=np.array(counts, np.int32),
-                        margin=np.array(margins), iters=np.int64(cfg.iters), rounds=np.int64(cfg.rounds))
+                        margin=np.array(margins), iters=np.int64(cfg.iters), rounds=np.int64(cfg.rounds), **extra)
     meta = dict(case=name, shape=[B, H, W, C], iters=cfg.iters, rounds=cfg.rounds, counts=counts,
                 margin_min=min(margins), oracle_seconds=round(time.time() - t0, 1), cores=os.cpu_count(),
                 bytes=os.path.getsize(path))
