@@ -64,6 +64,6 @@ def hook_env(**hooks) -> dict:
     """Environment of a subprocess that runs the testing build of the library (the same kernels plus the
     environment test hooks, the experimental sweep K1 and the in-process NCCL transport):
     the product libmsa.so reads no environment variable, so hook-driven cases must load this one."""
-    env = dict(os.environ, MSA_LIB=TESTING_LIB)
+    env = dict(os.environ, MSA_LIB=os.environ.get("MSA_TEST_LIB", TESTING_LIB))  # MSA_TEST_LIB: a variant build
     env.update({k: str(v) for k, v in hooks.items()})
     return env

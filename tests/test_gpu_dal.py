@@ -45,7 +45,13 @@ def test_dal_gradient_parity(cost, kernel):
     Jo, go = oracle.dal_gradient(_oracle_params(I, sp), od, eps, I.astype(np.float64), v, mu)
     assert J == pytest.approx(Jo, rel=1e-5)
     scale = np.max(np.abs(go), axis=0)
-    assert np.all(np.abs(g - go) <= 2e-3 * scale + 1e-9), (np.max(np.abs(g - go) / scale))
+    err = float(np.max(np.abs(g - go) / scale))
+    print(f"dal gradient cost={cost} kernel={kernel}: max |g - g_oracle| / column max = {err:.2e}")
+    # The gradient is a sum over M = 12 Euler steps of <lambda^(m+1), dF/deps(c^(m))>: image-wide sums of
+    # products of the fp32 adjoint (M transposed-Jacobian stencil steps) with phi' factors. Measured on
+    # the B200: 1.4e-7, 2.0e-7 and 8.8e-7 of the column maximum for the three cases (fp32 rounding of
+    # the states and addends); the gate keeps about a 10x margin.
+    assert err <= 1e-5, err
 
 
 def test_dal_terminal_state_and_cost():
