@@ -38,11 +38,6 @@ constexpr int TW = 32, TH = MSA_CN_TH, NT = TW * TH;  // one pixel per thread
 #ifndef MSA_CN_OCC
 #define MSA_CN_OCC 2
 #endif
-// MSA_CN_TMA = 1: p, mu and I also arrive by TMA (with the c / cbar tiles, on one mbarrier), so a CTA
-// has all of its tile's input bytes in flight at once and steps 2-3 read shared memory only
-#ifndef MSA_CN_TMA
-#define MSA_CN_TMA 0
-#endif
 constexpr int CN_OCC = MSA_CN_OCC;
 // smem column of tile column 0 (>= R, box starts 16-byte aligned) and the c / cbar tile width
 template <int R>
@@ -67,19 +62,12 @@ struct CnMaps {
 template <int C, int R>
 struct CnSmem {
   static constexpr int CW = CnGeo<R>::CW;
-  static constexpr int PW = CW - CnGeo<R>::CX;  // p / mu box width (columns x0 - CX .. x0 + 31)
-  static constexpr int al(int n) { return (n + 31) / 32 * 32; }
   static constexpr int c_floats = C * (TH + 2 * R) * CW;
   static constexpr int q_floats = 2 * C * QH * QW;
-  static constexpr int u_floats = al(c_floats > q_floats ? c_floats : q_floats);
+  static constexpr int u_floats = ((c_floats > q_floats ? c_floats : q_floats) + 31) / 32 * 32;
   static constexpr int cb_off = u_floats;
   static constexpr int cb_floats = C * (TH + 2) * CW;
-  // MSA_CN_TMA: p, mu [2C][TH+1][PW] and I [C][TH][TW] tiles follow
-  static constexpr int p_off = cb_off + al(cb_floats);
-  static constexpr int mu_off = p_off + al(2 * C * QH * PW);
-  static constexpr int I_off = mu_off + al(2 * C * QH * PW);
-  static constexpr int total = MSA_CN_TMA ? I_off + al(C * TH * TW) : cb_off + cb_floats;
-  static constexpr size_t bytes = sizeof(float) * total;
+  static constexpr size_t bytes = sizeof(float) * (cb_off + cb_floats);
 };
 
 template <int C, int R, int KER>
@@ -106,20 +94,7 @@ __global__ void __launch_bounds__(NT, CN_OCC)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  constexpr int PW = S::PW;
-  float* sp = smem + S::p_off;    // MSA_CN_TMA: [2C][QH][PW] p, rows y0-1 .. y0+TH-1
-  float* smu = smem + S::mu_off;  // MSA_CN_TMA: [2C][QH][PW] mu
-  float* sI = smem + S::I_off;    // MSA_CN_TMA: [C][TH][TW] I
-  (void)sp; (void)smu; (void)sI;
   if (threadIdx.x == 0) {
-#if MSA_CN_TMA
-    mbar_expect_tx(&bar, (unsigned)(sizeof(float) * (C * SH * CW + C * BH * CW + 4 * C * QH * PW + C * TH * TW)));
-    tma_load3(sc, &tm.c, x0 - CX, ys - R, b * C, &bar);
-    tma_load3(scb, &tm.cb, x0 - CX, ys - 1, b * C, &bar);
-    tma_load3(sp, &tm.p, x0 - CX, ys - 1, b * 2 * C, &bar);
-    tma_load3(smu, &tm.mu, x0 - CX, ys - 1, b * 2 * C, &bar);
-    tma_load3(sI, &tm.I, x0, ys, b * C, &bar);
-#else
     mbar_expect_tx(&bar, (unsigned)(sizeof(float) * (C * SH * CW + C * BH * CW)));
     tma_load3(sc, &tm.c, x0 - CX, ys - R, b * C, &bar);
     tma_load3(scb, &tm.cb, x0 - CX, ys - 1, b * C, &bar);
@@ -128,7 +103,6 @@ __global__ void __launch_bounds__(NT, CN_OCC)
     tma_prefetch3(&tm.p, x0 - CX, ys - 1, b * 2 * C);
     tma_prefetch3(&tm.mu, x0 - CX, ys - 1, b * 2 * C);
     tma_prefetch3(&tm.I, x0, ys, b * C);
-#endif
   }
   mbar_wait(&bar, 0);
 
@@ -180,17 +154,10 @@ __global__ void __launch_bounds__(NT, CN_OCC)
       const float c0 = cbk[0];
       gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(cbk[1], c0), K.inv_hx) : 0.0f;
       gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(cbk[CW], c0), K.inv_hy) : 0.0f;
-#if MSA_CN_TMA
-      px[k] = sp[(k * QH + hy) * PW + CX + hx - 1];
-      py[k] = sp[((C + k) * QH + hy) * PW + CX + hx - 1];
-      mx[k] = smu[(k * QH + hy) * PW + CX + hx - 1];
-      my[k] = smu[((C + k) * QH + hy) * PW + CX + hx - 1];
-#else
       px[k] = __ldg(pp + k * g.plane);
       py[k] = __ldg(pp + (C + k) * g.plane);
       mx[k] = __ldg(mp + k * g.plane);
       my[k] = __ldg(mp + (C + k) * g.plane);
-#endif
     }
     msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
 #pragma unroll
@@ -212,11 +179,7 @@ __global__ void __launch_bounds__(NT, CN_OCC)
     if (y > 0) ay = __fsub_rn(ay, sq[((C + k) * QH + ty) * QW + tx + 1]);
     const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
     float cp, cbp;
-#if MSA_CN_TMA
-    msa_prox_extrap(K, chalf[k], d, sI[(k * TH + ty) * TW + tx], cp, cbp);
-#else
     msa_prox_extrap(K, chalf[k], d, __ldg(I + msa_idx(g, b, k, C, y, x)), cp, cbp);
-#endif
     c_out[msa_idx(g, b, k, C, y, x)] = cp;
     cb_out[msa_idx(g, b, k, C, y, x)] = cbp;
     p_out[msa_idx(g, b, k, 2 * C, y, x)] = qx0;
