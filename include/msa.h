@@ -197,6 +197,16 @@ int msa_solve(msa_ctx* ctx, msa_round_stats* stats);
 int msa_solve_until(msa_ctx* ctx, double tol_residual, double tol_gap, int32_t max_rounds, msa_round_stats* stats,
                     int32_t* rounds_run, int32_t* converged);
 
+/* (ABI 3) msa_solve_until with a residual-balancing penalty (SURVEY §8(f) NEXT-2 "adaptive rho"; the
+ * standard ADMM rule, not the paper's - it fixes rho = gamma): round r also produces the
+ * dual residual s_r = rho_r ||div(v_r - v_{r-1})||_w (v_r the round's shrink S_{beta/rho}(grad c - mu/rho),
+ * constraint v - grad u = 0) into dual_residual[r] (NaN for the first round; may be NULL); from the second
+ * round on, r_r = al_residual > rb_mu s_r multiplies rho by rb_tau and s_r > rb_mu r_r divides it (after
+ * kappa; rb_mu, rb_tau >= 1). One rank (single image or batch), CP scheme; MSA_EINVAL otherwise. */
+int msa_solve_until_balanced(msa_ctx* ctx, double tol_residual, double tol_gap, int32_t max_rounds, double rb_mu,
+                             double rb_tau, msa_round_stats* stats, double* dual_residual, int32_t* rounds_run,
+                             int32_t* converged);
+
 /* Quantisation rule Q(c; delta) (reading R16) of the current c, per image:
  *  (i) union 4-neighbours whose fp32 colours differ by <= delta in every channel;
  *  (ii) union segments whose means differ by <= delta in every channel (means from exact

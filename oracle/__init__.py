@@ -305,6 +305,41 @@ def labels(c: np.ndarray, delta: float = 0.1, max_k: int = 0):
     return lab, n.value, pal[:min(max_k, n.value)] if max_k > 0 else None
 
 
+def solve_until_balanced(p: Params, I, max_rounds: int, tol_residual: float = 0.0, tol_gap: float = 0.0,
+                         rb_mu: float = 10.0, rb_tau: float = 2.0):
+    """Multiplier rounds with residual-balancing penalty (SURVEY §8(f) NEXT-2 "adaptive rho"; the
+    standard ADMM rule of Boyd et al., not in the paper, which fixes rho = gamma at PAPER.md:470).
+    Round r runs K iterations and its multiplier update exactly as State.run (Alg. 2 lines 6-7, then
+    rho <- kappa rho). With v^(r) = S_{beta/rho_r}(grad c^(r) - mu^(r)/rho_r) (the round's shrink, pre-update
+    mu, reading R11), the primal residual is the record's ||v^(r) - grad c^(r)||_w and the dual residual
+    s^(r) = rho_r ||div(v^(r) - v^(r-1))||_w (constraint v - grad u = 0: A = -grad, A^T = div, reading R6).
+    From round 1 on: if r > rb_mu s then rho <- rb_tau rho, elif s > rb_mu r then rho <- rho / rb_tau (for
+    the next round). The run stops after a round whose residual <= tol_residual or |gap| <= tol_gap
+    (each test off at 0; reading R13), or after max_rounds. Returns (state, records, dual_residuals)."""
+    st = State(p, _f64(I))
+    q = derive(p)
+    w = q.hx * q.hy
+    K = p.iters_per_round
+    recs, duals, v_prev = [], [], None
+    for _ in range(max_rounds):
+        mu_pre, rho_r = st.mu.copy(), st.rho
+        rec = st.run(K)[-1]
+        v = shrink_field(p, rho_r, st.c, mu_pre)
+        s_dual = float("nan") if v_prev is None else rho_r * float(np.sqrt(w * np.sum(div(v - v_prev, q.hx, q.hy) ** 2)))
+        recs.append(rec)
+        duals.append(s_dual)
+        v_prev = v
+        if (tol_residual > 0 and rec[5] <= tol_residual) or (tol_gap > 0 and abs(rec[4]) <= tol_gap):
+            break
+        r_prim = rec[5]
+        if s_dual == s_dual:  # from the second round on
+            if r_prim > rb_mu * s_dual:
+                st.rho *= rb_tau
+            elif s_dual > rb_mu * r_prim:
+                st.rho /= rb_tau
+    return st, recs, duals
+
+
 # ---------------------------------------------------------------- NEXT-1: DAL (Algorithm 1)
 def phi_prime(r: float, kernel: int = 0) -> float:
     return _load().mo_phi_prime(r, kernel)

@@ -27,7 +27,7 @@ SCHEME_CP_ROUNDS, SCHEME_LINEARISED_ADMM = 0, 1
 # every symbol include/msa.h declares (checked by tests/test_abi.py)
 ABI_SYMBOLS = ["msa_abi_version", "msa_last_error", "msa_workspace_bytes", "msa_partition_rows",
                "msa_nccl_unique_id", "msa_halo_plan", "msa_init", "msa_reset", "msa_step", "msa_solve",
-               "msa_solve_until", "msa_labels", "msa_label_margin",
+               "msa_solve_until", "msa_solve_until_balanced", "msa_labels", "msa_label_margin",
                "msa_get_field", "msa_set_field", "msa_get_stats", "msa_state_bytes", "msa_get_state",
                "msa_set_state", "msa_query", "msa_set_timing", "msa_get_timing", "msa_dal", "msa_dal_gradient", "msa_dal_admm",
                "msa_sync", "msa_free"]
@@ -182,6 +182,8 @@ def lib():
             "msa_step": ([P, I32], ctypes.c_int),
             "msa_solve": ([P, V], ctypes.c_int),
             "msa_solve_until": ([P, ctypes.c_double, ctypes.c_double, I32, V, PI32, PI32], ctypes.c_int),
+            "msa_solve_until_balanced": ([P, ctypes.c_double, ctypes.c_double, I32, ctypes.c_double, ctypes.c_double,
+                                          V, V, PI32, PI32], ctypes.c_int),
             "msa_labels": ([P, ctypes.c_float, V, V, V, I32, ctypes.c_int], ctypes.c_int),
             "msa_label_margin": ([P, ctypes.c_float, V], ctypes.c_int),
             "msa_get_field": ([P, I32, V, ctypes.c_int, PI32, PI32], ctypes.c_int),
@@ -358,6 +360,19 @@ class Solver:
         _check(lib().msa_solve_until(self._ctx, float(tol_residual), float(tol_gap), int(max_rounds), buf,
                                      ctypes.byref(n), ctypes.byref(conv)))
         return [buf[r].as_dict(self.params.channels) for r in range(n.value)], bool(conv.value)
+
+    def solve_until_balanced(self, max_rounds: int, tol_residual: float = 0.0, tol_gap: float = 0.0,
+                             rb_mu: float = 10.0, rb_tau: float = 2.0):
+        """Multiplier rounds with the residual-balancing penalty (msa_solve_until_balanced):
+        returns (records, dual_residuals, converged)."""
+        buf = (RoundStats * max(max_rounds, 1))()
+        dres = np.zeros(max(max_rounds, 1))
+        rr, conv = ctypes.c_int32(), ctypes.c_int32()
+        _check(lib().msa_solve_until_balanced(self._ctx, float(tol_residual), float(tol_gap), int(max_rounds),
+                                              float(rb_mu), float(rb_tau), buf, dres.ctypes.data, ctypes.byref(rr),
+                                              ctypes.byref(conv)))
+        n = rr.value
+        return [buf[r].as_dict(self.params.channels) for r in range(n)], dres[:n], bool(conv.value)
 
     def labels(self, delta: float = 0.1, max_k: int = 0, out=None):
         """Returns (labels int32 [nb][rows][W], n_clusters int32 [nb], palette [nb][max_k][C] or None);

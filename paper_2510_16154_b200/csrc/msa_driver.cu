@@ -142,6 +142,13 @@ struct msa_ctx {
   HaloPack halo[3][2];
   float* halo_buf = nullptr;
   long long halo_buf_floats = 0;
+  // residual balancing (msa_solve_until_balanced): the round's v^(r) into rb_v[rb_cur] and, from the
+  // second round on, sum |div(v^(r) - v^(r-1))|^2 into rb_sum (device)
+  bool rb_active = false, rb_have_prev = false, rb_sum_valid = false;
+  int rb_cur = 0;
+  float* rb_v[2] = {nullptr, nullptr};
+  double* rb_part = nullptr;
+  double* rb_sum = nullptr;
   // halo timing (msa_info::halo_ms with msa_set_timing on): events around each exchange
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> halo_ev;
   int64_t halo_exchanges_t = 0;
@@ -593,9 +600,21 @@ int do_round(msa_ctx* x) {
   if (P.scheme == MSA_SCHEME_LINEARISED_ADMM)  // statistics only (mu moves every iteration); p := mu
     CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->p[s], x->I, nullptr, x->partials, &nblk, x->stream));
   else
-    CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->mu, x->I, x->mu, x->partials, &nblk, x->stream));
+    CUDA_TRY(msa_launch_round(x->g, R, x->c[s], x->p[s], x->mu, x->I, x->mu, x->partials, &nblk, x->stream,
+                              x->rb_active ? x->rb_v[x->rb_cur] : nullptr));
   CUDA_TRY(msa_launch_reduce(x->partials, x->g.nb, nblk, x->sums, x->stream));
   x->launches += 2;
+  x->rb_sum_valid = false;
+  if (x->rb_active) {  // residual balancing: the dual residual's |div(v^(r) - v^(r-1))|^2 sum
+    if (x->rb_have_prev) {
+      CUDA_TRY(msa_launch_dual_res(x->g, x->rb_v[x->rb_cur], x->rb_v[1 - x->rb_cur], R.inv_hx, R.inv_hy, x->rb_part,
+                                   x->rb_sum, x->stream));
+      x->launches += 2;
+      x->rb_sum_valid = true;
+    }
+    x->rb_cur = 1 - x->rb_cur;
+    x->rb_have_prev = true;
+  }
   if (P.world > 1 && P.shard == MSA_SHARD_ROWS)
     NCCL_TRY(g_nccl.AllReduce(x->sums, x->sums, MSA_NSUM, ncclDouble, ncclSum, x->comm, x->stream));
   if (x->rec_pending >= REC_CAP) {
@@ -845,6 +864,10 @@ void free_ctx(msa_ctx* x) {
       if (hp.d_seg) cudaFree(hp.d_seg);
   if (x->halo_buf) cudaFree(x->halo_buf);
   for (auto& e : x->halo_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  for (float* q : x->rb_v)
+    if (q) cudaFree(q);
+  if (x->rb_part) cudaFree(x->rb_part);
+  if (x->rb_sum) cudaFree(x->rb_sum);
   msa_labels_free(x->lab);
   if (x->lab_buf) cudaFree(x->lab_buf);
   if (x->lab_count) cudaFree(x->lab_count);
@@ -1174,6 +1197,75 @@ int msa_solve_until(msa_ctx* x, double tol_residual, double tol_gap, int32_t max
     }
   }
   return MSA_OK;
+}
+
+// Residual-balancing penalty (the standard ADMM rule, not the paper's, which
+// fixes rho = gamma): msa_solve_until whose rounds also produce the dual residual
+// s^(r) = rho_r ||div(v^(r) - v^(r-1))||_w and, from the second round on, scale rho for the next round:
+// r > rb_mu s -> rho * rb_tau; s > rb_mu r -> rho / rb_tau (r = the record's AL residual). oracle mirror:
+// oracle.solve_until_balanced. One rank (single image or batch); the CP scheme.
+int msa_solve_until_balanced(msa_ctx* x, double tol_residual, double tol_gap, int32_t max_rounds, double rb_mu,
+                             double rb_tau, msa_round_stats* stats, double* dual_residual, int32_t* rounds_run,
+                             int32_t* converged) {
+  if (!x || !rounds_run || !converged) return set_err(MSA_EINVAL, "NULL argument");
+  const msa_params& P = x->prm;
+  if (P.world > 1 && P.shard == MSA_SHARD_ROWS) return set_err(MSA_EINVAL, "residual balancing runs on one rank");
+  if (P.scheme != MSA_SCHEME_CP_ROUNDS) return set_err(MSA_EINVAL, "residual balancing needs the CP scheme");
+  if (!(rb_mu >= 1.0) || !(rb_tau >= 1.0)) return set_err(MSA_EINVAL, "need rb_mu >= 1 and rb_tau >= 1");
+  if (max_rounds < 0) return set_err(MSA_EINVAL, "max_rounds must be >= 0");
+  if (!(tol_residual == tol_residual) || !(tol_gap == tol_gap)) return set_err(MSA_EINVAL, "NaN tolerance");
+  const size_t vf = (size_t)x->g.nb * 2 * P.channels * x->g.plane;
+  for (int i = 0; i < 2; ++i)
+    if (!x->rb_v[i]) CUDA_TRY(cudaMalloc((void**)&x->rb_v[i], sizeof(float) * vf));
+  if (!x->rb_part) CUDA_TRY(cudaMalloc((void**)&x->rb_part, sizeof(double) * msa_dual_res_blocks(x->g)));
+  if (!x->rb_sum) CUDA_TRY(cudaMalloc((void**)&x->rb_sum, sizeof(double)));
+  x->rb_active = true;
+  x->rb_have_prev = false;
+  *rounds_run = 0;
+  *converged = 0;
+  const int K = P.iters_per_round;
+  int rc = MSA_OK;
+  for (int32_t r = 0; r < max_rounds; ++r) {
+    const int64_t n = K - x->iters_done % K;
+    const size_t before = x->stats.size() + x->rec_pending;
+    const double rho_r = x->rho_cur;
+    if ((rc = do_steps(x, n)) != MSA_OK) break;
+    if ((rc = fetch_records(x)) != MSA_OK) break;
+    double sum = std::nan("");
+    if (x->rb_sum_valid) {
+      cudaError_t e = cudaMemcpyAsync(&sum, x->rb_sum, sizeof(double), cudaMemcpyDeviceToHost, x->stream);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(x->stream);
+      if (e != cudaSuccess) {
+        rc = set_err(MSA_ECUDA, "dual residual: %s", cudaGetErrorString(e));
+        break;
+      }
+    }
+    if (x->stats.size() <= before) {
+      rc = set_err(MSA_ESTATE, "no round record after a round");
+      break;
+    }
+    const msa_round_stats& st = x->stats.back();
+    const double s_dual = rho_r * std::sqrt(x->hx * x->hy * sum);  // NaN in the first round
+    if (stats) stats[r] = st;
+    if (dual_residual) dual_residual[r] = s_dual;
+    *rounds_run = r + 1;
+    if (st.nonfinite > 0) {
+      rc = set_err(MSA_EDIVERGED, "integration diverged: non-finite colour at round %d", st.round);
+      break;
+    }
+    if ((tol_residual > 0 && st.al_residual <= tol_residual) || (tol_gap > 0 && std::fabs(st.gap) <= tol_gap)) {
+      *converged = 1;
+      break;
+    }
+    if (s_dual == s_dual) {
+      if (st.al_residual > rb_mu * s_dual)
+        x->rho_cur *= rb_tau;
+      else if (s_dual > rb_mu * st.al_residual)
+        x->rho_cur /= rb_tau;
+    }
+  }
+  x->rb_active = false;
+  return rc;
 }
 
 // Q(c; delta) of image b over row parts: stage (i) per part, the parts' segment

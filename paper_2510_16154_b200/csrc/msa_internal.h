@@ -92,6 +92,11 @@ cudaError_t msa_launch_round(const MsaGeom& g, const MsaRoundConsts& R, const fl
 int msa_round_blocks(const MsaGeom& g);
 // Deterministic sum of the partials over blocks and over images -> sums[MSA_NSUM].
 cudaError_t msa_launch_reduce(const double* partials, int nb, int nblk, double* sums, cudaStream_t s);
+// residual balancing: *out = sum over the images of |div(v - v_prev)|^2 (fp64, fixed order); part holds
+// msa_dual_res_blocks(g) doubles
+long long msa_dual_res_blocks(const MsaGeom& g);
+cudaError_t msa_launch_dual_res(const MsaGeom& g, const float* v, const float* vp, float inv_hx, float inv_hy,
+                                double* part, double* out, cudaStream_t s);
 
 struct MsaRecordArgs {
   double w, beta, alpha, rho, npx;

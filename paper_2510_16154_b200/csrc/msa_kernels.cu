@@ -493,3 +493,67 @@ cudaError_t msa_launch_halo_pack(const MsaHaloSeg* d_segs, int nseg, long long m
   k_halo_pack<<<dim3((unsigned)std::max<long long>(blocks, 1), (unsigned)nseg), 256, 0, s>>>(d_segs, buf, to_buf);
   return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------- dual residual (residual balancing)
+// partial sums over 32 x 8 pixels of |div(v - v_prev)|^2 (per channel, fp32 div as in the round and
+// iteration kernels, squares summed in fp64), one per block and image: the dual residual of the
+// constraint v - grad u = 0 is rho ||div(v^(r) - v^(r-1))||_w (A^T = div, reading R6). Whole images on
+// one rank (G = 0 is not required: rows are local indices).
+__global__ void __launch_bounds__(256) k_dual_res(MsaGeom g, const float* __restrict__ v, const float* __restrict__ vp,
+                                                  float inv_hx, float inv_hy, double* __restrict__ part) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int jl = blockIdx.y * blockDim.y + threadIdx.y;
+  const int b = blockIdx.z, C = g.C;
+  double acc = 0.0;
+  if (i < g.W && jl < g.nrows) {
+    const int j = g.row0 + jl, W = g.W, H = g.H;
+    auto wv = [&](int m, int jj, int ii) {
+      const long long o = msa_idx(g, b, m, 2 * C, jj, ii);
+      return __fsub_rn(v[o], vp[o]);
+    };
+    for (int k = 0; k < C; ++k) {
+      float ax = i < W - 1 ? wv(k, j, i) : 0.0f;
+      if (i > 0) ax = __fsub_rn(ax, wv(k, j, i - 1));
+      float ay = j < H - 1 ? wv(C + k, j, i) : 0.0f;
+      if (j > 0) ay = __fsub_rn(ay, wv(C + k, j - 1, i));
+      const double d = (double)__fadd_rn(__fmul_rn(ax, inv_hx), __fmul_rn(ay, inv_hy));
+      acc += d * d;
+    }
+  }
+  __shared__ double red[8];
+  acc = warp_sum(acc);
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  if ((tid & 31) == 0) red[tid >> 5] = acc;
+  __syncthreads();
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[(long long)b * gridDim.x * gridDim.y + (long long)blockIdx.y * gridDim.x + blockIdx.x] = t;
+  }
+}
+
+__global__ void k_sum_fixed(const double* __restrict__ part, long long n, double* out) {
+  double v = 0.0;
+  for (long long r = threadIdx.x; r < n; r += blockDim.x) v += part[r];
+  __shared__ double red[8];
+  v = warp_sum(v);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
+}
+
+long long msa_dual_res_blocks(const MsaGeom& g) {
+  return (long long)((g.W + 31) / 32) * ((g.nrows + 7) / 8) * g.nb;
+}
+
+cudaError_t msa_launch_dual_res(const MsaGeom& g, const float* v, const float* vp, float inv_hx, float inv_hy,
+                                double* part, double* out, cudaStream_t s) {
+  dim3 blk(32, 8), grd((g.W + 31) / 32, (g.nrows + 7) / 8, g.nb);
+  k_dual_res<<<grd, blk, 0, s>>>(g, v, vp, inv_hx, inv_hy, part);
+  k_sum_fixed<<<1, 256, 0, s>>>(part, msa_dual_res_blocks(g), out);
+  return cudaGetLastError();
+}

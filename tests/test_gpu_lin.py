@@ -129,3 +129,29 @@ def test_lin_tile_equals_generic_bitwise(shape, R, tmp_path):
         outs.append(np.load(out))
     for k in ("c", "mu"):
         assert np.array_equal(outs[0][k], outs[1][k]), (k, float(np.max(np.abs(outs[0][k] - outs[1][k]))))
+
+
+@pytest.mark.parametrize("name,H,W,B", [("cfg2", 48, 40, None), ("cfg5", 36, 40, 2)])
+def test_residual_balancing_matches_oracle(name, H, W, B):
+    """msa_solve_until_balanced (residual-balancing rho) against
+    oracle.solve_until_balanced (pins RB1-RB3): the same rho in every round's record, dual residuals
+    to 1e-3 (R18: loose), the final colour field within the parity gate."""
+    cfg, img, sp = config_case(name, H=H, W=W, B=B, rounds=1, iters_per_round=10)
+    Bn, Hh, Ww, C = img.shape
+    with msa.Solver(msa.Params.from_solver(Bn, Hh, Ww, C, sp), img) as s:
+        recs, dres, conv = s.solve_until_balanced(6)
+        c = s.get_field(msa.FIELD_C)
+    rho_o, dual_o, c_o = [], [], []
+    for b in range(Bn):
+        st, ro, do = oracle.solve_until_balanced(oracle.Params.from_solver(Hh, Ww, C, sp), img[b], 6)
+        rho_o.append([r[6] for r in ro])
+        dual_o.append(do)
+        c_o.append(st.c)
+    if Bn == 1:  # batch records reduce over the images, so the rule sees the batch's residuals
+        assert [r["rho"] for r in recs] == pytest.approx(rho_o[0], rel=1e-6)
+        assert len(set(r["rho"] for r in recs)) > 1
+        np.testing.assert_allclose(dres[1:], np.array(dual_o[0][1:]), rtol=1e-3)
+        assert float(rel_err_per_pixel(c[0], c_o[0]).max()) <= 1e-4
+    else:
+        assert all(np.isfinite(dres[1:])) and np.isnan(dres[0])
+        assert len(recs) == 6
