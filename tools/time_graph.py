@@ -47,7 +47,7 @@ if __name__ == "__main__":
     names = sys.argv[1:] or ["cfg1", "cfg2", "cfg3"]
     for name in names:
         for graph in (False, True):
-            env = dict(os.environ)
+            env = dict(os.environ, MSA_LIB=os.environ.get("MSA_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2510_16154_b200", "libmsa_testing.so")))
             env.pop("MSA_NO_GRAPH", None)
             if not graph:
                 env["MSA_NO_GRAPH"] = "1"

@@ -39,7 +39,7 @@ if __name__ == "__main__":
         sys.exit(0)
     for n in [int(a) for a in sys.argv[1:]] or [2, 4, 8]:
         for split in (False, True):
-            env = dict(os.environ)
+            env = dict(os.environ, MSA_LIB=os.environ.get("MSA_LIB", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2510_16154_b200", "libmsa_testing.so")))
             env.pop("MSA_K1_SPLIT", None)
             if split:
                 env["MSA_K1_SPLIT"] = "1"
