@@ -16,6 +16,8 @@
 #include <cmath>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/msa.h"
 #include "msa_internal.h"
 
@@ -71,6 +73,7 @@ bool nccl_load() {
   LOADSYM(AllReduce, "ncclAllReduce");
   LOADSYM(AllGather, "ncclAllGather");
   LOADSYM(GetErrorString, "ncclGetErrorString");
+  LOADSYM(CommGetAsyncError, "ncclCommGetAsyncError");
 #undef LOADSYM
   g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.CommDestroy && g_nccl.Send && g_nccl.Recv &&
               g_nccl.GroupStart && g_nccl.GroupEnd && g_nccl.AllReduce && g_nccl.AllGather &&
@@ -82,6 +85,25 @@ bool nccl_load() {
     ncclResult_t r_ = (x);                                                                                     \
     if (r_ != ncclSuccess) return set_err(MSA_ENCCL, "%s failed: %s", #x, g_nccl.GetErrorString(r_));          \
   } while (0)
+
+// NVTX ranges around the ABI entry points, rounds and halo exchanges (visible in nsys / ncu timelines;
+// a push / pop pair each when no tool is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// rows mode: an NCCL error raised asynchronously (a peer failed, a network error) surfaces here after
+// the stream synchronisations of the blocking entry points (MSA_ENCCL instead of a later hang)
+int nccl_async_check(const void* comm) {
+  if (!comm || !g_nccl.CommGetAsyncError) return MSA_OK;
+  ncclResult_t a = ncclSuccess;
+  ncclResult_t r = g_nccl.CommGetAsyncError((ncclComm_t)comm, &a);
+  if (r != ncclSuccess) return set_err(MSA_ENCCL, "ncclCommGetAsyncError failed: %s", g_nccl.GetErrorString(r));
+  if (a != ncclSuccess && a != ncclInProgress)
+    return set_err(MSA_ENCCL, "asynchronous NCCL error: %s", g_nccl.GetErrorString(a));
+  return MSA_OK;
+}
 
 constexpr int REC_CAP = 1024;  // device-side round records pending a host fetch
 }  // namespace
@@ -545,6 +567,7 @@ int halo_exchange(msa_ctx* x, int phase, cudaStream_t st = nullptr) {
   if ((rc = build_halo_packs(x)) != MSA_OK) return rc;
   const int ph = phase == MSA_HALO_ITER ? 0 : (phase == MSA_HALO_ROUND ? 1 : 2);
   msa_ctx::HaloPack& hp = x->halo[ph][x->cur];
+  NvtxRange nv(phase == MSA_HALO_ITER ? "msa_halo_iter" : phase == MSA_HALO_ROUND ? "msa_halo_round" : "msa_halo_mu");
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (x->timing) {
     CUDA_TRY(cudaEventCreate(&e0));
@@ -576,6 +599,7 @@ int halo_exchange(msa_ctx* x, int phase, cudaStream_t st = nullptr) {
 
 // --- one multiplier round (steps 4-5) at the end of an iteration that completed a round
 int do_round(msa_ctx* x) {
+  NvtxRange nv("msa_round");
   const msa_params& P = x->prm;
   const int s = x->cur;
   int rc;
@@ -1140,12 +1164,14 @@ int msa_reset(msa_ctx* x, const float* image, int image_on_device) {
 }
 
 int msa_step(msa_ctx* x, int32_t n_iters) {
+  NvtxRange nv("msa_step");
   if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
   if (n_iters < 0) return set_err(MSA_EINVAL, "n_iters must be >= 0");
   return do_steps(x, n_iters);
 }
 
 int msa_solve(msa_ctx* x, msa_round_stats* stats) {
+  NvtxRange nv("msa_solve");
   if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
   const size_t before = x->stats.size() + x->rec_pending;
   const int64_t n = (int64_t)x->prm.rounds * x->prm.iters_per_round;
@@ -1157,6 +1183,7 @@ int msa_solve(msa_ctx* x, msa_round_stats* stats) {
   if (!graphed && (rc = do_steps(x, n)) != MSA_OK) return rc;
   if ((rc = fetch_records(x)) != MSA_OK) return rc;
   CUDA_TRY(cudaStreamSynchronize(x->stream));
+  if ((rc = nccl_async_check(x->comm)) != MSA_OK) return rc;
   for (size_t r = before; graphed && r < x->stats.size(); ++r) {
     x->stats[r].round += shift_round;
     x->stats[r].iters += shift_iters;
@@ -1172,6 +1199,7 @@ int msa_solve(msa_ctx* x, msa_round_stats* stats) {
 
 int msa_solve_until(msa_ctx* x, double tol_residual, double tol_gap, int32_t max_rounds, msa_round_stats* stats,
                     int32_t* rounds_run, int32_t* converged) {
+  NvtxRange nv("msa_solve_until");
   if (!x || !rounds_run || !converged) return set_err(MSA_EINVAL, "NULL argument");
   if (max_rounds < 0) return set_err(MSA_EINVAL, "max_rounds must be >= 0");
   if (!(tol_residual == tol_residual) || !(tol_gap == tol_gap)) return set_err(MSA_EINVAL, "NaN tolerance");
@@ -1186,6 +1214,7 @@ int msa_solve_until(msa_ctx* x, double tol_residual, double tol_gap, int32_t max
     if ((rc = do_steps(x, n)) != MSA_OK) return rc;
     if ((rc = fetch_records(x)) != MSA_OK) return rc;
     CUDA_TRY(cudaStreamSynchronize(x->stream));
+    if ((rc = nccl_async_check(x->comm)) != MSA_OK) return rc;
     if (x->stats.size() <= before) return set_err(MSA_ESTATE, "no round record after a round");
     const msa_round_stats& s = x->stats.back();
     if (stats) stats[r] = s;
@@ -1207,6 +1236,7 @@ int msa_solve_until(msa_ctx* x, double tol_residual, double tol_gap, int32_t max
 int msa_solve_until_balanced(msa_ctx* x, double tol_residual, double tol_gap, int32_t max_rounds, double rb_mu,
                              double rb_tau, msa_round_stats* stats, double* dual_residual, int32_t* rounds_run,
                              int32_t* converged) {
+  NvtxRange nv("msa_solve_until_balanced");
   if (!x || !rounds_run || !converged) return set_err(MSA_EINVAL, "NULL argument");
   const msa_params& P = x->prm;
   if (P.world > 1 && P.shard == MSA_SHARD_ROWS) return set_err(MSA_EINVAL, "residual balancing runs on one rank");
@@ -1446,6 +1476,7 @@ int msa_label_margin(msa_ctx* x, float delta, float* margin) {
 
 int msa_labels(msa_ctx* x, float delta, int32_t* labels, int32_t* n_clusters, float* palette, int32_t max_k,
                int out_on_device) {
+  NvtxRange nv("msa_labels");
   if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
   if (!(delta >= 0) || !isfinite(delta)) return set_err(MSA_EINVAL, "delta must be finite and >= 0");
   if (!labels || !n_clusters) return set_err(MSA_EINVAL, "labels and n_clusters must not be NULL");
@@ -1951,6 +1982,7 @@ int msa_dal_gradient(msa_ctx* x, const msa_dal_params* d, const double* eps, con
 
 int msa_dal(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, const float* mu, double* J_hist,
             double* sigma_hist, int32_t* stop) {
+  NvtxRange nv("msa_dal");
   int rc = dal_check(x, d);
   if (rc != MSA_OK) return rc;
   if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
@@ -1968,6 +2000,7 @@ int msa_dal(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, co
 // mu is left in the context (MSA_FIELD_MU). rho is fixed (kappa is not applied).
 int msa_dal_admm(msa_ctx* x, const msa_dal_params* d, double* eps, const float* v, const float* mu, int32_t outer,
                  double* J_hist, msa_round_stats* stats, double* gamma_hist) {
+  NvtxRange nv("msa_dal_admm");
   int rc = dal_check(x, d);
   if (rc != MSA_OK) return rc;
   if (!eps) return set_err(MSA_EINVAL, "eps is NULL");
@@ -2140,7 +2173,8 @@ int msa_dal_admm(msa_ctx* x, const msa_dal_params* d, double* eps, const float* 
 int msa_sync(msa_ctx* x) {
   if (!x) return set_err(MSA_EINVAL, "ctx is NULL");
   CUDA_TRY(cudaStreamSynchronize(x->stream));
-  return MSA_OK;
+  if (x->comm_stream) CUDA_TRY(cudaStreamSynchronize(x->comm_stream));
+  return nccl_async_check(x->comm);
 }
 
 int msa_free(msa_ctx* x) {

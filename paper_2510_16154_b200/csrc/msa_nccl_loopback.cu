@@ -240,6 +240,10 @@ ncclResult_t lb_all_gather(const void* send, void* recv, size_t count, ncclDataT
 }
 
 const char* lb_error_string(ncclResult_t r) { return r == ncclSuccess ? "success (loopback)" : "loopback error"; }
+ncclResult_t lb_async_error(ncclComm_t, ncclResult_t* r) {
+  *r = ncclSuccess;  // the in-process transport reports its errors synchronously
+  return ncclSuccess;
+}
 
 }  // namespace
 
@@ -255,5 +259,6 @@ MsaNcclFns msa_nccl_loopback() {
   f.AllReduce = lb_all_reduce;
   f.AllGather = lb_all_gather;
   f.GetErrorString = lb_error_string;
+  f.CommGetAsyncError = lb_async_error;
   return f;
 }
