@@ -52,6 +52,15 @@ def test_row_slabs_match_one_context(shape, R, worlds, extra):
         assert rep["worlds"][str(w)]["fields"] == "bitwise"
 
 
+def test_row_slabs_at_the_bench_geometry():
+    # the 8-GPU bench geometry of cfg4: 4096^2 RGB, R = 5, eight 512-row slabs (interior / boundary split,
+    # the packed halo exchange at full row width), against one context on the whole image
+    shape, R = (1, 4096, 4096, 3), 5
+    spec = dict(seed=11, shape=list(shape), worlds=[8], params=_params(shape[2], R, K=3, rounds=2))
+    rep = _run(spec)
+    assert rep["worlds"]["8"]["fields"] == "bitwise" and rep["worlds"]["8"]["labels"] == "identical"
+
+
 def test_row_slabs_serial_exchange_and_generic_kernel():
     # the exchange on the compute stream before each K1 (MSA_NO_OVERLAP), and the generic kernel
     shape, R = (1, 256, 64, 3), 5
