@@ -689,7 +689,7 @@ int k1_variant() {
 
 // Step 1 by the chunked large-support kernel (NEXT-3): radii beyond the tiled kernel's R <= 5, C <= 4
 bool uses_large_kernel(const msa_params& P) {
-  static const int large_from = MSA_HOOK("MSA_LARGE_FROM") ? atoi(MSA_HOOK("MSA_LARGE_FROM")) : 6;  // A/B hook
+  static const int large_from = msa_hook_int("MSA_LARGE_FROM", 6);  // A/B hook
   return P.radius >= large_from && P.radius > 5 && P.channels <= 4 && k1_variant() != K1_GENERIC;
 }
 
@@ -1482,7 +1482,7 @@ int msa_labels(msa_ctx* x, float delta, int32_t* labels, int32_t* n_clusters, fl
   if (!labels || !n_clusters) return set_err(MSA_EINVAL, "labels and n_clusters must not be NULL");
   if (max_k < 0 || (max_k > 0 && !palette)) return set_err(MSA_EINVAL, "palette needs max_k > 0 and a buffer");
   const bool dist = x->prm.world > 1 && x->prm.shard == MSA_SHARD_ROWS;
-  static const int test_parts = MSA_HOOK("MSA_LABELS_PARTS") ? atoi(MSA_HOOK("MSA_LABELS_PARTS")) : 0;  // test hook
+  static const int test_parts = msa_hook_int("MSA_LABELS_PARTS", 0);  // test hook
   const MsaGeom& g = x->g;
   const int nparts = dist ? x->prm.world : std::min(test_parts, g.H);
   if (dist) {  // stage (i) across the slab boundary needs the current c row above each slab

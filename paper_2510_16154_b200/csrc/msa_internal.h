@@ -12,6 +12,12 @@
 #else
 #define MSA_HOOK(name) ((const char*)nullptr)
 #endif
+// integer value of a test hook, or def when unset (always def in the product build)
+inline int msa_hook_int(const char* name, int def) {
+  const char* v = MSA_HOOK(name);
+  (void)name;
+  return v ? atoi(v) : def;
+}
 #include <cuda_runtime.h>
 #include <nccl.h>
 #include <stdint.h>

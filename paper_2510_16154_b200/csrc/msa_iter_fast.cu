@@ -216,7 +216,6 @@ __global__ void __launch_bounds__(NT, (Occ<C, P>::blocks))
   constexpr int TH = S::TH, SH = S::SH, BH = S::BH, QH = S::QH, SPH = S::SPH;
   extern __shared__ __align__(128) float smem[];
   float* sc = smem;               // [C][SH][SW]    c tile + halo (step 1)
-  float* sp = smem;               // [2C][SPH][SPW] p+ (steps 2-3; reuses the c tile)
   float* scb = smem + S::cb_off;  // [C][BH][BW]
   float* spp = smem + S::p_off;   // [2C][QH][QW]
   float* smu = smem + S::mu_off;  // [2C][QH][QW]
@@ -349,9 +348,9 @@ __global__ void __launch_bounds__(NT, (Occ<C, P>::blocks))
     }
     return;
   }
-  __syncthreads();  // every warp is done with the c tile (sp reuses it)
-
-  // ---- step 2: p+ at tile pixel (tx, ty) (tx in [-1, 31], ty in [-1, TH-1]) -> sp[.][ty+1][tx+1]
+  // ---- step 2: p+ at tile pixel (tx, ty) (tx in [-1, 31], ty in [-1, TH-1]), written in place over p
+  // (each point's p is read only by its own dual step). Step 2 does not depend on step 1 and touches
+  // no c-tile memory, so a warp goes on from its step 1 without waiting for the others.
   auto dual_at = [&](int tx, int ty) {
     const int xx = x0 + tx, yy = y0 + ty;
     if (xx < 0 || yy < 0 || xx >= W || yy >= H) return;
@@ -370,8 +369,8 @@ __global__ void __launch_bounds__(NT, (Occ<C, P>::blocks))
     msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
 #pragma unroll
     for (int k = 0; k < C; ++k) {
-      sp[(k * SPH + ty + 1) * SPW + tx + 1] = qx[k];
-      sp[((C + k) * SPH + ty + 1) * SPW + tx + 1] = qy[k];
+      spp[(k * QH + ty + 1) * QW + BX + tx] = qx[k];
+      spp[((C + k) * QH + ty + 1) * QW + BX + tx] = qy[k];
     }
   };
 #pragma unroll
@@ -380,23 +379,24 @@ __global__ void __launch_bounds__(NT, (Occ<C, P>::blocks))
   if (strip == 1 && lx < TH) dual_at(-1, lx);  // halo column x0-1
   __syncthreads();
 
-  // ---- step 3: div p+ (R6), prox fidelity, extrapolation (R21) -> output tiles in smem (the p,
-  // mu buffers are dead), then TMA tensor stores (clipped at the image / slab edges)
-  float* oc = spp;                 // [C][TH][TW] c+
-  float* ocb = spp + C * TH * TW;  // [C][TH][TW] cbar+
+  // ---- step 3: div p+ (R6), prox fidelity, extrapolation (R21) -> output tiles in smem (the c tile
+  // and mu buffers are dead), then TMA tensor stores (clipped at the image / slab edges)
+  float* oc = sc;                  // [C][TH][TW] c+
+  float* ocb = sc + C * TH * TW;   // [C][TH][TW] cbar+
   float* op = smu;                 // [2C][TH][TW] p+
+  static_assert(2 * C * TH * TW <= S::u_floats, "c+ / cbar+ staging fits the dead c tile");
   if (x < W) {
 #pragma unroll
     for (int r = 0; r < P; ++r) {
       const int ty = strip * P + r, yy = ybase + r;
-      const int sy = ty + 1, sx = lx + 1;
+      const int sy = ty + 1, sx = BX + lx;
 #pragma unroll
       for (int k = 0; k < C; ++k) {
-        const float qx0 = sp[(k * SPH + sy) * SPW + sx], qy0 = sp[((C + k) * SPH + sy) * SPW + sx];
+        const float qx0 = spp[(k * QH + sy) * QW + sx], qy0 = spp[((C + k) * QH + sy) * QW + sx];
         float ax = x < W - 1 ? qx0 : 0.0f;
-        if (x > 0) ax = __fsub_rn(ax, sp[(k * SPH + sy) * SPW + sx - 1]);
+        if (x > 0) ax = __fsub_rn(ax, spp[(k * QH + sy) * QW + sx - 1]);
         float ay = yy < H - 1 ? qy0 : 0.0f;
-        if (yy > 0) ay = __fsub_rn(ay, sp[((C + k) * SPH + sy - 1) * SPW + sx]);
+        if (yy > 0) ay = __fsub_rn(ay, spp[((C + k) * QH + sy - 1) * QW + sx]);
         const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
         float cp, cbp;
         msa_prox_extrap(K, chalf[r][k], d, sI[(k * TH + ty) * TW + lx], cp, cbp);
@@ -521,7 +521,7 @@ cudaError_t launch_cr(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
   }
   // P = 4 rows per thread (C <= 3); C = 4 takes P = 2 (the P = 4 tiles would need 145 KB of shared
   // memory, one CTA per SM). MSA_K1_P=2 / 4 forces the choice for C <= 3 (A/B hook).
-  static const int rows_per_thread = MSA_HOOK("MSA_K1_P") ? atoi(MSA_HOOK("MSA_K1_P")) : 0;
+  static const int rows_per_thread = msa_hook_int("MSA_K1_P", 0);
   if constexpr (C == 4) {
     return launch_rp<C, R, 2, LIN>(g, K, om, c, cb, p, mu, I, co, cbo, po, s);
   } else {

@@ -508,7 +508,7 @@ SweepPlan make_plan(const MsaGeom& g, int BS, int slots) {
   pl.jfirst = g.row0 / P;
   pl.jend = (g.row0 + g.nrows - 1) / P + 1;
   const int nch = pl.jend - pl.jfirst;
-  static const int force_seg = MSA_HOOK("MSA_SWEEP_SEG") ? atoi(MSA_HOOK("MSA_SWEEP_SEG")) : 0;  // test hook (chunks)
+  static const int force_seg = msa_hook_int("MSA_SWEEP_SEG", 0);  // test hook (chunks)
   long long best = -1;
   int best_s = 1;
   for (int s = 1; s <= nch; ++s) {
