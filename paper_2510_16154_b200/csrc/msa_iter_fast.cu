@@ -254,9 +254,43 @@ __global__ void __launch_bounds__(NT, (Occ<C, P>::blocks))
     }
     tma_load3(sI, &tm.I, x0, ys, b * C, &bars[1]);
   }
-  mbar_wait(&bars[0], 0);
   asm volatile("griddepcontrol.launch_dependents;");  // the next iteration may start launching
 
+  // ---- step 2 (defined here, run after step 1; running it first, while the c tile lands, measured
+  // 0.664 vs 0.648 ms at cfg4): p+ at tile pixel
+  // (tx, ty) (tx in [-1, 31], ty in [-1, TH-1]), written in place over p (each point's p is read only by
+  // its own dual step). Step 2 does not depend on step 1 and touches no c-tile memory, so no CTA barrier
+  // separates them.
+  auto dual_phase = [&]() {
+    auto dual_at = [&](int tx, int ty) {
+      const int xx = x0 + tx, yy = y0 + ty;
+      if (xx < 0 || yy < 0 || xx >= W || yy >= H) return;
+      float gx[C], gy[C], px[C], py[C], mx[C], my[C], qx[C], qy[C];
+  #pragma unroll
+      for (int k = 0; k < C; ++k) {
+        const float* cbk = scb + (k * BH + ty + 1) * BW + BX + tx;
+        const float c0 = cbk[0];
+        gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(cbk[1], c0), K.inv_hx) : 0.0f;
+        gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(cbk[BW], c0), K.inv_hy) : 0.0f;
+        px[k] = spp[(k * QH + ty + 1) * QW + BX + tx];
+        py[k] = spp[((C + k) * QH + ty + 1) * QW + BX + tx];
+        mx[k] = smu[(k * QH + ty + 1) * QW + BX + tx];
+        my[k] = smu[((C + k) * QH + ty + 1) * QW + BX + tx];
+      }
+      msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
+  #pragma unroll
+      for (int k = 0; k < C; ++k) {
+        spp[(k * QH + ty + 1) * QW + BX + tx] = qx[k];
+        spp[((C + k) * QH + ty + 1) * QW + BX + tx] = qy[k];
+      }
+    };
+  #pragma unroll
+    for (int r = 0; r < P; ++r) dual_at(lx, strip * P + r);
+    if (strip == 0) dual_at(lx, -1);             // halo row y0-1
+    if (strip == 1 && lx < TH) dual_at(-1, lx);  // halo column x0-1
+
+  };
+  mbar_wait(&bars[0], 0);
   // ---- step 1: agent Euler step for P rows (P/2 packed pixel pairs) of column x
   f2 ci[P / 2][C], acc[P / 2][C];
 #pragma unroll
@@ -348,35 +382,7 @@ __global__ void __launch_bounds__(NT, (Occ<C, P>::blocks))
     }
     return;
   }
-  // ---- step 2: p+ at tile pixel (tx, ty) (tx in [-1, 31], ty in [-1, TH-1]), written in place over p
-  // (each point's p is read only by its own dual step). Step 2 does not depend on step 1 and touches
-  // no c-tile memory, so a warp goes on from its step 1 without waiting for the others.
-  auto dual_at = [&](int tx, int ty) {
-    const int xx = x0 + tx, yy = y0 + ty;
-    if (xx < 0 || yy < 0 || xx >= W || yy >= H) return;
-    float gx[C], gy[C], px[C], py[C], mx[C], my[C], qx[C], qy[C];
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const float* cbk = scb + (k * BH + ty + 1) * BW + BX + tx;
-      const float c0 = cbk[0];
-      gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(cbk[1], c0), K.inv_hx) : 0.0f;
-      gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(cbk[BW], c0), K.inv_hy) : 0.0f;
-      px[k] = spp[(k * QH + ty + 1) * QW + BX + tx];
-      py[k] = spp[((C + k) * QH + ty + 1) * QW + BX + tx];
-      mx[k] = smu[(k * QH + ty + 1) * QW + BX + tx];
-      my[k] = smu[((C + k) * QH + ty + 1) * QW + BX + tx];
-    }
-    msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
-#pragma unroll
-    for (int k = 0; k < C; ++k) {
-      spp[(k * QH + ty + 1) * QW + BX + tx] = qx[k];
-      spp[((C + k) * QH + ty + 1) * QW + BX + tx] = qy[k];
-    }
-  };
-#pragma unroll
-  for (int r = 0; r < P; ++r) dual_at(lx, strip * P + r);
-  if (strip == 0) dual_at(lx, -1);             // halo row y0-1
-  if (strip == 1 && lx < TH) dual_at(-1, lx);  // halo column x0-1
+  dual_phase();
   __syncthreads();
 
   // ---- step 3: div p+ (R6), prox fidelity, extrapolation (R21) -> output tiles in smem (the c tile
