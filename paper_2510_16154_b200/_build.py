@@ -18,6 +18,7 @@ TEST_LIB = os.path.join(PKG, "libmsa_testing.so")
 SOURCES = ["msa_driver.cu", "msa_kernels.cu", "msa_iter_fast.cu", "msa_iter_cn.cu", "msa_agent_large.cu", "msa_dal.cu",
            "msa_labels.cu"]
 TEST_SOURCES = SOURCES + ["msa_iter_sweep.cu", "msa_nccl_loopback.cu"]
+FILE_FLAGS: dict[str, list[str]] = {}  # per-file nvcc flags (none at present)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"),
@@ -54,7 +55,7 @@ def _build_one(force, verbose, defines, lib, build_dir, flags, sources) -> str:
 
     def compile_one(src: str) -> str:
         obj = os.path.join(build_dir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *ARCH, *FLAGS, *FILE_FLAGS.get(src, []), *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

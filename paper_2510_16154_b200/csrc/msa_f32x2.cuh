@@ -32,6 +32,23 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
   asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
   return d;
 }
+// a + b per lane by two scalar add.rn.f32: ptxas contracts mul.rn.f32x2 followed by add.rn.f32x2 into
+// FFMA2 (one rounding fewer) even under --fmad=false, but leaves scalar add.rn alone. Use it wherever a
+// packed sum of products must round like the scalar code (__fadd_rn(__fmul_rn(..), ..)).
+__device__ __forceinline__ f2 add2_nc(f2 a, f2 b) {
+  float a0, a1, b0, b1;
+  upk(a, a0, a1);
+  upk(b, b0, b1);
+  return pk(__fadd_rn(a0, b0), __fadd_rn(a1, b1));
+}
+
+// fma with the result clamped to [0, 1] (FFMA.SAT; no f32x2 form exists)
+__device__ __forceinline__ float fma_sat(float a, float b, float c) {
+  float d;
+  asm("fma.rn.sat.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 __device__ __forceinline__ f2 relu2(f2 v) {
   float a, b;
   upk(v, a, b);

@@ -24,11 +24,13 @@
 #include <mutex>
 
 #include "msa_internal.h"
+#include "msa_f32x2.cuh"
 #include "msa_tma.cuh"
 
 namespace {
 
 using namespace msa_tma;
+using namespace msa_f32x2;
 
 
 #ifndef MSA_CN_TH
@@ -107,22 +109,48 @@ __global__ void __launch_bounds__(NT, CN_OCC)
   mbar_wait(&bar, 0);
 
   const int y = y0 + ty;
-  // ---- step 1: agent Euler step (the driver's offset order, msa_agent_term_s - the scaled form:
-  // bitwise equal to the generic kernel)
-  float chalf[C];
+  // Channels travel in pairs (2j, 2j+1) through packed f32x2 arithmetic (FADD2/FFMA2/FMUL2: half the
+  // arithmetic instructions of the one-channel form; the kernel is issue-bound at C = 16). Per channel
+  // the operations and their order are those of msa_agent_term_s / msa_dual_step / msa_prox_extrap,
+  // so results stay bitwise equal to the generic kernel (sums of products add per lane, add2_nc: ptxas
+  // would contract mul.rn.f32x2 + add.rn.f32x2 into FFMA2). Odd C: the last pair's second lane is a
+  // dummy zero.
+  constexpr int NP = (C + 1) / 2;
+  auto ldp = [](const float* q, int j, int stride) -> f2 {  // channels 2j, 2j+1 of planes `stride` apart
+    return pk(q[2 * j * stride], 2 * j + 1 < C ? q[(2 * j + 1) * stride] : 0.0f);
+  };
+  auto ln = [](const f2 (&v)[NP], int k) -> float {  // channel k
+    float a, b;
+    upk(v[k >> 1], a, b);
+    return (k & 1) ? b : a;
+  };
+  // ---- step 1: agent Euler step (the driver's offset order, msa_agent_term_s - the scaled form,
+  // its clamp t = max(-s, 0) as FFMA.SAT: equal for e_c >= 1, the launcher's condition)
+  f2 chalf[NP];
   {
-    float ci[C], acc[C];
+    f2 ci[NP], acc[NP];
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-      ci[k] = sc[(k * SH + ty + R) * CW + CX + tx];
-      acc[k] = 0.0f;
+    for (int j = 0; j < NP; ++j) {
+      ci[j] = ldp(sc + (ty + R) * CW + CX + tx, j, SH * CW);
+      acc[j] = pk(0.0f, 0.0f);
     }
+    const float qc = KER == 0 ? 5.0f : 3.0f;
     auto term = [&](int o) {
       const float* src = sc + (ty + R + T.dy[o]) * CW + CX + tx + T.dx[o];
-      float cj[C];
+      f2 d[NP];
 #pragma unroll
-      for (int k = 0; k < C; ++k) cj[k] = src[k * SH * CW];
-      msa_agent_term_s<C, KER>(ci, cj, T.om[o], K.m4, acc);
+      for (int j = 0; j < NP; ++j) d[j] = sub2(ldp(src, j, SH * CW), ci[j]);
+      float sq = __fmaf_rn(ln(d, 0), ln(d, 0), T.om[o]);
+#pragma unroll
+      for (int k = 1; k < C - 1; ++k) sq = __fmaf_rn(ln(d, k), ln(d, k), sq);
+      const float dl = ln(d, C - 1);
+      const float t = fma_sat(-dl, dl, -sq);
+      const float t2 = __fmul_rn(t, t);
+      const float t4 = __fmul_rn(t2, t2);
+      const float w = __fmul_rn(t4, __fmaf_rn(K.m4, t, qc));
+      const f2 w2 = pk(w, w);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) acc[j] = fma2(w2, d[j], acc[j]);
     };
     if (x0 - R >= 0 && x0 + TW + R <= W && y0 - R >= 0 && y0 + TH + R <= H) {  // interior tile
 #pragma unroll 4
@@ -134,56 +162,94 @@ __global__ void __launch_bounds__(NT, CN_OCC)
         term(o);
       }
     }
+    const f2 DT = pk(K.dt_s, K.dt_s);
 #pragma unroll
-    for (int k = 0; k < C; ++k) chalf[k] = __fmaf_rn(K.dt_s, acc[k], ci[k]);
+    for (int j = 0; j < NP; ++j) chalf[j] = fma2(DT, acc[j], ci[j]);
   }
   __syncthreads();  // the c tile is dead: sq reuses it
 
+  const f2 IHX = pk(K.inv_hx, K.inv_hx), IHY = pk(K.inv_hy, K.inv_hy);
   // ---- step 2: p+ at tile coordinates (hx - 1, hy - 1), hx < 33, hy < TH + 1
-  for (int idx = threadIdx.x; idx < QW * QH; idx += NT) {
-    const int hy = idx / QW, hx = idx - hy * QW;
-    const int xx = x0 + hx - 1, yy = y0 + hy - 1;
-    if (xx < 0 || yy < 0 || xx >= W || yy >= H) continue;  // never read (div masks those terms)
-    float gx[C], gy[C], px[C], py[C], mx[C], my[C], qx[C], qy[C];
-    const long long o0 = msa_idx(g, b, 0, 2 * C, yy, xx);
-    const float* pp = p + o0;
-    const float* mp = mu + o0;
+  {
+    const f2 SIG = pk(K.sigma, K.sigma), ARS = pk(K.a_rs, K.a_rs), NBRS = pk(-K.b_rs, -K.b_rs);
+    for (int idx = threadIdx.x; idx < QW * QH; idx += NT) {
+      const int hy = idx / QW, hx = idx - hy * QW;
+      const int xx = x0 + hx - 1, yy = y0 + hy - 1;
+      if (xx < 0 || yy < 0 || xx >= W || yy >= H) continue;  // never read (div masks those terms)
+      f2 qx[NP], qy[NP];
+      const long long o0 = msa_idx(g, b, 0, 2 * C, yy, xx);
+      const float* pp = p + o0;
+      const float* mp = mu + o0;
+      const long long pl = g.plane;
+      auto ldgp = [&](const float* q, int j) -> f2 {
+        return pk(__ldg(q + 2 * j * pl), 2 * j + 1 < C ? __ldg(q + (2 * j + 1) * pl) : 0.0f);
+      };
+      const float* cbk = scb + hy * CW + CX + hx - 1;
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-      const float* cbk = scb + (k * BH + hy) * CW + CX + hx - 1;
-      const float c0 = cbk[0];
-      gx[k] = xx < W - 1 ? __fmul_rn(__fsub_rn(cbk[1], c0), K.inv_hx) : 0.0f;
-      gy[k] = yy < H - 1 ? __fmul_rn(__fsub_rn(cbk[CW], c0), K.inv_hy) : 0.0f;
-      px[k] = __ldg(pp + k * g.plane);
-      py[k] = __ldg(pp + (C + k) * g.plane);
-      mx[k] = __ldg(mp + k * g.plane);
-      my[k] = __ldg(mp + (C + k) * g.plane);
-    }
-    msa_dual_step<C>(K, gx, gy, px, py, mx, my, qx, qy);
+      for (int j = 0; j < NP; ++j) {
+        const f2 c0 = ldp(cbk, j, BH * CW);
+        const f2 gx = xx < W - 1 ? mul2(sub2(ldp(cbk + 1, j, BH * CW), c0), IHX) : pk(0.0f, 0.0f);
+        const f2 gy = yy < H - 1 ? mul2(sub2(ldp(cbk + CW, j, BH * CW), c0), IHY) : pk(0.0f, 0.0f);
+        qx[j] = fma2(ARS, fma2(SIG, gx, ldgp(pp, j)), mul2(NBRS, ldgp(mp, j)));
+        qy[j] = fma2(ARS, fma2(SIG, gy, ldgp(pp + C * pl, j)), mul2(NBRS, ldgp(mp + C * pl, j)));
+      }
+      float n2 = 0.0f;
 #pragma unroll
-    for (int k = 0; k < C; ++k) {
-      sq[(k * QH + hy) * QW + hx] = qx[k];
-      sq[((C + k) * QH + hy) * QW + hx] = qy[k];
+      for (int k = 0; k < C; ++k) {
+        n2 = __fmaf_rn(ln(qx, k), ln(qx, k), n2);
+        n2 = __fmaf_rn(ln(qy, k), ln(qy, k), n2);
+      }
+      // beta / |q| via the hardware reciprocal square root (R21); inside the ball q * 1 = q exactly
+      const float f = n2 > K.beta2 ? __fmul_rn(K.beta, rsqrtf(n2)) : 1.0f;
+      const f2 F = pk(f, f);
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        qx[j] = mul2(qx[j], F);
+        qy[j] = mul2(qy[j], F);
+      }
+#pragma unroll
+      for (int k = 0; k < C; ++k) {
+        sq[(k * QH + hy) * QW + hx] = ln(qx, k);
+        sq[((C + k) * QH + hy) * QW + hx] = ln(qy, k);
+      }
     }
   }
   __syncthreads();
 
   // ---- step 3: div p+ (R6), prox fidelity, extrapolation (R21), coalesced stores
   if (x >= W || y >= g.row0 + g.nrows) return;
+  const f2 TAU = pk(K.tau, K.tau), TA = pk(K.tau_alpha, K.tau_alpha), INV = pk(K.inv_1ta, K.inv_1ta);
+  const f2 THE = pk(K.theta, K.theta), Z = pk(0.0f, 0.0f);
+  const float* sqx = sq + (ty + 1) * QW + tx + 1;   // px+ at (x, y), channel stride QH * QW
+  const float* sqy = sqx + C * QH * QW;             // py+ at (x, y)
 #pragma unroll
-  for (int k = 0; k < C; ++k) {
-    const float qx0 = sq[(k * QH + ty + 1) * QW + tx + 1], qy0 = sq[((C + k) * QH + ty + 1) * QW + tx + 1];
-    float ax = x < W - 1 ? qx0 : 0.0f;
-    if (x > 0) ax = __fsub_rn(ax, sq[(k * QH + ty + 1) * QW + tx]);
-    float ay = y < H - 1 ? qy0 : 0.0f;
-    if (y > 0) ay = __fsub_rn(ay, sq[((C + k) * QH + ty) * QW + tx + 1]);
-    const float d = __fadd_rn(__fmul_rn(ax, K.inv_hx), __fmul_rn(ay, K.inv_hy));
-    float cp, cbp;
-    msa_prox_extrap(K, chalf[k], d, __ldg(I + msa_idx(g, b, k, C, y, x)), cp, cbp);
-    c_out[msa_idx(g, b, k, C, y, x)] = cp;
-    cb_out[msa_idx(g, b, k, C, y, x)] = cbp;
-    p_out[msa_idx(g, b, k, 2 * C, y, x)] = qx0;
-    p_out[msa_idx(g, b, C + k, 2 * C, y, x)] = qy0;
+  for (int j = 0; j < NP; ++j) {
+    const f2 qx0 = ldp(sqx, j, QH * QW), qy0 = ldp(sqy, j, QH * QW);
+    f2 ax = x < W - 1 ? qx0 : Z;
+    if (x > 0) ax = sub2(ax, ldp(sqx - 1, j, QH * QW));
+    f2 ay = y < H - 1 ? qy0 : Z;
+    if (y > 0) ay = sub2(ay, ldp(sqy - QW, j, QH * QW));
+    const f2 d = add2_nc(mul2(ax, IHX), mul2(ay, IHY));
+    const long long oi = msa_idx(g, b, 2 * j, C, y, x);
+    const f2 Iv = pk(__ldg(I + oi), 2 * j + 1 < C ? __ldg(I + oi + g.plane) : 0.0f);
+    const f2 ch = chalf[j];
+    const f2 inc = fma2(TAU, d, mul2(TA, sub2(Iv, ch)));
+    const f2 cp = add2_nc(ch, mul2(inc, INV));
+    const f2 cbp = fma2(THE, sub2(cp, ch), cp);
+    float a, bb;
+    upk(cp, a, bb);
+    c_out[oi] = a;
+    if (2 * j + 1 < C) c_out[oi + g.plane] = bb;
+    upk(cbp, a, bb);
+    cb_out[oi] = a;
+    if (2 * j + 1 < C) cb_out[oi + g.plane] = bb;
+    const long long op = msa_idx(g, b, 2 * j, 2 * C, y, x);
+    upk(qx0, a, bb);
+    p_out[op] = a;
+    if (2 * j + 1 < C) p_out[op + g.plane] = bb;
+    upk(qy0, a, bb);
+    p_out[op + C * g.plane] = a;
+    if (2 * j + 1 < C) p_out[op + (C + 1) * g.plane] = bb;
   }
 }
 
@@ -401,7 +467,9 @@ cudaError_t launch_cn(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
                       const float* cb, const float* p, const float* mu, const float* I, float* c_out, float* cb_out,
                       float* p_out, cudaStream_t s, int* launched) {
   *launched = 0;
-  if (g.C < 5 || g.C > 16 || R < 1 || R > 5 || T.n > CN_MAXOFF || !K.scaled) return cudaErrorNotSupported;
+  // scaled form with e_c >= 1 only (the saturating clamp of step 1)
+  if (g.C < 5 || g.C > 16 || R < 1 || R > 5 || T.n > CN_MAXOFF || !K.scaled || !(K.e_c >= 1.0f))
+    return cudaErrorNotSupported;
   CnOffsets off;
   off.n = T.n;
   for (int o = 0; o < T.n; ++o) {

@@ -120,10 +120,20 @@ __device__ __forceinline__ void column_pass_m(const float* __restrict__ s, const
       f2 d[C];
 #pragma unroll
       for (int k = 0; k < C; ++k) d[k] = sub2(Cp[q][k], ci[j][k]);
-      f2 sq = fma2(d[0], d[0], OM);  // |d|^2 - om/e_c (scaled form, msa_agent_term_s)
+      // t = max(-(|d|^2 + nom), 0) (scaled form, msa_agent_term_s) as clamp(-(d_last^2 + s), 0, 1) by
+      // two FFMA.SAT: equal while t <= om/e_c <= 1, i.e. e_c >= 1 (the launcher's condition; the paper's
+      // control box E = [2, 1100]^2 has eps_c >= 2). One issue slot and two FMNMX fewer per pair of
+      // pixels than FFMA2 + FMNMX x2, and a shorter dependency chain.
+      f2 sq = C == 1 ? OM : fma2(d[0], d[0], OM);
 #pragma unroll
-      for (int k = 1; k < C; ++k) sq = fma2(d[k], d[k], sq);
-      const f2 t = relu2n(sq);
+      for (int k = 1; k < C - 1; ++k) sq = fma2(d[k], d[k], sq);
+      f2 t;
+      {
+        float da, db, sa, sb;
+        upk(d[C - 1], da, db);
+        upk(sq, sa, sb);
+        t = pk(fma_sat(-da, da, -sa), fma_sat(-db, db, -sb));
+      }
       const f2 t2 = mul2(t, t);
       const f2 t4 = mul2(t2, t2);
       const f2 qv = fma2(M4, t, QC);
@@ -553,7 +563,8 @@ cudaError_t launch_fast(const MsaGeom& g, const MsaIterConsts& K, const MsaOffse
   *launched = 0;
   // test hook: MSA_FORCE_GENERIC=1 selects the generic kernel (bitwise-identical results)
   static const bool force_generic = MSA_HOOK("MSA_FORCE_GENERIC") != nullptr;
-  if (g.C < 1 || g.C > 4 || force_generic || !K.scaled) return cudaErrorNotSupported;  // scaled form only
+  // scaled form with e_c >= 1 only (the saturating clamp of step 1, column_pass_m)
+  if (g.C < 1 || g.C > 4 || force_generic || !K.scaled || !(K.e_c >= 1.0f)) return cudaErrorNotSupported;
   // every active offset must lie in the interior disc (true for eps_x >= the default)
   for (int o = 0; o < T.n; ++o)
     if (T.dx[o] * T.dx[o] + T.dy[o] * T.dy[o] >= R * R) return cudaErrorNotSupported;
