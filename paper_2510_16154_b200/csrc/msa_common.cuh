@@ -86,15 +86,31 @@ __device__ __forceinline__ void msa_agent_term(const float (&ci)[C], const float
 
 // The same term in the scaled form (MsaIterConsts::scaled): nom = -om/e_c, m4 = -4 e_c;
 // acc accumulates phi / e_c^4 (d), the caller applies dt_s = dt/N_R e_c^4.
+// |d|^2 + nom: one fma chain for C <= 4; for C >= 5 two interleaved partial sums (even channels from
+// nom, odd channels from 0) added at the end - the order of the channel-pair kernel (msa_iter_cn.cu),
+// whose packed FFMA2 chain carries both sums at once.
 template <int C, int KER>
 __device__ __forceinline__ void msa_agent_term_s(const float (&ci)[C], const float (&cj)[C], float nom, float m4,
                                                  float (&acc)[C]) {
   float d[C];
 #pragma unroll
   for (int k = 0; k < C; ++k) d[k] = __fsub_rn(cj[k], ci[k]);
-  float s = __fmaf_rn(d[0], d[0], nom);
+  float s;
+  if constexpr (C >= 5) {
+    float se = __fmaf_rn(d[0], d[0], nom), so = __fmul_rn(d[1], d[1]);
 #pragma unroll
-  for (int k = 1; k < C; ++k) s = __fmaf_rn(d[k], d[k], s);
+    for (int k = 2; k < C; ++k) {
+      if (k & 1)
+        so = __fmaf_rn(d[k], d[k], so);
+      else
+        se = __fmaf_rn(d[k], d[k], se);
+    }
+    s = __fadd_rn(se, so);
+  } else {
+    s = __fmaf_rn(d[0], d[0], nom);
+#pragma unroll
+    for (int k = 1; k < C; ++k) s = __fmaf_rn(d[k], d[k], s);
+  }
   const float t = fmaxf(-s, 0.0f);
   const float t2 = __fmul_rn(t, t);
   const float t4 = __fmul_rn(t2, t2);

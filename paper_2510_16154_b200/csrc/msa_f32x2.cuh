@@ -49,6 +49,13 @@ __device__ __forceinline__ float fma_sat(float a, float b, float c) {
   return d;
 }
 
+// a + b clamped to [0, 1] (FADD.SAT)
+__device__ __forceinline__ float add_sat(float a, float b) {
+  float d;
+  asm("add.rn.sat.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b));
+  return d;
+}
+
 __device__ __forceinline__ f2 relu2(f2 v) {
   float a, b;
   upk(v, a, b);

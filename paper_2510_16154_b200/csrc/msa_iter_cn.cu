@@ -55,6 +55,7 @@ struct CnOffsets {
   int n;
   signed char dx[CN_MAXOFF], dy[CN_MAXOFF];
   float om[CN_MAXOFF];
+  float2 om0[CN_MAXOFF];  // (om, 0): the two starting values of the packed |d|^2 chain (one uniform pair)
 };
 struct CnMaps {
   CUtensorMap c, cb;
@@ -140,11 +141,14 @@ __global__ void __launch_bounds__(NT, CN_OCC)
       f2 d[NP];
 #pragma unroll
       for (int j = 0; j < NP; ++j) d[j] = sub2(ldp(src, j, SH * CW), ci[j]);
-      float sq = __fmaf_rn(ln(d, 0), ln(d, 0), T.om[o]);
+      // |d|^2 + nom as msa_agent_term_s orders it for C >= 5: lane 0 sums the even channels from nom,
+      // lane 1 the odd ones from 0 (fma(d1, d1, 0) rounds as d1 * d1; an odd C's dummy lane adds 0)
+      f2 S = fma2(d[0], d[0], *reinterpret_cast<const f2*>(&T.om0[o]));
 #pragma unroll
-      for (int k = 1; k < C - 1; ++k) sq = __fmaf_rn(ln(d, k), ln(d, k), sq);
-      const float dl = ln(d, C - 1);
-      const float t = fma_sat(-dl, dl, -sq);
+      for (int j = 1; j < NP; ++j) S = fma2(d[j], d[j], S);
+      float se, so;
+      upk(S, se, so);
+      const float t = add_sat(-se, -so);
       const float t2 = __fmul_rn(t, t);
       const float t4 = __fmul_rn(t2, t2);
       const float w = __fmul_rn(t4, __fmaf_rn(K.m4, t, qc));
@@ -477,6 +481,7 @@ cudaError_t launch_cn(const MsaGeom& g, const MsaIterConsts& K, const MsaOffsetT
     off.dx[o] = (signed char)T.dx[o];
     off.dy[o] = (signed char)T.dy[o];
     off.om[o] = T.oms[o];
+    off.om0[o] = make_float2(T.oms[o], 0.0f);
   }
   CnKey key;
   memset(&key, 0, sizeof(key));
