@@ -52,7 +52,9 @@ CASES = [
 # many-channel tiled kernel (msa_iter_cn.cu, C = 16): same contract, bitwise equal to the generic one
 CN_CASES = [((2, 40, 36, 16), 3, 0), ((1, 33, 70, 16), 4, 1), ((1, 9, 5, 16), 2, 0), ((1, 64, 64, 16), 1, 0),
             ((1, 40, 36, 5), 3, 0), ((2, 33, 41, 8), 4, 1), ((1, 50, 64, 12), 2, 0), ((1, 17, 90, 7), 3, 0),
-            ((1, 45, 70, 16), 5, 0), ((1, 37, 29, 6), 5, 1)]
+            ((1, 45, 70, 16), 5, 0), ((1, 37, 29, 6), 5, 1),
+            # more tiles (10 x 26 x 2 = 520) than persistent CTAs (2 x 148): each CTA walks several tiles
+            ((2, 203, 290, 16), 3, 0)]
 # the tiled kernel for grey (the paper's images), two-channel and RGBA fields (C = 1, 2, 4)
 C_CASES = [((1, 64, 32, 1), 5, 0), ((2, 70, 45, 1), 3, 1), ((1, 37, 29, 2), 4, 0), ((1, 100, 66, 2), 5, 0),
            ((1, 48, 40, 4), 5, 0), ((2, 33, 70, 4), 2, 1), ((1, 1, 50, 1), 2, 0)]
