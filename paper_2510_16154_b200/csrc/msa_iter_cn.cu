@@ -37,10 +37,17 @@ using namespace msa_f32x2;
 #define MSA_CN_TH 8
 #endif
 constexpr int TW = 32, TH = MSA_CN_TH, NT = TW * TH;  // one pixel per thread
-#ifndef MSA_CN_OCC
-#define MSA_CN_OCC 2
+// CTAs per SM the launch bounds ask for. C = 16 (config 5) fits 3 (80 registers, no spills; 61 KB of
+// shared memory each at R <= 4): 4.94-4.98 vs 5.05-5.10 ms at cfg5 (profiles/README.md); the other
+// channel counts and the linearised kernel spill at 3 and keep 2.
+template <int C, bool LIN>
+struct CnOcc {
+#ifdef MSA_CN_OCC
+  static constexpr int v = MSA_CN_OCC;
+#else
+  static constexpr int v = (!LIN && C == 16) ? 3 : 2;
 #endif
-constexpr int CN_OCC = MSA_CN_OCC;
+};
 // smem column of tile column 0 (>= R, box starts 16-byte aligned) and the c / cbar tile width
 template <int R>
 struct CnGeo {
@@ -74,7 +81,7 @@ struct CnSmem {
 };
 
 template <int C, int R, int KER>
-__global__ void __launch_bounds__(NT, CN_OCC)
+__global__ void __launch_bounds__(NT, (CnOcc<C, false>::v))
     k_iter_cn(MsaGeom g, MsaIterConsts K, const __grid_constant__ CnOffsets T, const __grid_constant__ CnMaps tm,
               const float* __restrict__ p, const float* __restrict__ mu, const float* __restrict__ I,
               float* __restrict__ c_out, float* __restrict__ cb_out, float* __restrict__ p_out) {
@@ -271,7 +278,7 @@ struct CnSmemLin {
 };
 
 template <int C, int R, int KER>
-__global__ void __launch_bounds__(NT, CN_OCC)
+__global__ void __launch_bounds__(NT, (CnOcc<C, true>::v))
     k_iter_cn_lin(MsaGeom g, MsaIterConsts K, const __grid_constant__ CnOffsets T, const __grid_constant__ CnMaps tm,
                   const float* __restrict__ mu, const float* __restrict__ I, float* __restrict__ c_out,
                   float* __restrict__ mu_out) {
