@@ -53,6 +53,8 @@ template <int R>
 struct CnGeo {
   static constexpr int CX = R <= 4 ? 4 : 8;
   static constexpr int CW = TW + 2 * CX;  // 40 or 48
+  // TMA box starts x0 - CX must be 16-byte-aligned global addresses (an 8-byte-aligned start faults)
+  static_assert(CX % 4 == 0 && TW % 4 == 0, "TMA box starts must be 16-byte aligned");
 };
 constexpr int QW = TW + 1;      // p+ tile: columns x0-1 .. x0+31
 constexpr int QH = TH + 1;      // rows y0-1 .. y0+7

@@ -51,6 +51,9 @@ constexpr int NT = 32 * NSTRIP;
 constexpr int SX = 8;            // smem column of tile column 0 in the c tile (>= R, 16-byte aligned)
 constexpr int SW = TW + 2 * SX;  // 48
 constexpr int BX = 4;            // smem column of tile column 0 in the cbar / p / mu tiles
+// TMA box starts x0 - SX, x0 - BX must be 16-byte-aligned global addresses (an 8-byte-aligned start
+// faults with an illegal instruction on sm_100a, profiles/README.md round 2)
+static_assert(SX % 4 == 0 && BX % 4 == 0 && TW % 4 == 0, "TMA box starts must be 16-byte aligned");
 constexpr int BW = 40;           // cbar: global columns x0-4 .. x0+35
 constexpr int QW = 36;           // p, mu: columns x0-4 .. x0+31
 constexpr int SPW = TW + 1;      // p+ tile with the low-side halo
