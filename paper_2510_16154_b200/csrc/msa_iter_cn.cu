@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(NT, (CnOcc<C, false>::v))
   float* sc = smem;             // [C][SH][CW] c tile (step 1)
   float* sq = smem;             // [2C][QH][QW] p+ (steps 2-3, reuses the c tile)
   float* scb = smem + S::cb_off;  // [C][BH][CW] cbar rows y0-1 .. y0+TH
-  __shared__ __align__(8) unsigned long long bar;
+  __shared__ __align__(8) unsigned long long bar[2];  // 0: c tile (step 1); 1: cbar tile (step 2)
 
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int x0 = blockIdx.x * TW, y0 = g.row0 + g.k1_lo + blockIdx.y * TH, b = blockIdx.z;
@@ -102,21 +102,23 @@ __global__ void __launch_bounds__(NT, (CnOcc<C, false>::v))
   const int x = x0 + tx;
   const int ys = y0 - g.row0 + g.G;  // stored row of y0
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    mbar_expect_tx(&bar, (unsigned)(sizeof(float) * (C * SH * CW + C * BH * CW)));
-    tma_load3(sc, &tm.c, x0 - CX, ys - R, b * C, &bar);
-    tma_load3(scb, &tm.cb, x0 - CX, ys - 1, b * C, &bar);
+  if (threadIdx.x == 0) {  // step 1 waits for the c tile only; cbar lands while it runs
+    mbar_expect_tx(&bar[0], (unsigned)(sizeof(float) * C * SH * CW));
+    tma_load3(sc, &tm.c, x0 - CX, ys - R, b * C, &bar[0]);
+    mbar_expect_tx(&bar[1], (unsigned)(sizeof(float) * C * BH * CW));
+    tma_load3(scb, &tm.cb, x0 - CX, ys - 1, b * C, &bar[1]);
     // steps 2-3 read p, mu (tile + low-side halo) and I straight from global memory: pull them
     // into L2 now, so those loads wait for L2 rather than HBM after step 1
     tma_prefetch3(&tm.p, x0 - CX, ys - 1, b * 2 * C);
     tma_prefetch3(&tm.mu, x0 - CX, ys - 1, b * 2 * C);
     tma_prefetch3(&tm.I, x0, ys, b * C);
   }
-  mbar_wait(&bar, 0);
+  mbar_wait(&bar[0], 0);
 
   const int y = y0 + ty;
   // Channels travel in pairs (2j, 2j+1) through packed f32x2 arithmetic (FADD2/FFMA2/FMUL2: half the
@@ -180,6 +182,7 @@ __global__ void __launch_bounds__(NT, (CnOcc<C, false>::v))
     for (int j = 0; j < NP; ++j) chalf[j] = fma2(DT, acc[j], ci[j]);
   }
   __syncthreads();  // the c tile is dead: sq reuses it
+  mbar_wait(&bar[1], 0);
 
   const f2 IHX = pk(K.inv_hx, K.inv_hx), IHY = pk(K.inv_hy, K.inv_hy);
   // ---- step 2: p+ at tile coordinates (hx - 1, hy - 1), hx < 33, hy < TH + 1
