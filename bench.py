@@ -379,7 +379,7 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32",
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (seeded generator synth/, BASELINE config 4 recipe)",
             "config": _config(cfg, world),
             # north_star's metric: the fraction of measured HBM bandwidth (algorithmic bytes); the FP32
